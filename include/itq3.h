@@ -1,0 +1,128 @@
+/*
+ * libitq3 -- C ABI of the B200-native ITQ3_S hot path.
+ *
+ * Plain pointers and sizes only (no torch / numpy types).  Every entry point
+ *   * takes a cudaStream_t (passed as void*; NULL = legacy default stream),
+ *   * is stream-ordered, does NO hidden host synchronisation and never frees
+ *     or allocates caller memory (the caller owns every buffer),
+ *   * returns ITQ3_OK or an ITQ3_E_* code whose classes mirror the reference's
+ *     exception taxonomy (reference: pkg/src/itq3/errors.py:16-59); the detail
+ *     string is available from itq3_last_error() on the calling thread.
+ * Device-side data errors (corrupt planes, NaN scales) are reported through a
+ * caller-owned device word written by itq3_validate, read back when the caller
+ * synchronises -- the library itself never blocks.
+ *
+ * Payload = the container's block array exactly as write_container emits it
+ * (codec.py:222-235): n_blocks x block_nbytes(block_n, ss) bytes, each block =
+ * 3 bit planes (3n/8 B) | scale f16 LE | zero-point f16 LE [| 8 x sub-scale f16 LE].
+ * "Tiled" = the device-resident GEMV/MMQ layout produced by itq3_repack_tiled
+ * (2-bit codes in mma-fragment order, 66 B per 256 weights).
+ */
+#ifndef ITQ3_H
+#define ITQ3_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum itq3_status {
+    ITQ3_OK = 0,
+    ITQ3_E_LENGTH = 1,      /* LengthError    errors.py:16-19 */
+    ITQ3_E_DOMAIN = 2,      /* DomainError    errors.py:22-25 */
+    ITQ3_E_SHAPE = 3,       /* ShapeError     errors.py:28-31 */
+    ITQ3_E_CORRUPT = 4,     /* CorruptionError errors.py:34-37 */
+    ITQ3_E_UNSUPPORTED = 8, /* layout has no kernel here (caller routes elsewhere) */
+    ITQ3_E_CUDA = 16        /* launch / runtime failure */
+};
+
+enum itq3_dtype { ITQ3_F32 = 0, ITQ3_F64 = 1, ITQ3_BF16 = 2, ITQ3_F16 = 3 };
+
+/* ScalePolicy.kind (quantizer.py:33-49) */
+enum itq3_policy { ITQ3_POLICY_CONSTANT = 0, ITQ3_POLICY_ARGMIN = 1, ITQ3_POLICY_MEAN_ABS = 2 };
+
+/* itq3_validate check mask bits and the error kinds packed in the first-bad key */
+enum itq3_check {
+    ITQ3_CHECK_PLANES = 1,    /* stored code > 2 (packing.py:80-83)            kind 0 */
+    ITQ3_CHECK_SCALE_NAN = 2, /* scale is NaN (packing.py:185-186)             kind 1 */
+    ITQ3_CHECK_ZP = 4,        /* zero-point not in {-1,0,1} (packing.py:187-189) kind 2 */
+    ITQ3_CHECK_SUB_NAN = 8,   /* sub-scale NaN (packing.py:193-195)            kind 3 */
+    ITQ3_CHECK_ZP_FINITE = 16 /* zero-point non-finite: int() would raise       kind 4 */
+};
+
+const char* itq3_version(void);
+const char* itq3_last_error(void);
+int itq3_sm_count(void);
+
+/* ---- K1 encoder: replaces quantize_tensor / encode_block (codec.py:113-189) ----
+ * w: numel values (f32 or f64, row-major flattened); the tail of the last block
+ * is zero-padded as codec.py:173-179 does.  Writes n_blocks*block_nbytes bytes.
+ * Bit-exact with the reference (fp64, numpy pairwise summation order). */
+int itq3_encode(const void* w, int w_dtype, int64_t numel, int block_n, int sub_scales, int policy,
+                double coeff, int symmetric, uint8_t* payload, void* stream);
+
+/* ---- K7 validation: replaces the per-block checks of deserialize_block /
+ * unpack_ternary (packing.py:67-84,171-197).  *d_first_bad (device u64) must be
+ * preset to UINT64_MAX; receives min over offenders of
+ * (block << 16) | (kind << 10) | index. */
+int itq3_validate(const uint8_t* payload, int64_t n_blocks, int block_n, int sub_scales, uint32_t check_mask,
+                  unsigned long long* d_first_bad, void* stream);
+
+/* ---- K2 dequantiser: replaces dequantize_tensor / decode_block (codec.py:152-202).
+ * out: numel values (F64 = bit-exact with the reference, F32 = exact value cast). */
+int itq3_dequant(const uint8_t* payload, int64_t n_blocks, int block_n, int sub_scales, int64_t numel, void* out,
+                 int out_dtype, void* stream);
+
+/* ---- transform: fwht_forward / fwht_inverse (transform.py:61-96) on n_vec
+ * contiguous vectors of length n (2..512, power of two), dtype F32 or F64,
+ * bit-identical to numpy's butterfly order.  normalize=0 skips the 1/sqrt(n). */
+int itq3_fwht(const void* in, void* out, int dtype, int64_t n_vec, int n, int normalize, void* stream);
+
+/* ---- fast layout (block_n = 256, variant s, cols % 256 == 0) ---- */
+int64_t itq3_tiled_nbytes(int64_t rows, int64_t cols, int asymmetric);
+int itq3_repack_tiled(const uint8_t* payload, int64_t rows, int64_t cols, int asymmetric, uint8_t* tiled,
+                      void* stream);
+
+/* ---- K3 activation rotation: x'_b = H_256 x_b per 256-block of K, quantised to
+ * `limbs` signed-byte limbs (fixed point, per (block, token) power-of-two scale)
+ * in mma-fragment order.  x element (k, m) at x[k*stride_k + m*stride_m]. */
+int64_t itq3_act_nbytes(int64_t cols, int64_t m, int limbs);
+int itq3_rotate_act(const void* x, int x_dtype, int64_t cols, int64_t m, int64_t stride_k, int64_t stride_m,
+                    int limbs, uint8_t* act, void* stream);
+
+/* ---- K4 fused GEMV / small-M matmul (replaces fused_matvec / fused_matmul,
+ * compute.py:98-133) on the tiled layout:  y[r, m] = sum_k w_hat[r, k] x[k, m].
+ * y element (r, m) at y[r*stride_r + m*stride_m]; y_dtype F32 (fp32 accumulate)
+ * or F64 (fp64 accumulate, parity mode). */
+int itq3_gemv(const uint8_t* tiled, int64_t rows, int64_t cols, int asymmetric, const uint8_t* act, int64_t m,
+              int limbs, void* y, int y_dtype, int64_t stride_r, int64_t stride_m, void* stream);
+
+/* ---- generic fused matmul for every other layout (any block_n, variant ss,
+ * row-straddling blocks): fp64 exact decode + fp64 dot, deterministic block order.
+ * X (cols x k) fp64 at X[c*stride_c + j*stride_j]; Y (rows x k) fp64 row-major.
+ * workspace: itq3_generic_ws_nbytes(...) bytes. */
+int64_t itq3_generic_ws_nbytes(int64_t rows, int64_t cols, int block_n, int64_t k);
+int itq3_matmul_generic(const uint8_t* payload, int64_t rows, int64_t cols, int block_n, int sub_scales,
+                        const double* X, int64_t k, int64_t stride_c, int64_t stride_j, double* Y, void* workspace,
+                        void* stream);
+
+/* ---- packing utilities: pack_ternary / unpack_ternary (packing.py:43-84) on n_rows rows
+ * of n codes (n % 8 == 0, n <= 512).  *d_bad (device u64, preset UINT64_MAX) receives
+ * (row << 16) | index of the first out-of-range code (pack) or
+ * (row << 16) | (code << 12) | index of the first stored code > 2 (unpack). */
+int itq3_pack_codes(const int8_t* codes, int64_t n_rows, int n, uint8_t* planes, unsigned long long* d_bad,
+                    void* stream);
+int itq3_unpack_codes(const uint8_t* planes, int64_t n_rows, int n, int8_t* codes, unsigned long long* d_bad,
+                      void* stream);
+
+/* ---- scalar binary16 codec (host): encode_f16 / decode_f16 (packing.py:87-109) */
+uint16_t itq3_f16_encode(double x);
+double itq3_f16_decode(uint16_t bits);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ITQ3_H */

@@ -1,0 +1,89 @@
+"""Fused decode-and-multiply paths of the drop-in API (compute.py:98-133 of the reference).
+
+Two modes, chosen by the operand type:
+  * numpy / array-like X  -> parity mode: float64 result equal to the reference's
+    ``fused_matmul`` within its own tolerance (test_compute.py:66-103, rtol 1e-5): the
+    rotated activations carry 6 fixed-point limbs (48 bits) and blocks accumulate in fp64.
+  * CUDA torch tensor X   -> perf mode: float32 result (float64 if X is float64); 3 limbs
+    (24-bit activations) at M = 1 and 2 limbs (16-bit) for M > 1, fp32 accumulation.
+Both run the same kernels: K3 ``itq3_rotate_act`` + K4 ``itq3_gemv`` on the tiled layout
+(block_n 256, variant s, cols % 256 == 0), else the generic fp64 kernel
+``itq3_matmul_generic`` (any block size / variant / row-straddling blocks).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .codec import QuantizedTensor
+from .errors import DomainError, ShapeError
+
+PARITY_LIMBS = 6
+
+
+def perf_limbs(m: int) -> int:
+    return 3 if m == 1 else 2
+
+
+def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, limbs: int) -> torch.Tensor:
+    """Y (rows x k) = w_hat @ X for a CUDA X (cols x k, any strides)."""
+    dev = X.device
+    rows, cols = q.rows, q.cols
+    k = X.shape[1]
+    if q.fast_layout():
+        tiled = q.tiled()
+        act = torch.empty(_lib.load().itq3_act_nbytes(cols, k, limbs), dtype=torch.uint8, device=dev)
+        xcode = _lib.TORCH_DTYPE_CODE[X.dtype]
+        s = _lib.stream_ptr(dev)
+        _lib.call("itq3_rotate_act", _lib.ptr(X), xcode, cols, k, X.stride(0), X.stride(1), limbs, _lib.ptr(act), s)
+        Y = torch.empty((rows, k), dtype=out_dtype, device=dev)
+        _lib.call("itq3_gemv", _lib.ptr(tiled), rows, cols, int(not q.symmetric), _lib.ptr(act), k, limbs,
+                  _lib.ptr(Y), _lib.TORCH_DTYPE_CODE[out_dtype], Y.stride(0), Y.stride(1), s)
+        return Y
+    p = q.ensure_decodable()
+    Xd = X.to(torch.float64)
+    ws = torch.empty(_lib.load().itq3_generic_ws_nbytes(rows, cols, q.block_n, k), dtype=torch.uint8, device=dev)
+    Y = torch.empty((rows, k), dtype=torch.float64, device=dev)
+    _lib.call("itq3_matmul_generic", _lib.ptr(p), rows, cols, q.block_n, int(q.variant == "ss"), _lib.ptr(Xd), k,
+              Xd.stride(0), Xd.stride(1), _lib.ptr(Y), _lib.ptr(ws), _lib.stream_ptr(dev))
+    return Y if out_dtype == torch.float64 else Y.to(out_dtype)
+
+
+def fused_matmul(q: QuantizedTensor, x, *, limbs: int | None = None):
+    """Multiply the quantized matrix by X (cols x k) without materialising it."""
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        if x.ndim != 2:
+            raise ShapeError(f"fused_matmul: X must be 2-D (cols x k), got shape {tuple(x.shape)}")
+        if x.shape[0] != q.cols:
+            raise ShapeError(f"fused_matmul: X has {x.shape[0]} rows, tensor has {q.cols} columns")
+        if x.dtype not in _lib.TORCH_DTYPE_CODE:
+            x = x.to(torch.float32)
+        if not bool(torch.isfinite(x).all()):
+            raise DomainError("fused_matmul: X contains non-finite values")
+        parity = x.dtype == torch.float64
+        L = limbs or (PARITY_LIMBS if parity else perf_limbs(x.shape[1]))
+        return _matmul_device(q, x, torch.float64 if parity else torch.float32, L)
+    a = np.asarray(x, dtype=np.float64)
+    if a.ndim != 2:
+        raise ShapeError(f"fused_matmul: X must be 2-D (cols x k), got shape {a.shape}")
+    if a.shape[0] != q.cols:
+        raise ShapeError(f"fused_matmul: X has {a.shape[0]} rows, tensor has {q.cols} columns")
+    dev = _lib.device()
+    t = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    if not bool(torch.isfinite(t).all()):
+        raise DomainError("fused_matmul: X contains non-finite values")
+    return _matmul_device(q, t, torch.float64, limbs or PARITY_LIMBS).cpu().numpy()
+
+
+def fused_matvec(q: QuantizedTensor, x, *, limbs: int | None = None):
+    """Matrix-vector product: exactly the k = 1 column of fused_matmul."""
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        if x.ndim != 1:
+            raise ShapeError(f"fused_matvec: x must be 1-D, got shape {tuple(x.shape)}")
+        return fused_matmul(q, x[:, None], limbs=limbs)[:, 0]
+    a = np.asarray(x, dtype=np.float64)
+    if a.ndim != 1:
+        raise ShapeError(f"fused_matvec: x must be 1-D, got shape {a.shape}")
+    return fused_matmul(q, a[:, None], limbs=limbs)[:, 0]
