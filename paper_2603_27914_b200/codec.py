@@ -125,7 +125,7 @@ class QuantizedTensor:
             host = np.frombuffer(b"".join(b.to_bytes() for b in self._blocks), np.uint8).reshape(-1, want)
             self._payload = torch.from_numpy(host.copy()).to(dev)
         elif self._payload.device != dev:
-            return self._payload.to(dev)
+            self._payload = self._payload.to(dev)
         return self._payload
 
     def ensure_decodable(self) -> torch.Tensor:
@@ -141,7 +141,7 @@ class QuantizedTensor:
 
     def tiled(self) -> torch.Tensor:
         """Tiled GEMV/MMQ layout (csrc/gemv.cu) for the fast path, built once per device."""
-        if len(self._tiled) == 1 and self._payload is None:
+        if len(self._tiled) == 1 and (self._payload is None or not self._payload.is_cuda):
             return next(iter(self._tiled.values()))
         p = self.ensure_decodable()
         key = p.device
@@ -155,12 +155,12 @@ class QuantizedTensor:
         return self._tiled[key]
 
     def drop_payload(self) -> None:
-        """Free the container-order payload once the tiled copy exists (GEMV-only serving)."""
+        """Move the container-order payload to host memory once the tiled copy exists
+        (GEMV-only serving keeps 66 B instead of 166 B per 256 weights on the device)."""
         if not self._tiled:
             raise ValueError("drop_payload: no tiled copy built")
-        if self._blocks is None:
-            self.blocks  # keep a host copy for serialisation
-        self._payload = None
+        if self._payload is not None and self._payload.is_cuda:
+            self._payload = self._payload.cpu()
 
 
 # ------------------------------------------------------------------------------------------------

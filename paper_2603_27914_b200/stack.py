@@ -1,0 +1,97 @@
+"""Decode-time linear stack: a dependent chain of fused GEMVs replayed as one CUDA graph.
+
+There is no reference counterpart (the reference has no model); this is the harness behind
+the "decode tokens/sec" metric.  Stage i multiplies the
+quantized matrix q_i by the first q_i.cols entries of stage i-1's output, so every GEMV
+depends on the previous one exactly as in a decoder's qkv -> o -> gate_up -> down chain.
+Per stage: K3 ``itq3_rotate_act`` (x -> rotated fixed-point limbs) + K4 ``itq3_gemv``.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .codec import QuantizedTensor
+from .errors import ShapeError
+
+
+class LinearStack:
+    def __init__(self, qs: list[QuantizedTensor], limbs: int = 3):
+        if not qs:
+            raise ShapeError("LinearStack: no stages")
+        for a, b in zip(qs, qs[1:]):
+            if b.cols > a.rows:
+                raise ShapeError(f"LinearStack: stage needs {b.cols} inputs, previous stage has {a.rows} rows")
+        for q in qs:
+            if not q.fast_layout():
+                raise ShapeError("LinearStack: stages need the tiled layout (block_n 256, variant s, cols % 256 == 0)")
+        self.dev = _lib.device()
+        self.qs = qs
+        self.limbs = limbs
+        lib = _lib.load()
+        self.tiled = [q.tiled() for q in qs]
+        self.x = torch.zeros(qs[0].cols, dtype=torch.float32, device=self.dev)
+        self.acts = [torch.empty(lib.itq3_act_nbytes(q.cols, 1, limbs), dtype=torch.uint8, device=self.dev)
+                     for q in qs]
+        self.ys = [torch.empty(q.rows, dtype=torch.float32, device=self.dev) for q in qs]
+        self.graph = None
+        self.host_in = torch.empty(qs[0].cols, dtype=torch.float32).pin_memory()
+        self.host_out = torch.empty(qs[-1].rows, dtype=torch.float32).pin_memory()
+
+    @property
+    def launches_per_step(self) -> int:
+        return 2 * len(self.qs)
+
+    def gemv_bytes(self, i: int) -> int:
+        """Algorithmic bytes of stage i's GEMV launch: tiled weights + activation fragments + y."""
+        q = self.qs[i]
+        return int(self.tiled[i].numel()) + (q.cols // 256) * (2048 + 64) + 4 * q.rows
+
+    def launch_stage(self, i: int, stream: int | None = None, parts: str = "both") -> None:
+        q = self.qs[i]
+        s = stream if stream is not None else _lib.stream_ptr(self.dev)
+        xin = self.x if i == 0 else self.ys[i - 1]
+        if parts in ("both", "rotate"):
+            _lib.call("itq3_rotate_act", _lib.ptr(xin), _lib.F32, q.cols, 1, 1, q.cols, self.limbs,
+                      _lib.ptr(self.acts[i]), s)
+        if parts in ("both", "gemv"):
+            _lib.call("itq3_gemv", _lib.ptr(self.tiled[i]), q.rows, q.cols, int(not q.symmetric),
+                      _lib.ptr(self.acts[i]), 1, self.limbs, _lib.ptr(self.ys[i]), _lib.F32, 1, 1, s)
+
+    def launch_all(self) -> None:
+        for i in range(len(self.qs)):
+            self.launch_stage(i)
+
+    def capture(self) -> None:
+        """Record the whole chain as one CUDA graph (launch overhead off the critical path)."""
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(side):
+            self.launch_all()  # warm-up outside capture
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.launch_all()
+        self.graph = g
+
+    def replay(self) -> None:
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+
+    def forward(self, x) -> np.ndarray:
+        """Host in -> host out: H2D of x, the graphed chain, D2H of the last stage's output."""
+        xt = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x, dtype=np.float32))
+        if xt.numel() != self.x.numel():
+            raise ShapeError(f"LinearStack.forward: expected {self.x.numel()} inputs, got {xt.numel()}")
+        if xt.is_cuda:
+            self.x.copy_(xt.reshape(-1))
+        else:
+            self.host_in.copy_(xt.reshape(-1))
+            self.x.copy_(self.host_in, non_blocking=True)
+        self.replay()
+        self.host_out.copy_(self.ys[-1], non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        return self.host_out.numpy()
