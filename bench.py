@@ -188,7 +188,7 @@ def ncu_traffic():
         return None
 
 
-def build_stack(n_layers: int, seed: int, dev):
+def build_stack(n_layers: int, seed: int, dev, mode: str = "chain"):
     import torch
 
     import paper_2603_27914_b200 as P
@@ -205,7 +205,7 @@ def build_stack(n_layers: int, seed: int, dev):
             q.drop_payload()  # serving keeps only the tiled copy resident
             qs.append(q)
             del w
-    return LinearStack(qs, limbs=3)
+    return LinearStack(qs, limbs=3, mode=mode)
 
 
 def run_ours(args):
@@ -219,7 +219,7 @@ def run_ours(args):
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    stack = build_stack(args.layers, 1000 + rank, dev)
+    stack = build_stack(args.layers, 1000 + rank, dev, args.mode)
     stack.capture()
     x0 = torch.from_numpy(np.random.default_rng(rank).standard_normal(stack.x.numel()).astype(np.float32))
     stack.forward(x0)
@@ -263,34 +263,28 @@ def run_ours(args):
         stack.forward(x0)
     e2e_ms = max_over_ranks(1000.0 * (time.perf_counter() - t) / args.steps)
 
-    # ---- roofline: the GEMV kernel alone, all 128 launches in one graph, CUDA events ----------------
-    n_st = len(stack.qs)
-    g_only = torch.cuda.CUDAGraph()
-    side = torch.cuda.Stream(dev)
-    side.wait_stream(torch.cuda.current_stream(dev))
-    with torch.cuda.stream(side):
-        for i in range(n_st):
-            stack.launch_stage(i, parts="gemv")
-    torch.cuda.current_stream(dev).wait_stream(side)
-    with torch.cuda.graph(g_only):
-        for i in range(n_st):
-            stack.launch_stage(i, parts="gemv")
-    for _ in range(3):
-        g_only.replay()
-    torch.cuda.synchronize()
-    reps = max(3, args.steps)
-    e0.record()
-    for _ in range(reps):
-        g_only.replay()
-    e1.record()
-    torch.cuda.synchronize()
-    gemv_ms_total = e0.elapsed_time(e1) / reps
-    gemv_bytes = sum(stack.gemv_bytes(i) for i in range(n_st))
-    per_launch_bytes = gemv_bytes / n_st
-    per_launch_s = gemv_ms_total / 1000.0 / n_st
-    achieved = per_launch_bytes / per_launch_s / 1e9
+    # ---- roofline: the chain kernel is the only kernel of the step (1 launch + a counter memset) ----
     peak, peak_src = measured_peak()
     traffic = ncu_traffic()
+    step_bytes = stack.step_bytes()
+    achieved = step_bytes / (ms / 1000.0) / 1e9
+    # for comparison: the same chain as 2 launches per stage (rotate_act + gemv) in one graph
+    sep = None
+    if not args.no_compare:
+        from paper_2603_27914_b200.stack import LinearStack
+
+        st2 = LinearStack(stack.qs, limbs=stack.limbs, mode="kernels")
+        st2.capture()
+        for _ in range(3):
+            st2.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            st2.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        sep = 1000.0 / (e0.elapsed_time(e1) / args.steps)
+        del st2
 
     if rank != 0:
         if world > 1:
@@ -305,6 +299,7 @@ def run_ours(args):
         cpu_tok = arm.weights_per_step * len(ts) / sum(ts) / WEIGHTS_PER_TOKEN
         cpu = {"value": cpu_tok, "unit": "tokens/s", "cores": arm.procs, "kind": "port", "sample": arm.sample_desc()}
     tiled_bytes = sum(int(t.numel()) for t in stack.tiled)
+    n_st = len(stack.qs)
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -316,13 +311,13 @@ def run_ours(args):
                    "l2": f"{tiled_bytes / 1e9:.2f} GB of tiled weights per step > 126 MB L2; no flush needed"},
         "packed_weight_gbps": tiled_bytes / (ms / 1000.0) / 1e9,
         "container_equiv_gbps": WEIGHTS_PER_TOKEN * 100 / 256 / (ms / 1000.0) / 1e9,
-        "gemv_share_of_step": gemv_ms_total / ms,
+        "separate_kernels_tokens_per_s": sep,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic.get("bytes_per_launch") if traffic else None,
-                     "kernel": "itq3::gemv_kernel<float,float>", "peak_source": peak_src,
-                     "bytes_per_launch": per_launch_bytes, "launch_us": per_launch_s * 1e6,
-                     "algorithmic_bytes": "66 B per 256 weights (64 B 2-bit codes + 2 B f16 scale) + 2112 B per "
-                                          "256-block of rotated activation + 4 B per output row"},
+                     "kernel": "itq3::chain_kernel (whole step, 1 launch)", "peak_source": peak_src,
+                     "bytes_per_launch": step_bytes, "launch_us": ms * 1000.0,
+                     "algorithmic_bytes": "66 B per 256 weights (64 B 2-bit codes + 2 B f16 scale) + 800 B per "
+                                          "256-block of rotated activation (3 limbs) + 4 B per output row"},
         "cpu_baseline": cpu,
         "e2e": {"value": world * 1000.0 / e2e_ms, "unit": "tokens/s", "h2d_bytes_per_step": 4 * stack.x.numel(),
                 "d2h_bytes_per_step": 4 * stack.ys[-1].numel(), "api": "LinearStack.forward(host np.float32)"},
@@ -344,6 +339,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=64)
     ap.add_argument("--cpu-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-compare", action="store_true")
+    ap.add_argument("--mode", choices=["chain", "kernels"], default="chain")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

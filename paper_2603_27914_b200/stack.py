@@ -9,6 +9,8 @@ Per stage: K3 ``itq3_rotate_act`` (x -> rotated fixed-point limbs) + K4 ``itq3_g
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -18,7 +20,10 @@ from .errors import ShapeError
 
 
 class LinearStack:
-    def __init__(self, qs: list[QuantizedTensor], limbs: int = 3):
+    """mode="chain": one persistent cooperative kernel per step (csrc/chain.cu, default);
+    mode="kernels": 2 launches per stage (K3 rotate_act + K4 gemv), for comparison."""
+
+    def __init__(self, qs: list[QuantizedTensor], limbs: int = 3, mode: str = "chain"):
         if not qs:
             raise ShapeError("LinearStack: no stages")
         for a, b in zip(qs, qs[1:]):
@@ -37,17 +42,51 @@ class LinearStack:
                      for q in qs]
         self.ys = [torch.empty(q.rows, dtype=torch.float32, device=self.dev) for q in qs]
         self.graph = None
+        self.mode = mode
+        if mode == "chain":
+            self._setup_chain()
+        elif mode != "kernels":
+            raise ValueError(f"LinearStack: unknown mode {mode!r}")
         self.host_in = torch.empty(qs[0].cols, dtype=torch.float32).pin_memory()
         self.host_out = torch.empty(qs[-1].rows, dtype=torch.float32).pin_memory()
 
+    def _setup_chain(self) -> None:
+        lib = _lib.load()
+        S = len(self.qs)
+        nd = lib.itq3_chain_desc_nbytes()
+        host = ctypes.create_string_buffer(nd * S)
+        ab = lib.itq3_chain_act_block_bytes(self.limbs)
+        self.chain_act = [torch.empty((q.cols // 256) * ab, dtype=torch.uint8, device=self.dev) for q in self.qs]
+        off = 0
+        for i, q in enumerate(self.qs):
+            _lib.check(lib.itq3_chain_write_desc(host, i, _lib.ptr(self.tiled[i]), _lib.ptr(self.ys[i]),
+                                                 _lib.ptr(self.chain_act[i]), q.rows, q.cols, int(not q.symmetric),
+                                                 off))
+            off += -(-q.rows // 256)
+        self.counters = torch.zeros(S, dtype=torch.int32, device=self.dev)
+        self.trace = None
+        self.desc = torch.frombuffer(bytearray(host.raw), dtype=torch.uint8).to(self.dev)
+
+    def enable_trace(self) -> torch.Tensor:
+        """Per-(CTA, stage) globaltimer stamps: entered, input ready, input rotated, last tile done."""
+        sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
+        self.trace = torch.zeros((sms, len(self.qs), 4), dtype=torch.int64, device=self.dev)
+        self.graph = None
+        return self.trace
+
     @property
     def launches_per_step(self) -> int:
-        return 2 * len(self.qs)
+        return 1 if self.mode == "chain" else 2 * len(self.qs)
+
+    def step_bytes(self) -> int:
+        """Algorithmic bytes of one step: all tiled weights + rotated activations + outputs."""
+        return sum(self.gemv_bytes(i) for i in range(len(self.qs)))
 
     def gemv_bytes(self, i: int) -> int:
         """Algorithmic bytes of stage i's GEMV launch: tiled weights + activation fragments + y."""
         q = self.qs[i]
-        return int(self.tiled[i].numel()) + (q.cols // 256) * (2048 + 64) + 4 * q.rows
+        act = _lib.load().itq3_chain_act_block_bytes(self.limbs) if self.mode == "chain" else 2048 + 64
+        return int(self.tiled[i].numel()) + (q.cols // 256) * act + 4 * q.rows
 
     def launch_stage(self, i: int, stream: int | None = None, parts: str = "both") -> None:
         q = self.qs[i]
@@ -61,6 +100,12 @@ class LinearStack:
                       _lib.ptr(self.acts[i]), 1, self.limbs, _lib.ptr(self.ys[i]), _lib.F32, 1, 1, s)
 
     def launch_all(self) -> None:
+        if self.mode == "chain":
+            self.counters.zero_()
+            trace = _lib.ptr(self.trace) if self.trace is not None else None
+            _lib.call("itq3_chain_run", _lib.ptr(self.desc), len(self.qs), _lib.ptr(self.x), self.limbs,
+                      _lib.ptr(self.counters), 0, trace, _lib.stream_ptr(self.dev))
+            return
         for i in range(len(self.qs)):
             self.launch_stage(i)
 

@@ -1,0 +1,89 @@
+"""GPU: the decode-chain harness (stack.py) in both modes -- the persistent chain kernel
+(csrc/chain.cu) and the per-stage kernels -- against the CPU oracle, stage by stage.
+
+Each stage's output is checked against the exact fp64 product of the oracle-decoded weights
+with the GPU's own previous-stage output (so errors do not compound), within the perf-mode
+bound of test_gpu_parity.perf_bound (24-bit rotated activations, fp32 accumulation)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import itq3_oracle as O
+
+pytestmark = pytest.mark.gpu
+P = pytest.importorskip("paper_2603_27914_b200")
+from paper_2603_27914_b200.stack import LinearStack  # noqa: E402
+
+H256 = O.hadamard(256)
+
+
+def chain_bound(payload, rows, cols, x, limbs=3):
+    """A-priori error bound of the chain kernel's stage output vs the exact fp64 product.
+
+    The chain rotates in integers: x -> x_int = rint(x / s_in), s_in = 2^(ilogb(max|x_b|) - 21),
+    exact butterfly, x' rounded to |q| <= 2^(8L-2) by a shift k (csrc/chain.cu).  Per block:
+        |err| <= d/16 * ( |t|_1 * 2^(e_in+k) / 2 + |H t|_1 * s_in / 2 )
+    plus 1e-5 * sum |w_hat| |x| for fp32 accumulation (also covers the K3 path of mode="kernels").
+    """
+    n = 256
+    nb = cols // n
+    deq = O.dequantize(payload, rows, cols, n, False)
+    quants, sb, zb, _ = O.split_payload(payload, n, False)
+    codes, _ = O.unpack_planes(quants, n)
+    t = codes.astype(np.float64) - np.trunc(O.f16_value(zb))[:, None]
+    t1 = np.abs(t).sum(axis=1).reshape(rows, nb)
+    ht1 = np.abs(t @ H256).sum(axis=1).reshape(rows, nb)
+    d = O.f16_value(sb).reshape(rows, nb)
+    xb = np.asarray(x, np.float64).reshape(nb, n)
+    mx = np.abs(xb).max(axis=1)
+    e_in = np.where(mx > 0, np.floor(np.log2(np.where(mx > 0, mx, 1.0))) - 21, 0)
+    xi = np.rint(xb * 2.0 ** -e_in[:, None])
+    amax = np.abs(xi @ H256).max(axis=1)
+    bl = np.where(amax > 0, np.floor(np.log2(np.where(amax > 0, amax, 1.0))) + 1, 0)
+    k = np.maximum(0, bl - (8 * limbs - 2))
+    bound = (d / 16.0 * (t1 * 2.0 ** (e_in + k)[None, :] / 2 + ht1 * 2.0 ** e_in[None, :] / 2)).sum(axis=1)
+    mag = np.abs(deq) @ np.abs(np.asarray(x, np.float64))
+    return deq @ np.asarray(x, np.float64), bound + 1e-5 * mag
+
+SHAPES = [(768, 512), (512, 512), (1280, 512), (512, 1024), (4608, 512), (256, 4608), (512, 256), (300, 512)]
+
+
+def build(seed, shapes=SHAPES, asym=False):
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    qs = []
+    for r, c in shapes:
+        w = torch.randn((r, c), generator=g, device="cuda") / np.sqrt(c)
+        qs.append(P.quantize_tensor(w, P.QuantConfig(symmetric=not asym)))
+    return qs
+
+
+@pytest.mark.parametrize("mode", ["chain", "kernels"])
+@pytest.mark.parametrize("asym", [False, True])
+def test_stack_matches_oracle_stagewise(mode, asym):
+    qs = build(5, asym=asym)
+    pays = [q.payload().cpu().numpy() for q in qs]
+    st = LinearStack(qs, limbs=3, mode=mode)
+    x = np.random.default_rng(0).standard_normal(qs[0].cols).astype(np.float32)
+    out = st.forward(x)
+    xin = x.astype(np.float64)
+    for i, q in enumerate(qs):
+        y = st.ys[i].cpu().numpy().astype(np.float64)
+        exact, bound = chain_bound(pays[i], q.rows, q.cols, xin, 3)
+        assert np.all(np.abs(y - exact) <= bound), (mode, i, np.max(np.abs(y - exact) / bound))
+        if i + 1 < len(qs):
+            xin = st.ys[i].cpu().numpy().astype(np.float64)[: qs[i + 1].cols]
+    np.testing.assert_array_equal(out, st.ys[-1].cpu().numpy())
+
+
+def test_chain_replay_deterministic_and_matches_kernels():
+    qs = build(9)
+    a = LinearStack(qs, mode="chain")
+    b = LinearStack(qs, mode="kernels")
+    x = np.random.default_rng(1).standard_normal(qs[0].cols).astype(np.float32)
+    ya = a.forward(x).copy()
+    for _ in range(3):
+        np.testing.assert_array_equal(a.forward(x), ya)  # graph replays are bitwise reproducible
+    yb = b.forward(x)
+    np.testing.assert_allclose(ya, yb, rtol=1e-3, atol=1e-4 * np.abs(yb).max())

@@ -1,0 +1,49 @@
+"""Timeline of one chain-kernel step (globaltimer stamps per CTA and stage).
+
+    python tools/trace_chain.py [--layers 32]
+Prints, per stage kind, the median over CTAs of: wait for the previous stage (entered ->
+input ready), rotation (ready -> rotated), compute (rotated -> last tile published), and the
+stage's critical path (max publish of s - max publish of s-1).
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layers", type=int, default=32)
+    args = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    st = bench.build_stack(args.layers, 1000, dev, "chain")
+    tr = st.enable_trace()
+    x = np.random.default_rng(0).standard_normal(st.x.numel()).astype(np.float32)
+    for _ in range(3):
+        st.forward(x)
+    t = tr.cpu().numpy().astype(np.float64)  # (cta, stage, 4)
+    t0 = t[:, 0, 0].min()
+    t = (t - t0) / 1000.0  # us
+    S = t.shape[1]
+    names = [n for n, _, _ in bench.LAYER_SHAPES]
+    crit = np.diff(np.concatenate([[0.0], t[:, :, 3].max(axis=0)]))
+    print(f"step {t[:, :, 3].max():.1f} us over {S} stages; per-stage critical path median {np.median(crit):.2f} us")
+    for k, n in enumerate(names):
+        idx = list(range(k, S, len(names)))
+        w = np.median(t[:, idx, 1] - t[:, idx, 0])
+        r = np.median(t[:, idx, 2] - t[:, idx, 1])
+        c = np.median(t[:, idx, 3] - t[:, idx, 2])
+        cm = np.median((t[:, idx, 3] - t[:, idx, 2]).max(axis=0))
+        print(f"{n:8s} wait {w:6.2f}  rotate {r:5.2f}  compute med {c:6.2f} max {cm:6.2f}  crit {np.median(crit[idx]):6.2f} us")
+    # publish skew: last-first publish time of a stage
+    sk = t[:, :, 3].max(axis=0) - t[:, :, 3].min(axis=0)
+    print(f"publish skew across CTAs median {np.median(sk):.2f} us")
+
+
+if __name__ == "__main__":
+    main()
