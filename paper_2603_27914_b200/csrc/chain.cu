@@ -29,8 +29,8 @@ constexpr int kSlotCodes = kUnitBlocks * 1024;           // 16 KB
 constexpr int kSlotScales = kUnitBlocks * 32;            // 512 B
 constexpr int kSlotZps = kUnitBlocks * 16;               // 256 B
 constexpr int kSlotBytes = kSlotCodes + kSlotScales + kSlotZps;
-constexpr int kNumSlots = 8;
-constexpr int kMaxChainNB = 48;                          // K up to 12288
+constexpr int kNumSlots = 10;
+constexpr int kMaxChainNB = 256;                         // K up to 65536
 constexpr int kMaxLimbs = 4;
 
 struct ChainStage {
@@ -42,6 +42,7 @@ struct ChainStage {
 };
 
 __host__ __device__ inline int act_block_bytes(int L) { return 256 * L + 32; }
+constexpr int kActSmemBlock = 8 * 32 * 8 + 64;  // full 8-column fragments + 8 (factor, corr) pairs
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -87,39 +88,22 @@ __device__ __forceinline__ void mma_u8s8_c(int (&c)[4], uint32_t a0, uint32_t a1
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-struct ChainSmem {
-    uint8_t ring[kNumSlots][kSlotBytes];
-    uint8_t act[kMaxChainNB * (256 * kMaxLimbs + 32)];
-    float red[kNumSlots][kChainConsumerWarps][16];  // per-slot per-warp row partials (limbs combined)
-    float chunkpart[kNumSlots][4][16];                  // per in-flight row tile: per-chunk row sums
-    uint64_t full[kNumSlots];
-    uint64_t empty[kNumSlots];
-    int slotcnt[kNumSlots];
-    int rtcnt[kNumSlots];
-    int stage_tiles;  // row tiles of the current stage finalised by this CTA
-};
-
-constexpr int kMaxChunks = 4;
-
-__device__ __forceinline__ int stage_rt0(int cta, int s, int G) { return (cta + 7 * s) % G; }
-
-__device__ __forceinline__ unsigned long long globaltimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
-// Rotate 256 fp32 values (read through L2) into a compact fragment record in shared memory.
+// Rotate 256 fp32 values (read through L2; the sum of `nparts` K-chunk partial buffers) into
+// a compact fragment record in shared memory.
 // Integer pipeline on the INT32 pipe: y -> 23-bit fixed point with the block's power-of-two
 // scale s_in = 2^(ilogb(max|y|) - 21) (|y_int| < 2^22, as fine as fp32's own rounding of the
 // largest elements), exact int32 butterfly (|x'| < 2^30), then x' rounded to the limb range
 // |q| <= 2^(8L-2) with one more power-of-two shift k (tests/test_gpu_stack.py chain_bound).
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((e + 127) << 23); }  // e in [-126, 127]
 
-__device__ void chain_rotate_to_smem(const float* src, int L, uint8_t* img, int lane) {
+__device__ void chain_rotate_to_smem(const float* src, int nparts, int64_t part_stride, int L, uint8_t* img,
+                                     int lane) {
     float f[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) f[e] = __ldcg(src + lane + 32 * e);
+    for (int c = 1; c < nparts; ++c)  // K-chunk partials of the producing stage, fixed order
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[e] += __ldcg(src + c * part_stride + lane + 32 * e);
     float fmaxa = 0.f;
 #pragma unroll
     for (int e = 0; e < 8; ++e) fmaxa = fmaxf(fmaxa, fabsf(f[e]));
@@ -159,6 +143,9 @@ __device__ void chain_rotate_to_smem(const float* src, int L, uint8_t* img, int 
     const int ex = e_in + k;
     int Q = 0;
     const int tt = (lane & 15) >> 2, beta = lane & 3, half = lane >> 4;
+    // zero the record (unused columns must read as 0), then scatter the limb bytes
+    for (int i = lane; i < kActSmemBlock / 16; i += 32) reinterpret_cast<uint4*>(img)[i] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
         int q = k ? ((v[e] + (1 << (k - 1))) >> k) : v[e];
@@ -168,24 +155,63 @@ __device__ void chain_rotate_to_smem(const float* src, int L, uint8_t* img, int 
             if (l < L) {
                 const int lb = ((q + 128) & 255) - 128;
                 q = (q - lb) >> 8;
-                img[((e * L + l) * 4 + tt) * 8 + half * 4 + beta] = (uint8_t)(int8_t)lb;
+                img[(e * 32 + 4 * l + tt) * 8 + half * 4 + beta] = (uint8_t)(int8_t)lb;
             }
         }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) Q += __shfl_xor_sync(FULL, Q, o);
-    float* meta = reinterpret_cast<float*>(img + 256 * L);
+    float* meta = reinterpret_cast<float*>(img + 8 * 32 * 8);  // f[0..7], corr[0..7]
     if (lane < L) {
-        meta[2 * lane] = ldexpf(1.0f, 8 * lane + ex - 4);
-        meta[2 * lane + 1] = lane == 0 ? ldexpf((float)Q, ex - 4) : 0.0f;
+        meta[lane] = ldexpf(1.0f, 8 * lane + ex - 4);
+        meta[8 + lane] = lane == 0 ? ldexpf((float)Q, ex - 4) : 0.0f;
     }
 }
 
+struct ChainSmem {
+    uint8_t ring[kNumSlots][kSlotBytes];
+    uint8_t act[kUnitBlocks * kActSmemBlock];  // the CTA's K-chunk of the stage input (full fragments)
+    float part[kNumSlots][kChainConsumerWarps][16];       // per-segment row partials of a unit
+    uint64_t full[kNumSlots];
+    uint64_t empty[kNumSlots];
+    int partcnt[kNumSlots];
+};
+
+static_assert(sizeof(ChainSmem) <= 227 * 1024, "chain kernel shared memory exceeds the 227 KB per-CTA limit");
+
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Work split of stage st for CTA cta: K-chunk ch (CTAs c with c % nch == ch), and the row
+// tiles rt = rt0, rt0 + Gc, ... (Gc CTAs per chunk).  Returns false if the CTA is idle.
+struct StageSplit {
+    int nch, ch, rt0, Gc;
+};
+__device__ __forceinline__ bool stage_split(const ChainStage& st, int cta, int G, int s, StageSplit& sp) {
+    sp.nch = (st.NB + kUnitBlocks - 1) / kUnitBlocks;
+    sp.Gc = G / sp.nch;
+    sp.ch = cta % sp.nch;
+    const int idx = cta / sp.nch;
+    if (idx >= sp.Gc) return false;
+    sp.rt0 = (idx + 7 * s) % sp.Gc;
+    return sp.rt0 < st.RT;
+}
+
 // trace (optional): per (cta, stage) globaltimer stamps
-//   0 stage entered, 1 input observed ready, 2 input rotated, 3 last unit of the stage reduced
+//   0 stage entered, 1 input observed ready, 2 input rotated, 3 own units done
+// 17 warps: the per-SMSP register file (16K) caps a 5-warp SMSP at 96 registers/thread
 __global__ void __launch_bounds__(kChainThreads, 1)
     chain_kernel(const ChainStage* __restrict__ stages, int S, const float* __restrict__ x0, int L,
-                 unsigned* __restrict__ done, unsigned long long* __restrict__ trace) {
+                 unsigned* __restrict__ done, float* __restrict__ out, unsigned long long* __restrict__ trace) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     ChainSmem& sm = *reinterpret_cast<ChainSmem*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -196,10 +222,8 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         for (int i = 0; i < kNumSlots; ++i) {
             mbar_init(&sm.full[i], 1);
             mbar_init(&sm.empty[i], kChainConsumerWarps);
-            sm.slotcnt[i] = 0;
-            sm.rtcnt[i] = 0;
+            sm.partcnt[i] = 0;
         }
-        sm.stage_tiles = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -211,23 +235,24 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             unsigned phase = 0;
             for (int s = 0; s < S; ++s) {
                 const ChainStage st = stages[s];
+                StageSplit sp;
+                if (!stage_split(st, cta, G, s, sp)) continue;
                 const uint8_t* scales = st.tiled + (int64_t)st.RT * st.NB * 1024;
                 const uint8_t* zps = scales + (int64_t)st.RT * st.NB * 32;
-                for (int rt = stage_rt0(cta, s, G); rt < st.RT; rt += G) {
-                    for (int b0 = 0; b0 < st.NB; b0 += kUnitBlocks) {
-                        const int nb = min(kUnitBlocks, st.NB - b0);
-                        mbar_wait(&sm.empty[slot], phase ^ 1u);
-                        const int64_t t0 = (int64_t)rt * st.NB + b0;
-                        const unsigned bytes = nb * (1024 + 32 + (st.asym ? 16 : 0));
-                        mbar_expect_tx(&sm.full[slot], bytes);
-                        uint8_t* dst = sm.ring[slot];
-                        bulk_g2s(dst, st.tiled + t0 * 1024, nb * 1024, &sm.full[slot]);
-                        bulk_g2s(dst + kSlotCodes, scales + t0 * 32, nb * 32, &sm.full[slot]);
-                        if (st.asym) bulk_g2s(dst + kSlotCodes + kSlotScales, zps + t0 * 16, nb * 16, &sm.full[slot]);
-                        if (++slot == kNumSlots) {
-                            slot = 0;
-                            phase ^= 1u;
-                        }
+                const int b0 = sp.ch * kUnitBlocks;
+                const int nb = min(kUnitBlocks, st.NB - b0);
+                const unsigned bytes = nb * (1024 + 32 + (st.asym ? 16 : 0));
+                for (int rt = sp.rt0; rt < st.RT; rt += sp.Gc) {
+                    mbar_wait(&sm.empty[slot], phase ^ 1u);
+                    const int64_t t0 = (int64_t)rt * st.NB + b0;
+                    mbar_expect_tx(&sm.full[slot], bytes);
+                    uint8_t* dst = sm.ring[slot];
+                    bulk_g2s(dst, st.tiled + t0 * 1024, nb * 1024, &sm.full[slot]);
+                    bulk_g2s(dst + kSlotCodes, scales + t0 * 32, nb * 32, &sm.full[slot]);
+                    if (st.asym) bulk_g2s(dst + kSlotCodes + kSlotScales, zps + t0 * 16, nb * 16, &sm.full[slot]);
+                    if (++slot == kNumSlots) {
+                        slot = 0;
+                        phase ^= 1u;
                     }
                 }
             }
@@ -237,158 +262,193 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 
     // ------------------------------ consumers ------------------------------
     const int g = lane >> 2, t = lane & 3;
-    int slot = 0;
-    unsigned phase = 0;
-    int unit_seq = 0;  // row-tile sequence number within the CTA (indexes chunkpart / rtcnt)
+    int seq = 0;  // CTA-wide unit sequence number (ring slot = seq % kNumSlots)
     for (int s = 0; s < S; ++s) {
         const ChainStage st = stages[s];
-        int rt = stage_rt0(cta, s, G);
-        if (rt >= st.RT) continue;
+        StageSplit sp;
+        const bool active = stage_split(st, cta, G, s, sp);
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 0] = globaltimer();
-        // wait until every row tile of the previous stage is published, then rotate its output
-        const float* xin = x0;
+        // publish the previous stage's units (one cumulative fence per CTA) and wait for all
         if (s > 0) {
             const ChainStage pv = stages[s - 1];
-            xin = pv.y;
-            if (tid == 0) {
-                while (ld_acquire(&done[s - 1]) < (unsigned)pv.RT) __nanosleep(20);
+            const unsigned total = (unsigned)pv.RT * (unsigned)((pv.NB + kUnitBlocks - 1) / kUnitBlocks);
+            if (tid == 0 && active) {
+                while (ld_relaxed(&done[s - 1]) < total) {
+                }
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
             }
             consumer_sync();
         }
+        if (!active) continue;
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 1] = globaltimer();
-        for (int b = warp; b < st.NB; b += kChainConsumerWarps)
-            chain_rotate_to_smem(xin + 256 * b, L, sm.act + b * ab, lane);
+        const int b0 = sp.ch * kUnitBlocks;
+        const int nb = min(kUnitBlocks, st.NB - b0);
+        if (warp < nb) {
+            if (s == 0) {
+                chain_rotate_to_smem(x0 + 256 * (b0 + warp), 1, 0, L, sm.act + warp * kActSmemBlock, lane);
+            } else {
+                const ChainStage pv = stages[s - 1];
+                const int pn = (pv.NB + kUnitBlocks - 1) / kUnitBlocks;
+                chain_rotate_to_smem(pv.y + 256 * (b0 + warp), pn, pv.rows, L, sm.act + warp * kActSmemBlock, lane);
+            }
+        }
         consumer_sync();
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 2] = globaltimer();
-        const int nch = (st.NB + kUnitBlocks - 1) / kUnitBlocks;
-        const int my_tiles = (st.RT - 1 - rt) / G + 1;
-        for (; rt < st.RT; rt += G, ++unit_seq) {
-            const int rslot = unit_seq % kNumSlots;
-            for (int ch = 0; ch < nch; ++ch) {
-                const int b0 = ch * kUnitBlocks;
-                mbar_wait(&sm.full[slot], phase);
-                const int b = b0 + warp;
-                float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
-                if (b < st.NB) {
-                    const uint8_t* ring = sm.ring[slot];
-                    const uint4 wa0 = reinterpret_cast<const uint4*>(ring + warp * 1024)[lane];
-                    const uint4 wa1 = reinterpret_cast<const uint4*>(ring + warp * 1024 + 512)[lane];
-                    const uint32_t sc = reinterpret_cast<const uint32_t*>(ring + kSlotCodes + warp * 32)[g];
-                    uint16_t zz = 0;
-                    if (st.asym) zz = reinterpret_cast<const uint16_t*>(ring + kSlotCodes + kSlotScales + warp * 16)[g];
-                    const uint8_t* a = sm.act + b * ab;
-                    uint2 bf[8];
+
+        // The stage's T = n_units * nb tiles (unit j = row tile rt0 + j*Gc, tiles in K order) are
+        // split into min(16, T) balanced contiguous ranges, one per warp, crossing unit boundaries.  A
+        // unit covered by several warps ("segments") is summed by its last segment in segment
+        // order (deterministic); every warp publishes the units it stored with one release.
+        const int n_units_all = (st.RT - 1 - sp.rt0) / sp.Gc + 1;
+        float* yout = st.y + (int64_t)sp.ch * st.rows;
+        unsigned stored = 0;
+        unsigned long long* wtr = (trace && cta == 0) ? trace + (int64_t)G * S * 4 + ((int64_t)s * 16 + warp) * 4 : nullptr;
+        // rounds of at most kNumSlots units: a warp never waits on a ring slot more than one
+        // mbarrier phase ahead of its last release (no parity aliasing for any stage size)
+        for (int u0 = 0; u0 < n_units_all; u0 += kNumSlots) {
+        if (u0 > 0) consumer_sync();
+        const int n_units = min(kNumSlots, n_units_all - u0);
+        const int T = n_units * nb;
+        const int nw = min(kChainConsumerWarps, T);  // every active warp gets >= 1 tile
+        const int tau0 = warp < nw ? warp * T / nw : 0, tau1 = warp < nw ? (warp + 1) * T / nw : 0;
+        auto warp_of = [&](int tau) { return (nw * (tau + 1) + T - 1) / T - 1; };
+        if (wtr && lane == 0 && u0 == 0) wtr[0] = globaltimer();
+        bool first_wait = u0 == 0;
+        int tau = tau0;
+        while (tau < tau1) {
+            const int j = tau / nb;
+            const int bb_lo = tau - j * nb;
+            const int bb_hi = min(nb, tau1 - j * nb);
+            const int rt = sp.rt0 + (u0 + j) * sp.Gc;
+            const int useq = seq + u0 + j;
+            const int slot = useq % kNumSlots;
+            const unsigned phase = (unsigned)(useq / kNumSlots) & 1u;
+            const int w_first = warp_of(j * nb), w_last = warp_of(j * nb + nb - 1);
+            const int nseg = w_last - w_first + 1;
+            mbar_wait(&sm.full[slot], phase);
+            if (wtr && lane == 0 && first_wait) wtr[1] = globaltimer();
+            first_wait = false;
+            const uint8_t* ring = sm.ring[slot];
+            float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll 2
+            for (int bb = bb_lo; bb < bb_hi; ++bb) {
+                const uint4 wa0 = reinterpret_cast<const uint4*>(ring + bb * 1024)[lane];
+                const uint4 wa1 = reinterpret_cast<const uint4*>(ring + bb * 1024 + 512)[lane];
+                const uint32_t sc = reinterpret_cast<const uint32_t*>(ring + kSlotCodes + bb * 32)[g];
+                const uint8_t* a = sm.act + bb * kActSmemBlock;
+                uint2 bf[8];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        bf[q] = g < L ? reinterpret_cast<const uint2*>(a)[(q * L + g) * 4 + t] : make_uint2(0u, 0u);
-                    const float* meta = reinterpret_cast<const float*>(a + 256 * L);
-                    const float f0 = 2 * t < L ? meta[4 * t] : 0.f, c0 = 2 * t < L ? meta[4 * t + 1] : 0.f;
-                    const float f1 = 2 * t + 1 < L ? meta[4 * t + 2] : 0.f, c1 = 2 * t + 1 < L ? meta[4 * t + 3] : 0.f;
-                    int C[4][4];
+                for (int q = 0; q < 8; ++q) bf[q] = reinterpret_cast<const uint2*>(a)[q * 32 + lane];
+                // columns 2t, 2t+1 are limbs 2t, 2t+1 of the token: factors differ by exactly 256
+                const float2 fc = reinterpret_cast<const float2*>(a + 8 * 32 * 8)[t];       // f[2t], f[2t+1]
+                const float2 cc = reinterpret_cast<const float2*>(a + 8 * 32 * 8 + 32)[t];  // corr[2t], corr[2t+1]
+                int C[4][4];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) C[i][0] = C[i][1] = C[i][2] = C[i][3] = 0;
+                for (int i = 0; i < 4; ++i) C[i][0] = C[i][1] = C[i][2] = C[i][3] = 0;
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const uint32_t mk = 0x03030303u << (2 * i);
-                        mma_u8s8_c(C[i], wa0.x & mk, wa0.y & mk, wa0.z & mk, wa0.w & mk, bf[i].x, bf[i].y);
-                    }
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const uint32_t mk = 0x03030303u << (2 * i);
-                        mma_u8s8_c(C[i], wa1.x & mk, wa1.y & mk, wa1.z & mk, wa1.w & mk, bf[4 + i].x, bf[4 + i].y);
-                    }
-                    int Cc[4];
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) Cc[r] = C[0][r] + (C[1][r] >> 2) + (C[2][r] >> 4) + (C[3][r] >> 6);
-                    const float d0 = f16_bits_to_f32((uint16_t)(sc & 0xffffu));
-                    const float d1 = f16_bits_to_f32((uint16_t)(sc >> 16));
-                    float zf0 = 1.f, zf1 = 1.f;
-                    if (st.asym) {
-                        zf0 = (float)(1 + (int)(int8_t)(zz & 0xff));
-                        zf1 = (float)(1 + (int)(int8_t)(zz >> 8));
-                    }
-                    acc[0][0] = d0 * (f0 * (float)Cc[0] - zf0 * c0);
-                    acc[0][1] = d0 * (f1 * (float)Cc[1] - zf0 * c1);
-                    acc[1][0] = d1 * (f0 * (float)Cc[2] - zf1 * c0);
-                    acc[1][1] = d1 * (f1 * (float)Cc[3] - zf1 * c1);
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t mk = 0x03030303u << (2 * i);
+                    mma_u8s8_c(C[i], wa0.x & mk, wa0.y & mk, wa0.z & mk, wa0.w & mk, bf[i].x, bf[i].y);
                 }
-                // combine limb columns in-warp (fixed order: quad lanes t = 0..3 via xor 1, 2), then
-                // publish one partial per row; the last warp to finish the slot reduces it
-                float r0 = acc[0][0] + acc[0][1], r1 = acc[1][0] + acc[1][1];
-                r0 += __shfl_xor_sync(FULL, r0, 1);
-                r1 += __shfl_xor_sync(FULL, r1, 1);
-                r0 += __shfl_xor_sync(FULL, r0, 2);
-                r1 += __shfl_xor_sync(FULL, r1, 2);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t mk = 0x03030303u << (2 * i);
+                    mma_u8s8_c(C[i], wa1.x & mk, wa1.y & mk, wa1.z & mk, wa1.w & mk, bf[4 + i].x, bf[4 + i].y);
+                }
+                int Cc[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) Cc[r] = C[0][r] + (C[1][r] >> 2) + (C[2][r] >> 4) + (C[3][r] >> 6);
+                // |Cc| <= 2^16, so Cc[even] + 256 * Cc[odd] is exact in int32 (< 2^25)
+                const float v0 = (float)(Cc[0] + 256 * Cc[1]), v1 = (float)(Cc[2] + 256 * Cc[3]);
+                const float corr = cc.x + cc.y;
+                const float d0 = f16_bits_to_f32((uint16_t)(sc & 0xffffu));
+                const float d1 = f16_bits_to_f32((uint16_t)(sc >> 16));
+                float zf0 = 1.f, zf1 = 1.f;
+                if (st.asym) {
+                    const uint16_t zz = reinterpret_cast<const uint16_t*>(ring + kSlotCodes + kSlotScales + bb * 16)[g];
+                    zf0 = (float)(1 + (int)(int8_t)(zz & 0xff));
+                    zf1 = (float)(1 + (int)(int8_t)(zz >> 8));
+                }
+                acc[0][0] += d0 * (fc.x * v0 - zf0 * corr);
+                acc[1][0] += d1 * (fc.x * v1 - zf1 * corr);
+            }
+            // combine limb-pair columns over the quad (lanes t = 0..3, fixed order)
+            float r0 = acc[0][0], r1 = acc[1][0];
+            r0 += __shfl_xor_sync(FULL, r0, 1);
+            r1 += __shfl_xor_sync(FULL, r1, 1);
+            r0 += __shfl_xor_sync(FULL, r0, 2);
+            r1 += __shfl_xor_sync(FULL, r1, 2);
+            bool store = nseg == 1;
+            if (nseg > 1) {
+                const int segi = warp - w_first;
                 if (t == 0) {
-                    sm.red[slot][warp][g] = r0;
-                    sm.red[slot][warp][g + 8] = r1;
+                    sm.part[slot][segi][g] = r0;
+                    sm.part[slot][segi][g + 8] = r1;
                 }
                 __syncwarp();
                 int last = 0;
                 if (lane == 0) {
                     __threadfence_block();
-                    last = atomicAdd(&sm.slotcnt[slot], 1) == kChainConsumerWarps - 1;
+                    last = atomicAdd(&sm.partcnt[slot], 1) == nseg - 1;
                 }
                 last = __shfl_sync(FULL, last, 0);
-                if (!last) {
-                    if (lane == 0) mbar_arrive(&sm.empty[slot]);
-                } else {
+                if (last) {
                     __threadfence_block();
-                    float rsum = 0.f;
-                    if (lane < 16) {
-                        float part[kChainConsumerWarps];
-#pragma unroll
-                        for (int w = 0; w < kChainConsumerWarps; ++w) part[w] = sm.red[slot][w][lane];
-#pragma unroll
-                        for (int w = 0; w < kChainConsumerWarps; ++w) rsum += part[w];
-                    }
-                    __syncwarp();
-                    if (lane == 0) {
-                        sm.slotcnt[slot] = 0;
-                        mbar_arrive(&sm.empty[slot]);
-                    }
-                    bool final = nch == 1;
-                    if (!final) {
-                        if (lane < 16) sm.chunkpart[rslot][ch][lane] = rsum;
-                        __syncwarp();
-                        int cnt = 0;
-                        if (lane == 0) {
-                            __threadfence_block();
-                            cnt = atomicAdd(&sm.rtcnt[rslot], 1) + 1;
-                        }
-                        cnt = __shfl_sync(FULL, cnt, 0);
-                        if (cnt == nch) {
-                            __threadfence_block();
-                            final = true;
-                            rsum = 0.f;
-                            if (lane < 16)
-                                for (int c = 0; c < nch; ++c) rsum += sm.chunkpart[rslot][c][lane];
-                            if (lane == 0) sm.rtcnt[rslot] = 0;
+                    if (t == 0) {
+                        r0 = r1 = 0.f;
+                        for (int p2 = 0; p2 < nseg; ++p2) {
+                            r0 += sm.part[slot][p2][g];
+                            r1 += sm.part[slot][p2][g + 8];
                         }
                     }
-                    if (final) {
-                        const int64_t row = (int64_t)rt * 16 + lane;
-                        if (lane < 16 && row < st.rows) __stcg(st.y + row, rsum);
-                        __syncwarp();
-                        if (lane == 0) {
-                            // publish once per CTA per stage: the warp finalising the CTA's last
-                            // tile fences (cumulative over the CTA's y stores) and bumps done[s]
-                            __threadfence_block();
-                            if (atomicAdd(&sm.stage_tiles, 1) + 1 == my_tiles) {
-                                sm.stage_tiles = 0;
-                                __threadfence();
-                                atomicAdd(&done[s], (unsigned)my_tiles);
-                                if (trace) trace[((int64_t)cta * S + s) * 4 + 3] = globaltimer();
-                            }
-                        }
-                    }
+                    if (lane == 0) sm.partcnt[slot] = 0;
+                    store = true;
                 }
-                if (++slot == kNumSlots) {
-                    slot = 0;
-                    phase ^= 1u;
+                __syncwarp();
+            }
+            // release the slot: every segment arrives once, the first also for absent warps
+            if (lane == 0) {
+                const unsigned cnt = warp == w_first ? (unsigned)(kChainConsumerWarps - nseg + 1) : 1u;
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&sm.empty[slot])), "r"(cnt)
+                             : "memory");
+            }
+            if (store) {
+                if (t == 0) {
+                    const int64_t row0 = (int64_t)rt * 16 + g;
+                    if (row0 < st.rows) __stcg(yout + row0, r0);
+                    if (row0 + 8 < st.rows) __stcg(yout + row0 + 8, r1);
                 }
+                ++stored;
+            }
+            tau = (j + 1) * nb;
+        }
+        }  // rounds
+        if (wtr && lane == 0) wtr[2] = globaltimer();
+        if (stored) {
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence();
+                atomicAdd(&done[s], stored);
             }
         }
+        if (wtr && lane == 0) wtr[3] = globaltimer();
+        seq += n_units_all;
+        if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 3] = globaltimer();
+    }
+    // publish the last stage, then fold its K-chunk partials into `out` (fixed order)
+    const ChainStage last = stages[S - 1];
+    const int ln = (last.NB + kUnitBlocks - 1) / kUnitBlocks;
+    const unsigned total = (unsigned)last.RT * (unsigned)ln;
+    if (tid == 0) {
+        while (ld_relaxed(&done[S - 1]) < total) {
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    consumer_sync();
+    for (int64_t r = (int64_t)cta * (32 * kChainConsumerWarps) + tid; r < last.rows; r += (int64_t)G * 32 * kChainConsumerWarps) {
+        float v = __ldcg(last.y + r);
+        for (int c = 1; c < ln; ++c) v += __ldcg(last.y + c * last.rows + r);
+        out[r] = v;
     }
 }
 
@@ -421,7 +481,7 @@ extern "C" int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* 
 }
 
 extern "C" int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_counters,
-                              int grid, void* d_trace, void* stream) {
+                              float* out, int grid, void* d_trace, void* stream) {
     if (limbs < 1 || limbs > kMaxLimbs) {
         set_error("chain: limbs must be in [1, %d]", kMaxLimbs);
         return ITQ3_E_DOMAIN;
@@ -450,7 +510,7 @@ extern "C" int itq3_chain_run(const void* d_desc, int n_stages, const float* x0,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, chain_kernel, (const ChainStage*)d_desc, n_stages, x0, limbs,
-                                             d_counters, (unsigned long long*)d_trace);
+                                             d_counters, out, (unsigned long long*)d_trace);
     if (e != cudaSuccess) {
         set_error("chain: launch failed: %s", cudaGetErrorString(e));
         return ITQ3_E_CUDA;

@@ -55,14 +55,12 @@ class LinearStack:
         S = len(self.qs)
         nd = lib.itq3_chain_desc_nbytes()
         host = ctypes.create_string_buffer(nd * S)
-        ab = lib.itq3_chain_act_block_bytes(self.limbs)
-        self.chain_act = [torch.empty((q.cols // 256) * ab, dtype=torch.uint8, device=self.dev) for q in self.qs]
-        off = 0
+        self.nch = [-(-q.cols // 4096) for q in self.qs]
+        self.yparts = [torch.empty((c, q.rows), dtype=torch.float32, device=self.dev) for c, q in zip(self.nch, self.qs)]
+        self.out = torch.empty(self.qs[-1].rows, dtype=torch.float32, device=self.dev)
         for i, q in enumerate(self.qs):
-            _lib.check(lib.itq3_chain_write_desc(host, i, _lib.ptr(self.tiled[i]), _lib.ptr(self.ys[i]),
-                                                 _lib.ptr(self.chain_act[i]), q.rows, q.cols, int(not q.symmetric),
-                                                 off))
-            off += -(-q.rows // 256)
+            _lib.check(lib.itq3_chain_write_desc(host, i, _lib.ptr(self.tiled[i]), _lib.ptr(self.yparts[i]), None,
+                                                 q.rows, q.cols, int(not q.symmetric), 0))
         self.counters = torch.zeros(S, dtype=torch.int32, device=self.dev)
         self.trace = None
         self.desc = torch.frombuffer(bytearray(host.raw), dtype=torch.uint8).to(self.dev)
@@ -70,7 +68,8 @@ class LinearStack:
     def enable_trace(self) -> torch.Tensor:
         """Per-(CTA, stage) globaltimer stamps: entered, input ready, input rotated, last tile done."""
         sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
-        self.trace = torch.zeros((sms, len(self.qs), 4), dtype=torch.int64, device=self.dev)
+        S = len(self.qs)
+        self.trace = torch.zeros(sms * S * 4 + S * 16 * 4, dtype=torch.int64, device=self.dev)
         self.graph = None
         return self.trace
 
@@ -104,10 +103,24 @@ class LinearStack:
             self.counters.zero_()
             trace = _lib.ptr(self.trace) if self.trace is not None else None
             _lib.call("itq3_chain_run", _lib.ptr(self.desc), len(self.qs), _lib.ptr(self.x), self.limbs,
-                      _lib.ptr(self.counters), 0, trace, _lib.stream_ptr(self.dev))
+                      _lib.ptr(self.counters), _lib.ptr(self.out), 0, trace, _lib.stream_ptr(self.dev))
             return
         for i in range(len(self.qs)):
             self.launch_stage(i)
+
+    def output(self) -> torch.Tensor:
+        """Device output of the last stage."""
+        return self.out if self.mode == "chain" else self.ys[-1]
+
+    def stage_output(self, i: int) -> torch.Tensor:
+        """Stage i's output; in chain mode the K-chunk partials summed in the kernel's order."""
+        if self.mode != "chain":
+            return self.ys[i]
+        p = self.yparts[i]
+        y = p[0].clone()
+        for c in range(1, p.shape[0]):
+            y += p[c]
+        return y
 
     def capture(self) -> None:
         """Record the whole chain as one CUDA graph (launch overhead off the critical path)."""
@@ -137,6 +150,6 @@ class LinearStack:
             self.host_in.copy_(xt.reshape(-1))
             self.x.copy_(self.host_in, non_blocking=True)
         self.replay()
-        self.host_out.copy_(self.ys[-1], non_blocking=True)
+        self.host_out.copy_(self.output(), non_blocking=True)
         torch.cuda.current_stream(self.dev).synchronize()
         return self.host_out.numpy()

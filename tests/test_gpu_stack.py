@@ -46,7 +46,8 @@ def chain_bound(payload, rows, cols, x, limbs=3):
     mag = np.abs(deq) @ np.abs(np.asarray(x, np.float64))
     return deq @ np.asarray(x, np.float64), bound + 1e-5 * mag
 
-SHAPES = [(768, 512), (512, 512), (1280, 512), (512, 1024), (4608, 512), (256, 4608), (512, 256), (300, 512)]
+SHAPES = [(26112, 256), (768, 512), (512, 512), (1280, 512), (512, 1024), (4608, 512), (256, 4608), (9000, 256), (400, 8960),
+          (8960, 256), (300, 8704)]
 
 
 def build(seed, shapes=SHAPES, asym=False):
@@ -69,12 +70,12 @@ def test_stack_matches_oracle_stagewise(mode, asym):
     out = st.forward(x)
     xin = x.astype(np.float64)
     for i, q in enumerate(qs):
-        y = st.ys[i].cpu().numpy().astype(np.float64)
+        y = st.stage_output(i).cpu().numpy().astype(np.float64)
         exact, bound = chain_bound(pays[i], q.rows, q.cols, xin, 3)
         assert np.all(np.abs(y - exact) <= bound), (mode, i, np.max(np.abs(y - exact) / bound))
         if i + 1 < len(qs):
-            xin = st.ys[i].cpu().numpy().astype(np.float64)[: qs[i + 1].cols]
-    np.testing.assert_array_equal(out, st.ys[-1].cpu().numpy())
+            xin = st.stage_output(i).cpu().numpy().astype(np.float64)[: qs[i + 1].cols]
+    np.testing.assert_array_equal(out, st.stage_output(len(qs) - 1).cpu().numpy())
 
 
 def test_chain_replay_deterministic_and_matches_kernels():

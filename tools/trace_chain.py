@@ -26,10 +26,14 @@ def main():
     x = np.random.default_rng(0).standard_normal(st.x.numel()).astype(np.float32)
     for _ in range(3):
         st.forward(x)
-    t = tr.cpu().numpy().astype(np.float64)  # (cta, stage, 4)
+    raw = tr.cpu().numpy().astype(np.float64)
+    S = len(st.qs)
+    G = (raw.size - S * 64) // (S * 4)
+    t = raw[: G * S * 4].reshape(G, S, 4)
+    wt = raw[G * S * 4:].reshape(S, 16, 4)
     t0 = t[:, 0, 0].min()
     t = (t - t0) / 1000.0  # us
-    S = t.shape[1]
+    wt = np.where(wt > 0, (wt - t0) / 1000.0, np.nan)
     names = [n for n, _, _ in bench.LAYER_SHAPES]
     crit = np.diff(np.concatenate([[0.0], t[:, :, 3].max(axis=0)]))
     print(f"step {t[:, :, 3].max():.1f} us over {S} stages; per-stage critical path median {np.median(crit):.2f} us")
@@ -40,6 +44,14 @@ def main():
         c = np.median(t[:, idx, 3] - t[:, idx, 2])
         cm = np.median((t[:, idx, 3] - t[:, idx, 2]).max(axis=0))
         print(f"{n:8s} wait {w:6.2f}  rotate {r:5.2f}  compute med {c:6.2f} max {cm:6.2f}  crit {np.median(crit[idx]):6.2f} us")
+    # CTA 0 per-warp detail, relative to the stage's "rotated" stamp: first full wait, tiles, publish
+    for k, n in enumerate(names):
+        idx = list(range(k, S, len(names)))
+        base = t[0, idx, 2][:, None]
+        fw = np.nanmedian(wt[idx, :, 1] - base)
+        td = np.nanmedian(wt[idx, :, 2] - base)
+        pb = np.nanmedian(wt[idx, :, 3] - wt[idx, :, 2])
+        print(f"  cta0 {n:8s} first-full {fw:6.2f}  tiles-done {td:6.2f}  publish-fence {pb:5.2f} us (warp medians)")
     # publish skew: last-first publish time of a stage
     sk = t[:, :, 3].max(axis=0) - t[:, :, 3].min(axis=0)
     print(f"publish skew across CTAs median {np.median(sk):.2f} us")
