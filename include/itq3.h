@@ -99,6 +99,19 @@ int itq3_rotate_act(const void* x, int x_dtype, int64_t cols, int64_t m, int64_t
 int itq3_gemv(const uint8_t* tiled, int64_t rows, int64_t cols, int asymmetric, const uint8_t* act, int64_t m,
               int limbs, void* y, int y_dtype, int64_t stride_r, int64_t stride_m, void* stream);
 
+/* ---- K5 batched MMQ on tcgen05 tensor cores (csrc/mmq.cu): Y = w_hat @ X for M >= 16 tokens.
+ * Weights: itq3_repack_mmq layout (2-bit codes, 66 B per 256 weights + padding to 128 rows);
+ * activations: itq3_rotate_act_f16 (x'' = H x / 16 as f16, pre-swizzled token tiles of
+ * itq3_mmq_block_n(m) tokens).  A = d*t is exact in f16; fp32 accumulation in TMEM. */
+int64_t itq3_mmq_nbytes(int64_t rows, int64_t cols, int asymmetric);
+int itq3_repack_mmq(const uint8_t* payload, int64_t rows, int64_t cols, int asymmetric, uint8_t* out, void* stream);
+int itq3_mmq_block_n(int64_t m);
+int64_t itq3_mmq_act_nbytes(int64_t cols, int64_t m);
+int itq3_rotate_act_f16(const void* x, int x_dtype, int64_t cols, int64_t m, int64_t stride_k, int64_t stride_m,
+                        uint8_t* out, void* stream);
+int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asymmetric, const uint8_t* act, int64_t m, void* y,
+             int y_dtype, int64_t stride_r, int64_t stride_m, void* stream);
+
 /* ---- generic fused matmul for every other layout (any block_n, variant ss,
  * row-straddling blocks): fp64 exact decode + fp64 dot, deterministic block order.
  * X (cols x k) fp64 at X[c*stride_c + j*stride_j]; Y (rows x k) fp64 row-major.

@@ -69,6 +69,7 @@ class QuantizedTensor:
         self._payload = payload
         self._validated = validated  # planes + zero-point checked (decode paths)
         self._tiled = {}
+        self._mmq = {}
 
     # -- reference-compatible surface ------------------------------------------------------------
     @property
@@ -153,6 +154,18 @@ class QuantizedTensor:
                       _lib.stream_ptr(p.device))
             self._tiled[key] = t
         return self._tiled[key]
+
+    def mmq_layout(self) -> torch.Tensor:
+        """tcgen05 MMQ layout (csrc/mmq.cu: 2-bit codes in 64-k slabs, rows padded to 128)."""
+        p = self.ensure_decodable()
+        if p.device not in self._mmq:
+            asym = 0 if self.symmetric else 1
+            t = torch.empty(_lib.load().itq3_mmq_nbytes(self.rows, self.cols, asym), dtype=torch.uint8,
+                            device=p.device)
+            _lib.call("itq3_repack_mmq", _lib.ptr(p), self.rows, self.cols, asym, _lib.ptr(t),
+                      _lib.stream_ptr(p.device))
+            self._mmq[p.device] = t
+        return self._mmq[p.device]
 
     def drop_payload(self) -> None:
         """Move the container-order payload to host memory once the tiled copy exists

@@ -5,7 +5,9 @@ Two modes, chosen by the operand type:
     ``fused_matmul`` within its own tolerance (test_compute.py:66-103, rtol 1e-5): the
     rotated activations carry 6 fixed-point limbs (48 bits) and blocks accumulate in fp64.
   * CUDA torch tensor X   -> perf mode: float32 result (float64 if X is float64); 3 limbs
-    (24-bit activations) at M = 1 and 2 limbs (16-bit) for M > 1, fp32 accumulation.
+    (24-bit activations) at M = 1 and 2 limbs (16-bit) for M > 1, fp32 accumulation; for
+    M >= 16 columns the tcgen05 MMQ kernel (exact f16 weights d*t, f16 rotated activations,
+    fp32 TMEM accumulation).
 Both run the same kernels: K3 ``itq3_rotate_act`` + K4 ``itq3_gemv`` on the tiled layout
 (block_n 256, variant s, cols % 256 == 0), else the generic fp64 kernel
 ``itq3_matmul_generic`` (any block size / variant / row-straddling blocks).
@@ -21,6 +23,7 @@ from .codec import QuantizedTensor
 from .errors import DomainError, ShapeError
 
 PARITY_LIMBS = 6
+MMQ_MIN_TOKENS = 16  # perf mode: k >= 16 columns go to the tcgen05 MMQ kernel (csrc/mmq.cu)
 
 
 def perf_limbs(m: int) -> int:
@@ -32,6 +35,16 @@ def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, 
     dev = X.device
     rows, cols = q.rows, q.cols
     k = X.shape[1]
+    if q.fast_layout() and out_dtype != torch.float64 and k >= MMQ_MIN_TOKENS:
+        mmq = q.mmq_layout()
+        s = _lib.stream_ptr(dev)
+        act = torch.empty(_lib.load().itq3_mmq_act_nbytes(cols, k), dtype=torch.uint8, device=dev)
+        _lib.call("itq3_rotate_act_f16", _lib.ptr(X), _lib.TORCH_DTYPE_CODE[X.dtype], cols, k, X.stride(0),
+                  X.stride(1), _lib.ptr(act), s)
+        Y = torch.empty((rows, k), dtype=out_dtype, device=dev)
+        _lib.call("itq3_mmq", _lib.ptr(mmq), rows, cols, int(not q.symmetric), _lib.ptr(act), k, _lib.ptr(Y),
+                  _lib.TORCH_DTYPE_CODE[out_dtype], Y.stride(0), Y.stride(1), s)
+        return Y
     if q.fast_layout():
         tiled = q.tiled()
         act = torch.empty(_lib.load().itq3_act_nbytes(cols, k, limbs), dtype=torch.uint8, device=dev)

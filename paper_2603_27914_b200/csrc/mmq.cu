@@ -1,0 +1,431 @@
+// K5: batched MMQ on the 5th-gen tensor cores (tcgen05.mma kind::f16, TMEM accumulators).
+//
+// Y[r, m] = sum_b (1/16) <d_rb t_rb, H x_bm> with t = c - 1 - z (the rotated-activation identity,
+// see gemv.cu).  A = d * t is EXACT in binary16 (d is the stored f16 scale, t in {-2..2}), so
+// the whole K reduction stays in one fp32 TMEM accumulator with no per-block promotion; the
+// only approximation is B = f16(H x / 16).
+//
+// Per CTA: 128 weight rows x BN tokens.  Warp roles (6 warps):
+//   warp 0    producer: cp.async.bulk of the 2-bit code slab (128 rows x 64 k = 2 KB) and of the
+//             pre-swizzled activation tile (BN x 64 k f16) per K-chunk into a STAGES-deep ring;
+//   warp 1    MMA issuer (one thread): 4 x tcgen05.mma (K = 16) per chunk, tcgen05.commit frees
+//             the slot; the final commit signals the epilogue;
+//   warps 2-5 expanders, one weight row per thread: 2-bit codes -> f16 d*t written in the
+//             SWIZZLE_128B K-major canonical layout (magic-number decode: 4 ops per f16x2; exact
+//             while 2|d| < 65504),
+//             then the epilogue (tcgen05.ld 32x32b -> fp32/bf16 stores).
+// Layouts written by itq3_repack_mmq / itq3_rotate_act_f16 (host ABI below).
+#include "common.cuh"
+
+namespace itq3 {
+
+constexpr int kMmqBM = 128;
+constexpr int kMmqBK = 64;  // one 128-byte swizzle atom of f16 per row
+constexpr int kMmqThreads = 192;
+constexpr int kMmqCodeChunk = kMmqBM * 16;  // 2 KB: 128 rows x 64 codes x 2 bits
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init_(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "W_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra W_%=;\n}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row core groups 1024 B apart.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+// Instruction descriptor: D f32, A/B f16, both K-major, N = BN, M = 128.
+template <int BN>
+__device__ __forceinline__ uint32_t umma_idesc_f16() {
+    return (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kMmqBM >> 4) << 24);
+}
+
+template <int BN, int STAGES>
+struct MmqSmem {
+    uint8_t a[STAGES][kMmqBM * 128];   // expanded f16 A tiles (1024-aligned)
+    uint8_t b[STAGES][BN * 128];       // activation tiles (pre-swizzled in global)
+    uint8_t codes[STAGES][kMmqCodeChunk];
+    uint64_t full[STAGES];   // codes + B landed (TMA)
+    uint64_t aready[STAGES]; // A expanded (128 expander threads)
+    uint64_t empty[STAGES];  // MMA consumed the slot (tcgen05.commit)
+    uint64_t accum;          // all MMAs done
+    uint32_t tmem_base;
+};
+
+// swizzled byte offset of (row r, 16-byte chunk j) inside a K-major SW128 tile
+__device__ __forceinline__ uint32_t sw128_off(int r, int j) {
+    return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((j ^ (r & 7)) << 4));
+}
+
+template <int BN, int STAGES, typename TY>
+__global__ void __launch_bounds__(kMmqThreads, 1)
+    mmq_kernel(const uint8_t* __restrict__ codes, const uint16_t* __restrict__ scales, const int8_t* __restrict__ zps,
+               int rows_pad, int NC, const uint8_t* __restrict__ act, int64_t rows, int64_t M, TY* __restrict__ y,
+               int64_t stride_r, int64_t stride_m) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-byte alignment for the swizzled tiles
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    MmqSmem<BN, STAGES>& sm = *reinterpret_cast<MmqSmem<BN, STAGES>*>(base);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rt = blockIdx.x, nt = blockIdx.y;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init_(&sm.full[s], 1);
+            mbar_init_(&sm.aready[s], 128);
+            mbar_init_(&sm.empty[s], 1);
+        }
+        mbar_init_(&sm.accum, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {  // TMEM allocation (whole warp), BN fp32 columns x 128 lanes
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&sm.tmem_base)),
+                     "r"(BN < 32 ? 32 : BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = sm.tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint8_t* cbase = codes + (int64_t)rt * kMmqCodeChunk;
+            const uint8_t* bbase = act + (int64_t)nt * NC * BN * 128;
+            for (int kc = 0; kc < NC; ++kc) {
+                const int s = kc % STAGES;
+                const unsigned ph = (unsigned)(kc / STAGES) & 1u;
+                mbar_wait_(&sm.empty[s], ph ^ 1u);
+                mbar_expect_tx_(&sm.full[s], kMmqCodeChunk + BN * 128);
+                bulk_g2s_(sm.codes[s], cbase + (int64_t)kc * rows_pad * 16, kMmqCodeChunk, &sm.full[s]);
+                bulk_g2s_(sm.b[s], bbase + (int64_t)kc * BN * 128, BN * 128, &sm.full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = umma_idesc_f16<BN>();
+            for (int kc = 0; kc < NC; ++kc) {
+                const int s = kc % STAGES;
+                const unsigned ph = (unsigned)(kc / STAGES) & 1u;
+                mbar_wait_(&sm.aready[s], ph);
+                mbar_wait_(&sm.full[s], ph);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t a0 = smem_addr(sm.a[s]), b0 = smem_addr(sm.b[s]);
+#pragma unroll
+                for (int k = 0; k < kMmqBK / 16; ++k) {
+                    const uint64_t ad = umma_desc_sw128(a0 + 32 * k), bd = umma_desc_sw128(b0 + 32 * k);
+                    const uint32_t acc = (kc | k) != 0;
+                    asm volatile(
+                        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_addr(&sm.empty[s]))
+                             : "memory");
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_addr(&sm.accum))
+                         : "memory");
+        }
+    } else {
+        // ---- expanders: thread -> row r (TMEM lane quarter of this warp) ----
+        const int quarter = warp & 3;
+        const int r = quarter * 32 + lane;
+        const int64_t grow = (int64_t)rt * kMmqBM + r;
+        uint32_t d2 = 0, ndz2 = 0;
+        int cur_b = -1;
+        for (int kc = 0; kc < NC; ++kc) {
+            const int s = kc % STAGES;
+            const unsigned ph = (unsigned)(kc / STAGES) & 1u;
+            const int b = kc >> 2;  // 256-block (4 chunks of 64)
+            if (b != cur_b) {
+                cur_b = b;
+                const uint16_t dh = __ldg(scales + (int64_t)b * rows_pad + rt * kMmqBM + r);
+                const int z = zps ? (int)__ldg(zps + (int64_t)b * rows_pad + rt * kMmqBM + r) : 0;
+                const __half d = __ushort_as_half(dh);
+                const __half ndz = __hmul(d, __int2half_rn(-1 - z));  // exact: -(1 + z) in {0,-1,-2}
+                d2 = (uint32_t)dh | ((uint32_t)dh << 16);
+                ndz2 = (uint32_t)__half_as_ushort(ndz) * 0x10001u;
+            }
+            // wait for the slot to be free for A (previous MMA on this slot done) and codes landed
+            mbar_wait_(&sm.empty[s], ph ^ 1u);
+            mbar_wait_(&sm.full[s], ph);
+            const uint4 w4 = reinterpret_cast<const uint4*>(sm.codes[s])[r];
+            const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+            uint8_t* atile = sm.a[s];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {  // 16-byte chunk j = k in [8j, 8j+8)
+                const uint32_t w = wv[j >> 1];
+                uint32_t out[4];
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    const int m = 4 * (j & 1) + p;  // pair (k, k+1) = (16*(j/2) + 2m, +1)
+                    const uint32_t v = ((w >> (2 * m)) & 0x00030003u) | 0x64006400u;  // f16x2 1024 + c
+                    __half2 h = __hsub2(*reinterpret_cast<const __half2*>(&v), __floats2half2_rn(1024.f, 1024.f));
+                    // d * c - d * (1 + z) = d * t: the exact result is an f16, so the FMA returns it
+                    h = __hfma2(h, *reinterpret_cast<const __half2*>(&d2), *reinterpret_cast<const __half2*>(&ndz2));
+                    out[p] = *reinterpret_cast<uint32_t*>(&h);
+                }
+                *reinterpret_cast<uint4*>(atile + sw128_off(r, j)) = make_uint4(out[0], out[1], out[2], out[3]);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+            mbar_arrive_(&sm.aready[s]);
+        }
+        // ---- epilogue: TMEM lane r, columns = tokens ----
+        mbar_wait_(&sm.accum, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+            uint32_t v[32];
+            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0;
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                  "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                  "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                  "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (grow < rows) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int64_t m = (int64_t)nt * BN + c0 + i;
+                    if (m < M) y[grow * stride_r + m * stride_m] = (TY)__uint_as_float(v[i]);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Repack: container payload (block_n 256, variant s, cols % 256 == 0) -> MMQ layout
+//   codes  [NC = cols/64][rows_pad][4 x u32]  (word w of a row's 64-chunk holds k = 16w..16w+15:
+//          bits 2m..2m+1 = code of k = 16w + 2m, bits 16+2m.. = k = 16w + 2m + 1)
+//   scales [NB][rows_pad] f16,  zps [NB][rows_pad] int8 (asymmetric only)
+// ------------------------------------------------------------------------------------------
+__global__ void repack_mmq_kernel(const uint8_t* __restrict__ payload, int64_t rows, int rows_pad, int NB, int asym,
+                                  uint8_t* __restrict__ out) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (row, 64-chunk)
+    const int NC = NB * 4;
+    if (idx >= (int64_t)rows_pad * NC) return;
+    const int64_t row = idx / NC;
+    const int kc = (int)(idx % NC);
+    uint32_t* codes = reinterpret_cast<uint32_t*>(out);
+    uint16_t* scales = reinterpret_cast<uint16_t*>(out + (int64_t)NC * rows_pad * 16);
+    int8_t* zps = reinterpret_cast<int8_t*>(out + (int64_t)NC * rows_pad * 16 + (int64_t)NB * rows_pad * 2);
+    uint32_t w[4] = {0, 0, 0, 0};
+    const int b = kc >> 2;
+    if (row < rows) {
+        const uint8_t* blk = payload + (row * NB + b) * 100;
+        const int kbase = (kc & 3) * 64;
+        const uint32_t p0 = *reinterpret_cast<const uint32_t*>(blk + (kbase >> 3));
+        const uint32_t p0b = *reinterpret_cast<const uint32_t*>(blk + (kbase >> 3) + 4);
+        const uint32_t p1 = *reinterpret_cast<const uint32_t*>(blk + 32 + (kbase >> 3));
+        const uint32_t p1b = *reinterpret_cast<const uint32_t*>(blk + 32 + (kbase >> 3) + 4);
+        const uint64_t P0 = (uint64_t)p0 | ((uint64_t)p0b << 32), P1 = (uint64_t)p1 | ((uint64_t)p1b << 32);
+        for (int kk = 0; kk < 64; ++kk) {
+            const uint32_t c = (uint32_t)((P0 >> kk) & 1u) | ((uint32_t)((P1 >> kk) & 1u) << 1);
+            const int wi = kk >> 4, wk = kk & 15;
+            const int bit = (wk & 1) ? 16 + 2 * (wk >> 1) : 2 * (wk >> 1);
+            w[wi] |= c << bit;
+        }
+        if ((kc & 3) == 0) {
+            scales[(int64_t)b * rows_pad + row] = *reinterpret_cast<const uint16_t*>(blk + 96);
+            if (asym) zps[(int64_t)b * rows_pad + row] = (int8_t)(int)f16_bits_to_f64(*reinterpret_cast<const uint16_t*>(blk + 98));
+        }
+    } else if ((kc & 3) == 0) {
+        scales[(int64_t)b * rows_pad + row] = 0;
+        if (asym) zps[(int64_t)b * rows_pad + row] = 0;
+    }
+    reinterpret_cast<uint4*>(codes)[(int64_t)kc * rows_pad + row] = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// ------------------------------------------------------------------------------------------
+// Activation rotation for MMQ: x'' = (H_256 x_b) / 16 in f16, written pre-swizzled as
+// [token tile][64-chunk][BN rows x 128 B] (SW128 K-major canonical layout); padding = 0.
+// One warp per (256-block, token); butterfly in fp32.
+// ------------------------------------------------------------------------------------------
+template <typename TX>
+__global__ void rotate_act_f16_kernel(const TX* __restrict__ x, int64_t NB, int64_t M, int64_t M_pad,
+                                      int64_t stride_k, int64_t stride_m, int BN, uint8_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wid >= NB * M_pad) return;
+    const int64_t b = wid % NB, m = wid / NB;
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = m < M ? (float)x[(b * 256 + lane + 32 * e) * stride_k + m * stride_m] : 0.f;
+#pragma unroll
+    for (int h = 1; h < 32; h <<= 1) {
+        const bool high = (lane & h) != 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const float p = __shfl_xor_sync(FULL, v[e], h);
+            v[e] = high ? p - v[e] : v[e] + p;
+        }
+    }
+#pragma unroll
+    for (int hh = 1; hh < 8; hh <<= 1)
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if ((e & hh) == 0) {
+                const float lo = v[e], hi = v[e + hh];
+                v[e] = lo + hi;
+                v[e + hh] = lo - hi;
+            }
+    const int64_t NC = NB * 4;
+    const int64_t tile = m / BN;
+    const int r = (int)(m % BN);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int k = 256 * (int)b + lane + 32 * e;  // global k
+        const int64_t kc = k >> 6;
+        const int kk = k & 63;
+        uint8_t* t = out + ((tile * NC + kc) * BN) * 128;
+        *reinterpret_cast<__half*>(t + sw128_off(r, kk >> 3) + (kk & 7) * 2) = __float2half_rn(v[e] * 0.0625f);
+    }
+}
+
+}  // namespace itq3
+
+using namespace itq3;
+
+static int mmq_rows_pad(int64_t rows) { return (int)((rows + kMmqBM - 1) / kMmqBM * kMmqBM); }
+
+extern "C" int64_t itq3_mmq_nbytes(int64_t rows, int64_t cols, int asymmetric) {
+    const int64_t rp = mmq_rows_pad(rows), NB = cols / 256;
+    return NB * 4 * rp * 16 + NB * rp * 2 + (asymmetric ? NB * rp : 0);
+}
+
+extern "C" int itq3_repack_mmq(const uint8_t* payload, int64_t rows, int64_t cols, int asymmetric, uint8_t* out,
+                               void* stream) {
+    if (rows <= 0 || cols <= 0 || cols % 256) {
+        set_error("itq3_repack_mmq: needs cols %% 256 == 0 (got %lld x %lld)", (long long)rows, (long long)cols);
+        return ITQ3_E_UNSUPPORTED;
+    }
+    const int rp = mmq_rows_pad(rows);
+    const int NB = (int)(cols / 256);
+    const int64_t n = (int64_t)rp * NB * 4;
+    repack_mmq_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(payload, rows, rp, NB, asymmetric,
+                                                                                     out);
+    return check_launch("itq3_repack_mmq");
+}
+
+extern "C" int itq3_mmq_block_n(int64_t m) { return m <= 64 ? 64 : (m <= 128 ? 128 : 256); }
+
+extern "C" int64_t itq3_mmq_act_nbytes(int64_t cols, int64_t m) {
+    const int BN = itq3_mmq_block_n(m);
+    const int64_t M_pad = (m + BN - 1) / BN * BN;
+    return M_pad * cols * 2;
+}
+
+extern "C" int itq3_rotate_act_f16(const void* x, int x_dtype, int64_t cols, int64_t m, int64_t stride_k,
+                                   int64_t stride_m, uint8_t* out, void* stream) {
+    if (cols <= 0 || cols % 256 || m <= 0) {
+        set_error("itq3_rotate_act_f16: need cols %% 256 == 0 and m > 0");
+        return ITQ3_E_SHAPE;
+    }
+    const int BN = itq3_mmq_block_n(m);
+    const int64_t NB = cols / 256, M_pad = (m + BN - 1) / BN * BN;
+    const int64_t threads = NB * M_pad * 32;
+    const unsigned grid = (unsigned)((threads + 255) / 256);
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (x_dtype) {
+        case ITQ3_F32:
+            rotate_act_f16_kernel<float><<<grid, 256, 0, s>>>((const float*)x, NB, m, M_pad, stride_k, stride_m, BN, out);
+            break;
+        case ITQ3_F64:
+            rotate_act_f16_kernel<double><<<grid, 256, 0, s>>>((const double*)x, NB, m, M_pad, stride_k, stride_m, BN,
+                                                               out);
+            break;
+        case ITQ3_BF16:
+            rotate_act_f16_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, NB, m, M_pad, stride_k,
+                                                                      stride_m, BN, out);
+            break;
+        case ITQ3_F16:
+            rotate_act_f16_kernel<__half><<<grid, 256, 0, s>>>((const __half*)x, NB, m, M_pad, stride_k, stride_m, BN,
+                                                               out);
+            break;
+        default:
+            set_error("itq3_rotate_act_f16: unsupported dtype %d", x_dtype);
+            return ITQ3_E_DOMAIN;
+    }
+    return check_launch("itq3_rotate_act_f16");
+}
+
+template <int BN, typename TY>
+static int launch_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym, const uint8_t* act, int64_t m, TY* y,
+                      int64_t sr, int64_t sm_, cudaStream_t s) {
+    constexpr int STAGES = BN == 256 ? 3 : 4;
+    const int smem = (int)sizeof(MmqSmem<BN, STAGES>) + 1024;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(mmq_kernel<BN, STAGES, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+            cudaSuccess)
+            return check_launch("itq3_mmq: smem attribute");
+        attr = true;
+    }
+    const int rp = mmq_rows_pad(rows);
+    const int NB = (int)(cols / 256), NC = NB * 4;
+    const uint8_t* codes = mmq;
+    const uint16_t* scales = reinterpret_cast<const uint16_t*>(mmq + (int64_t)NC * rp * 16);
+    const int8_t* zps = asym ? reinterpret_cast<const int8_t*>(mmq + (int64_t)NC * rp * 16 + (int64_t)NB * rp * 2) : nullptr;
+    const dim3 grid((unsigned)(rp / kMmqBM), (unsigned)((m + BN - 1) / BN));
+    mmq_kernel<BN, STAGES, TY><<<grid, kMmqThreads, smem, s>>>(codes, scales, zps, rp, NC, act, rows, m, y, sr, sm_);
+    return check_launch("itq3_mmq");
+}
+
+extern "C" int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asymmetric, const uint8_t* act, int64_t m,
+                        void* y, int y_dtype, int64_t stride_r, int64_t stride_m, void* stream) {
+    if (rows <= 0 || cols <= 0 || cols % 256 || m <= 0) {
+        set_error("itq3_mmq: bad shape");
+        return ITQ3_E_SHAPE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const int BN = itq3_mmq_block_n(m);
+    if (y_dtype == ITQ3_F32) {
+        if (BN == 64) return launch_mmq<64>(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, s);
+        if (BN == 128) return launch_mmq<128>(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, s);
+        return launch_mmq<256>(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, s);
+    }
+    if (y_dtype == ITQ3_BF16) {
+        if (BN == 64) return launch_mmq<64>(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, s);
+        if (BN == 128)
+            return launch_mmq<128>(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, s);
+        return launch_mmq<256>(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, s);
+    }
+    set_error("itq3_mmq: output dtype must be float32 or bfloat16");
+    return ITQ3_E_DOMAIN;
+}

@@ -1,0 +1,58 @@
+"""GPU: K5 tcgen05 MMQ (csrc/mmq.cu) vs the exact fp64 product of the oracle-decoded weights.
+
+Tolerance: A = d*t is exact in f16, so the error comes only from the f16
+rounding of the rotated activations x'' = H x / 16 (relative 2^-11 per element) and the fp32
+butterfly / tensor-core accumulation:
+    |err| <= sum_{b,k} |d t_k| (2^-10 |x''_k| + 2^-18 |x_b|_1 / 16) + 1e-5 sum |w_hat| |x|.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import itq3_oracle as O
+
+pytestmark = pytest.mark.gpu
+P = pytest.importorskip("paper_2603_27914_b200")
+
+
+def mmq_bound(payload, rows, cols, X):
+    n = 256
+    nb = cols // n
+    deq = O.dequantize(payload, rows, cols, n, False)
+    quants, sb, zb, _ = O.split_payload(payload, n, False)
+    codes, _ = O.unpack_planes(quants, n)
+    t = codes.astype(np.float64) - np.trunc(O.f16_value(zb))[:, None]
+    a = np.abs(t * O.f16_value(sb)[:, None]).reshape(rows, cols)        # |d t| per (row, k)
+    Xd = np.asarray(X, np.float64)
+    xr = O.butterfly(Xd.T.reshape(-1, nb, n)).reshape(-1, cols).T / 16.0  # x'' (cols x m)
+    l1 = np.abs(Xd).reshape(nb, n, -1).sum(axis=1)                      # (nb, m)
+    term = 2.0 ** -10 * np.abs(xr) + 2.0 ** -18 * np.repeat(l1, n, axis=0) / 16.0
+    return deq @ Xd, a @ term + 1e-5 * (np.abs(deq) @ np.abs(Xd))
+
+
+@pytest.mark.parametrize("rows,cols", [(300, 512), (128, 1024), (1000, 256)])
+@pytest.mark.parametrize("m", [16, 64, 100, 256, 300])
+@pytest.mark.parametrize("asym", [False, True])
+def test_mmq_matches_exact(rows, cols, m, asym):
+    rng = np.random.default_rng(rows + cols + m)
+    w = rng.standard_normal((rows, cols)) * 0.05
+    q = P.quantize_tensor(w, P.QuantConfig(symmetric=not asym))
+    X = rng.standard_normal((cols, m)).astype(np.float32)
+    Y = P.fused_matmul(q, torch.from_numpy(X).cuda()).cpu().numpy().astype(np.float64)
+    exact, bound = mmq_bound(q.payload().cpu().numpy(), rows, cols, X)
+    assert np.all(np.abs(Y - exact) <= bound), np.max(np.abs(Y - exact) / bound)
+
+
+def test_mmq_dtypes_and_strides():
+    rng = np.random.default_rng(5)
+    q = P.quantize_tensor(rng.standard_normal((256, 768)) * 0.1)
+    X = torch.from_numpy(rng.standard_normal((768, 40)).astype(np.float32)).cuda()
+    Y = P.fused_matmul(q, X)
+    for dt in (torch.bfloat16, torch.float16):
+        Yd = P.fused_matmul(q, X.to(dt)).cpu().numpy()
+        exact, bound = mmq_bound(q.payload().cpu().numpy(), 256, 768, X.to(dt).float().cpu().numpy())
+        assert np.all(np.abs(Yd - exact) <= bound)
+    # token-major activations (M x K transposed view) -> identical result
+    Y2 = P.fused_matmul(q, X.t().contiguous().t())
+    torch.testing.assert_close(Y, Y2, rtol=0, atol=0)
