@@ -1,0 +1,75 @@
+"""C3 sweep: batched MMQ (tcgen05, csrc/mmq.cu) at Llama-3-8B shapes x M = 16..2048.
+
+    python tools/mmq_sweep.py [--out profiles/r01/mmq_sweep.json]
+Times itq3_rotate_act_f16 + itq3_mmq with CUDA events (20 reps after 3 warm-ups, weights of
+>= 2 distinct copies rotated to defeat L2 at small M), reports TFLOPS = 2*rows*K*M / t and the
+fraction of the measured dense bf16/f16 peak (MEASURED_PEAKS.json).
+"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2603_27914_b200 as P  # noqa: E402
+from paper_2603_27914_b200 import _lib  # noqa: E402
+
+SHAPES = [(4096, 4096), (1024, 4096), (14336, 4096), (4096, 14336)]
+MS = [16, 32, 64, 128, 256, 512, 1024, 2048]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--reps", type=int, default=20)
+    args = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    peak = peaks["bf16_tflops"]
+    lib = _lib.load()
+    res = []
+    for rows, K in SHAPES:
+        g = torch.Generator(device=dev)
+        g.manual_seed(rows + K)
+        copies = []
+        ncopy = max(2, int(160e6 // (rows * K * 66 / 256)) + 1)
+        for c in range(min(ncopy, 8)):
+            q = P.quantize_tensor(torch.randn((rows, K), generator=g, device=dev) / K ** 0.5)
+            copies.append(q.mmq_layout())
+        for M in MS:
+            X = torch.randn((K, M), generator=g, device=dev)
+            act = torch.empty(lib.itq3_mmq_act_nbytes(K, M), dtype=torch.uint8, device=dev)
+            Y = torch.empty((rows, M), dtype=torch.float32, device=dev)
+            s = _lib.stream_ptr(dev)
+
+            def run(i):
+                _lib.call("itq3_rotate_act_f16", _lib.ptr(X), _lib.F32, K, M, X.stride(0), X.stride(1),
+                          _lib.ptr(act), s)
+                _lib.call("itq3_mmq", _lib.ptr(copies[i % len(copies)]), rows, K, 0, _lib.ptr(act), M, _lib.ptr(Y),
+                          _lib.F32, Y.stride(0), Y.stride(1), s)
+
+            for i in range(3):
+                run(i)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for i in range(args.reps):
+                run(i)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / args.reps
+            tf = 2.0 * rows * K * M / (ms * 1e-3) / 1e12
+            wbytes = rows * K * 66 / 256
+            r = {"rows": rows, "K": K, "M": M, "us": ms * 1e3, "tflops": tf, "frac_of_bf16_peak": tf / peak,
+                 "weight_gbps": wbytes / (ms * 1e-3) / 1e9}
+            res.append(r)
+            print(json.dumps(r), flush=True)
+    if args.out:
+        json.dump({"peak_bf16_tflops": peak, "results": res}, open(args.out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
