@@ -134,17 +134,18 @@ int itq3_unpack_codes(const uint8_t* planes, int64_t n_rows, int n, int8_t* code
  * cooperative launch (csrc/chain.cu).  Stage i multiplies its tiled weights by the first
  * cols_i entries of stage i-1's output (stage 0: x0).  A stage with K > 16 blocks is split in
  * nch = ceil(cols/4096) K-chunks computed by different CTAs; its y buffer holds nch partial
- * rows-vectors ([nch][rows] fp32) that the consumer sums in fixed order.  The caller fills a
- * host descriptor array with itq3_chain_write_desc (itq3_chain_desc_nbytes() bytes/stage),
- * copies it to device memory and passes a u32 counter array of n_stages entries that is ZERO
- * before every launch.  `out` receives the last stage's rows outputs.  d_trace (optional):
+ * rows-vectors of 64-bit tagged words ([nch][rows] u64: low = fp32 bits, high = step epoch,
+ * zero-initialised once) that the consumer sums in fixed order.  The caller fills a host
+ * descriptor array with itq3_chain_write_desc (itq3_chain_desc_nbytes() bytes/stage), copies
+ * it to device memory and passes one device u32 epoch word (zero-initialised once; the call
+ * increments it on the stream before the launch).  `out` receives the last stage's outputs.  d_trace (optional):
  * n_ctas*n_stages*4 u64 globaltimer stamps for profiling. */
 int64_t itq3_chain_desc_nbytes(void);
 int itq3_chain_act_block_bytes(int limbs);
 int itq3_chain_smem_bytes(void);
-int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* tiled, float* y, uint8_t* act, int64_t rows,
+int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* tiled, void* y, uint8_t* act, int64_t rows,
                           int64_t cols, int asymmetric, int ycnt_off);
-int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_counters, float* out,
+int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch, float* out,
                    int grid, void* d_trace, void* stream);
 
 /* ---- scalar binary16 codec (host): encode_f16 / decode_f16 (packing.py:87-109) */

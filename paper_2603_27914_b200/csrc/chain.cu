@@ -7,13 +7,13 @@
 //     stream runs ahead across stage boundaries and HBM never idles on a dependency;
 //   * 16 consumer warps compute each unit with m16n8k32 u8 x s8 MMAs (same fragment
 //     algebra as gemv.cu) against the stage's rotated activations held in shared memory;
-//   * the 16 warps never synchronise per unit: each writes its partial for the slot and the
-//     LAST warp to finish (shared-memory counter) reduces it in fixed order, finalises the
-//     16-row tile (deterministic across chunks of K) and publishes it with one release
-//     increment of the stage's done counter;
-//   * at a stage boundary every CTA waits for done[s-1] == RT_{s-1}, then rotates the new
-//     input (FWHT + fixed-point limbs, the K3 math) itself into shared memory: no extra
-//     global hop for the activation.
+//   * the 16 consumer warps take balanced contiguous tile ranges of the CTA's units (crossing
+//     unit boundaries); a unit split over several warps is summed by its last segment in
+//     segment order (deterministic);
+//   * no counters, flags or fences between stages: every output word is 64 bits = (fp32 value,
+//     step epoch), stored and loaded single-copy atomically, so a consumer warp simply spins
+//     until the 256 x nch tags of the block it needs carry the current epoch, then rotates that
+//     block (FWHT + fixed-point limbs, the K3 math) straight into shared memory.
 // Co-residency of all CTAs (required by the spin waits) is guaranteed by a cooperative
 // launch sized to one CTA per SM.
 #include <cooperative_groups.h>
@@ -35,7 +35,7 @@ constexpr int kMaxLimbs = 4;
 
 struct ChainStage {
     const uint8_t* tiled;  // codes | scales | zps (itq3_repack_tiled layout)
-    float* y;              // rows outputs (fp32)
+    unsigned long long* y; // [nch][rows] tagged outputs: low 32 = fp32 bits, high 32 = step epoch
     uint8_t* act;          // NB x act_block_bytes: rotated input of this stage
     int64_t rows, cols;
     int32_t NB, RT, asym, reserved;
@@ -96,14 +96,44 @@ __device__ __forceinline__ void mma_u8s8_c(int (&c)[4], uint32_t a0, uint32_t a1
 // |q| <= 2^(8L-2) with one more power-of-two shift k (tests/test_gpu_stack.py chain_bound).
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((e + 127) << 23); }  // e in [-126, 127]
 
-__device__ void chain_rotate_to_smem(const float* src, int nparts, int64_t part_stride, int L, uint8_t* img,
-                                     int lane) {
+__device__ __forceinline__ unsigned long long ld_u64_relaxed(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_u64_relaxed(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Wait for, and sum, one 256-block of a producing stage's tagged K-chunk partials.  Each 64-bit
+// word carries its value and the step epoch in one single-copy-atomic access, so the consumer
+// needs no flag, counter or fence: it spins until all 256 x nparts tags equal `epoch`.
+__device__ __forceinline__ void load_tagged_block(const unsigned long long* src, int nparts, int64_t part_stride,
+                                                  unsigned epoch, int lane, float (&f)[8]) {
+    for (;;) {
+        bool ok = true;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const unsigned long long w = ld_u64_relaxed(src + lane + 32 * e);
+            ok &= (unsigned)(w >> 32) == epoch;
+            f[e] = __uint_as_float((unsigned)w);
+        }
+        for (int c = 1; c < nparts; ++c)  // K-chunk partials, fixed order
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const unsigned long long w = ld_u64_relaxed(src + c * part_stride + lane + 32 * e);
+                ok &= (unsigned)(w >> 32) == epoch;
+                f[e] += __uint_as_float((unsigned)w);
+            }
+        if (__all_sync(FULL, ok)) return;
+        __nanosleep(64);
+    }
+}
+
+__device__ void chain_rotate_to_smem(const float (&fin)[8], int L, uint8_t* img, int lane) {
     float f[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) f[e] = __ldcg(src + lane + 32 * e);
-    for (int c = 1; c < nparts; ++c)  // K-chunk partials of the producing stage, fixed order
-#pragma unroll
-        for (int e = 0; e < 8; ++e) f[e] += __ldcg(src + c * part_stride + lane + 32 * e);
+    for (int e = 0; e < 8; ++e) f[e] = fin[e];
     float fmaxa = 0.f;
 #pragma unroll
     for (int e = 0; e < 8; ++e) fmaxa = fmaxf(fmaxa, fabsf(f[e]));
@@ -209,14 +239,17 @@ __device__ __forceinline__ bool stage_split(const ChainStage& st, int cta, int G
 // trace (optional): per (cta, stage) globaltimer stamps
 //   0 stage entered, 1 input observed ready, 2 input rotated, 3 own units done
 // 17 warps: the per-SMSP register file (16K) caps a 5-warp SMSP at 96 registers/thread
+__global__ void chain_epoch_kernel(unsigned* epoch) { *epoch += 1; }
+
 __global__ void __launch_bounds__(kChainThreads, 1)
     chain_kernel(const ChainStage* __restrict__ stages, int S, const float* __restrict__ x0, int L,
-                 unsigned* __restrict__ done, float* __restrict__ out, unsigned long long* __restrict__ trace) {
+                 const unsigned* __restrict__ epoch_ptr, float* __restrict__ out,
+                 unsigned long long* __restrict__ trace) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     ChainSmem& sm = *reinterpret_cast<ChainSmem*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int cta = blockIdx.x, G = gridDim.x;
-    const int ab = act_block_bytes(L);
+    const unsigned epoch = *epoch_ptr;
 
     if (tid == 0) {
         for (int i = 0; i < kNumSlots; ++i) {
@@ -267,30 +300,23 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         const ChainStage st = stages[s];
         StageSplit sp;
         const bool active = stage_split(st, cta, G, s, sp);
-        if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 0] = globaltimer();
-        // publish the previous stage's units (one cumulative fence per CTA) and wait for all
-        if (s > 0) {
-            const ChainStage pv = stages[s - 1];
-            const unsigned total = (unsigned)pv.RT * (unsigned)((pv.NB + kUnitBlocks - 1) / kUnitBlocks);
-            if (tid == 0 && active) {
-                while (ld_relaxed(&done[s - 1]) < total) {
-                }
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");
-            }
-            consumer_sync();
-        }
         if (!active) continue;
-        if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 1] = globaltimer();
+        if (s > 0) consumer_sync();  // every warp is done reading sm.act of the previous stage
+        if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 0] = globaltimer();
         const int b0 = sp.ch * kUnitBlocks;
         const int nb = min(kUnitBlocks, st.NB - b0);
         if (warp < nb) {
+            float f[8];
             if (s == 0) {
-                chain_rotate_to_smem(x0 + 256 * (b0 + warp), 1, 0, L, sm.act + warp * kActSmemBlock, lane);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) f[e] = __ldg(x0 + 256 * (b0 + warp) + lane + 32 * e);
             } else {
                 const ChainStage pv = stages[s - 1];
                 const int pn = (pv.NB + kUnitBlocks - 1) / kUnitBlocks;
-                chain_rotate_to_smem(pv.y + 256 * (b0 + warp), pn, pv.rows, L, sm.act + warp * kActSmemBlock, lane);
+                load_tagged_block(pv.y + 256 * (b0 + warp), pn, pv.rows, epoch, lane, f);
             }
+            if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 1] = globaltimer();
+            chain_rotate_to_smem(f, L, sm.act + warp * kActSmemBlock, lane);
         }
         consumer_sync();
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 2] = globaltimer();
@@ -300,7 +326,8 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         // unit covered by several warps ("segments") is summed by its last segment in segment
         // order (deterministic); every warp publishes the units it stored with one release.
         const int n_units_all = (st.RT - 1 - sp.rt0) / sp.Gc + 1;
-        float* yout = st.y + (int64_t)sp.ch * st.rows;
+        unsigned long long* yout = st.y + (int64_t)sp.ch * st.rows;
+        const unsigned long long tag = (unsigned long long)epoch << 32;
         unsigned stored = 0;
         unsigned long long* wtr = (trace && cta == 0) ? trace + (int64_t)G * S * 4 + ((int64_t)s * 16 + warp) * 4 : nullptr;
         // rounds of at most kNumSlots units: a warp never waits on a ring slot more than one
@@ -415,8 +442,8 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             if (store) {
                 if (t == 0) {
                     const int64_t row0 = (int64_t)rt * 16 + g;
-                    if (row0 < st.rows) __stcg(yout + row0, r0);
-                    if (row0 + 8 < st.rows) __stcg(yout + row0 + 8, r1);
+                    if (row0 < st.rows) st_u64_relaxed(yout + row0, tag | __float_as_uint(r0));
+                    if (row0 + 8 < st.rows) st_u64_relaxed(yout + row0 + 8, tag | __float_as_uint(r1));
                 }
                 ++stored;
             }
@@ -424,13 +451,6 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         }
         }  // rounds
         if (wtr && lane == 0) wtr[2] = globaltimer();
-        if (stored) {
-            __syncwarp();
-            if (lane == 0) {
-                __threadfence();
-                atomicAdd(&done[s], stored);
-            }
-        }
         if (wtr && lane == 0) wtr[3] = globaltimer();
         seq += n_units_all;
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 3] = globaltimer();
@@ -438,16 +458,22 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     // publish the last stage, then fold its K-chunk partials into `out` (fixed order)
     const ChainStage last = stages[S - 1];
     const int ln = (last.NB + kUnitBlocks - 1) / kUnitBlocks;
-    const unsigned total = (unsigned)last.RT * (unsigned)ln;
-    if (tid == 0) {
-        while (ld_relaxed(&done[S - 1]) < total) {
+    for (int64_t r = (int64_t)cta * (32 * kChainConsumerWarps) + tid; r < last.rows;
+         r += (int64_t)G * 32 * kChainConsumerWarps) {
+        float v;
+        for (;;) {
+            bool ok = true;
+            unsigned long long w = ld_u64_relaxed(last.y + r);
+            ok &= (unsigned)(w >> 32) == epoch;
+            v = __uint_as_float((unsigned)w);
+            for (int c = 1; c < ln; ++c) {
+                w = ld_u64_relaxed(last.y + c * last.rows + r);
+                ok &= (unsigned)(w >> 32) == epoch;
+                v += __uint_as_float((unsigned)w);
+            }
+            if (ok) break;
+            __nanosleep(64);
         }
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    }
-    consumer_sync();
-    for (int64_t r = (int64_t)cta * (32 * kChainConsumerWarps) + tid; r < last.rows; r += (int64_t)G * 32 * kChainConsumerWarps) {
-        float v = __ldcg(last.y + r);
-        for (int c = 1; c < ln; ++c) v += __ldcg(last.y + c * last.rows + r);
         out[r] = v;
     }
 }
@@ -460,7 +486,7 @@ extern "C" int64_t itq3_chain_desc_nbytes(void) { return (int64_t)sizeof(ChainSt
 extern "C" int itq3_chain_act_block_bytes(int limbs) { return act_block_bytes(limbs); }
 extern "C" int itq3_chain_smem_bytes(void) { return (int)sizeof(ChainSmem); }
 
-extern "C" int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* tiled, float* y, uint8_t* act,
+extern "C" int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* tiled, void* y, uint8_t* act,
                                      int64_t rows, int64_t cols, int asymmetric, int ycnt_off) {
     if (cols % 256 || cols / 256 > kMaxChainNB) {
         set_error("chain: stage %d needs cols %% 256 == 0 and cols <= %d (got %lld)", index, 256 * kMaxChainNB,
@@ -469,7 +495,7 @@ extern "C" int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* 
     }
     ChainStage& st = reinterpret_cast<ChainStage*>(host_desc)[index];
     st.tiled = tiled;
-    st.y = y;
+    st.y = (unsigned long long*)y;
     st.act = act;
     st.rows = rows;
     st.cols = cols;
@@ -480,7 +506,7 @@ extern "C" int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* 
     return ITQ3_OK;
 }
 
-extern "C" int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_counters,
+extern "C" int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch,
                               float* out, int grid, void* d_trace, void* stream) {
     if (limbs < 1 || limbs > kMaxLimbs) {
         set_error("chain: limbs must be in [1, %d]", kMaxLimbs);
@@ -499,6 +525,7 @@ extern "C" int itq3_chain_run(const void* d_desc, int n_stages, const float* x0,
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         grid = sms;
     }
+    chain_epoch_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(d_epoch);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kChainThreads);
@@ -510,7 +537,7 @@ extern "C" int itq3_chain_run(const void* d_desc, int n_stages, const float* x0,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, chain_kernel, (const ChainStage*)d_desc, n_stages, x0, limbs,
-                                             d_counters, out, (unsigned long long*)d_trace);
+                                             (const unsigned*)d_epoch, out, (unsigned long long*)d_trace);
     if (e != cudaSuccess) {
         set_error("chain: launch failed: %s", cudaGetErrorString(e));
         return ITQ3_E_CUDA;

@@ -56,12 +56,13 @@ class LinearStack:
         nd = lib.itq3_chain_desc_nbytes()
         host = ctypes.create_string_buffer(nd * S)
         self.nch = [-(-q.cols // 4096) for q in self.qs]
-        self.yparts = [torch.empty((c, q.rows), dtype=torch.float32, device=self.dev) for c, q in zip(self.nch, self.qs)]
+        # tagged outputs: (fp32 bits | epoch << 32), zero = epoch 0 (never current)
+        self.yparts = [torch.zeros((c, q.rows), dtype=torch.int64, device=self.dev) for c, q in zip(self.nch, self.qs)]
         self.out = torch.empty(self.qs[-1].rows, dtype=torch.float32, device=self.dev)
         for i, q in enumerate(self.qs):
             _lib.check(lib.itq3_chain_write_desc(host, i, _lib.ptr(self.tiled[i]), _lib.ptr(self.yparts[i]), None,
                                                  q.rows, q.cols, int(not q.symmetric), 0))
-        self.counters = torch.zeros(S, dtype=torch.int32, device=self.dev)
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.trace = None
         self.desc = torch.frombuffer(bytearray(host.raw), dtype=torch.uint8).to(self.dev)
 
@@ -75,7 +76,7 @@ class LinearStack:
 
     @property
     def launches_per_step(self) -> int:
-        return 1 if self.mode == "chain" else 2 * len(self.qs)
+        return 2 if self.mode == "chain" else 2 * len(self.qs)  # chain: epoch bump + chain kernel
 
     def step_bytes(self) -> int:
         """Algorithmic bytes of one step: all tiled weights + rotated activations + outputs."""
@@ -100,10 +101,9 @@ class LinearStack:
 
     def launch_all(self) -> None:
         if self.mode == "chain":
-            self.counters.zero_()
             trace = _lib.ptr(self.trace) if self.trace is not None else None
             _lib.call("itq3_chain_run", _lib.ptr(self.desc), len(self.qs), _lib.ptr(self.x), self.limbs,
-                      _lib.ptr(self.counters), _lib.ptr(self.out), 0, trace, _lib.stream_ptr(self.dev))
+                      _lib.ptr(self.epoch), _lib.ptr(self.out), 0, trace, _lib.stream_ptr(self.dev))
             return
         for i in range(len(self.qs)):
             self.launch_stage(i)
@@ -116,7 +116,7 @@ class LinearStack:
         """Stage i's output; in chain mode the K-chunk partials summed in the kernel's order."""
         if self.mode != "chain":
             return self.ys[i]
-        p = self.yparts[i]
+        p = self.yparts[i].view(torch.int32).reshape(self.nch[i], self.qs[i].rows, 2)[..., 0].view(torch.float32)
         y = p[0].clone()
         for c in range(1, p.shape[0]):
             y += p[c]
