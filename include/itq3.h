@@ -138,13 +138,15 @@ int itq3_unpack_codes(const uint8_t* planes, int64_t n_rows, int n, int8_t* code
  * zero-initialised once) that the consumer sums in fixed order.  The caller fills a host
  * descriptor array with itq3_chain_write_desc (itq3_chain_desc_nbytes() bytes/stage), copies
  * it to device memory and passes one device u32 epoch word (zero-initialised once; the call
- * increments it on the stream before the launch).  `out` receives the last stage's outputs.  d_trace (optional):
+ * increments it on the stream before the launch).  `out` receives the last stage's outputs.
+ * A stage whose descriptor has a non-NULL `xin` reads that fp32 vector instead of the previous
+ * stage's output (independent stages: pure weight streaming, used to measure the roofline).  d_trace (optional):
  * n_ctas*n_stages*4 u64 globaltimer stamps for profiling. */
 int64_t itq3_chain_desc_nbytes(void);
 int itq3_chain_act_block_bytes(int limbs);
 int itq3_chain_smem_bytes(void);
-int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* tiled, void* y, uint8_t* act, int64_t rows,
-                          int64_t cols, int asymmetric, int ycnt_off);
+int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* tiled, void* y, const float* xin, int64_t rows,
+                          int64_t cols, int asymmetric, int reserved);
 int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch, float* out,
                    int grid, void* d_trace, void* stream);
 

@@ -29,20 +29,20 @@ constexpr int kSlotCodes = kUnitBlocks * 1024;           // 16 KB
 constexpr int kSlotScales = kUnitBlocks * 32;            // 512 B
 constexpr int kSlotZps = kUnitBlocks * 16;               // 256 B
 constexpr int kSlotBytes = kSlotCodes + kSlotScales + kSlotZps;
-constexpr int kNumSlots = 10;
+constexpr int kNumSlots = 11;
 constexpr int kMaxChainNB = 256;                         // K up to 65536
 constexpr int kMaxLimbs = 4;
 
 struct ChainStage {
     const uint8_t* tiled;  // codes | scales | zps (itq3_repack_tiled layout)
     unsigned long long* y; // [nch][rows] tagged outputs: low 32 = fp32 bits, high 32 = step epoch
-    uint8_t* act;          // NB x act_block_bytes: rotated input of this stage
+    const float* xin;      // optional: untagged fp32 input (independent stage, no dependency)
     int64_t rows, cols;
     int32_t NB, RT, asym, reserved;
 };
 
 __host__ __device__ inline int act_block_bytes(int L) { return 256 * L + 32; }
-constexpr int kActSmemBlock = 8 * 32 * 8 + 64;  // full 8-column fragments + 8 (factor, corr) pairs
+constexpr int kActSmemBlock = 8 * 16 * 8 + 64;  // 4-column fragments [q][g<4][t] + 8 (factor, corr) pairs
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -134,11 +134,12 @@ __device__ void chain_rotate_to_smem(const float (&fin)[8], int L, uint8_t* img,
     float f[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) f[e] = fin[e];
-    float fmaxa = 0.f;
+    // warp max of |f| as an integer max of the (non-negative) float bit patterns: one REDUX
+    unsigned fbits = 0;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) fmaxa = fmaxf(fmaxa, fabsf(f[e]));
-#pragma unroll
-    for (int o = 16; o; o >>= 1) fmaxa = fmaxf(fmaxa, __shfl_xor_sync(FULL, fmaxa, o));
+    for (int e = 0; e < 8; ++e) fbits = max(fbits, __float_as_uint(fabsf(f[e])));
+    fbits = __reduce_max_sync(FULL, fbits);
+    const float fmaxa = __uint_as_float(fbits);
     const int e_in = fmaxa > 0.f ? ilogbf(fmaxa) - 21 : 0;
     const float sc_in = pow2f(-e_in);
     int v[8];
@@ -165,8 +166,7 @@ __device__ void chain_rotate_to_smem(const float (&fin)[8], int L, uint8_t* img,
     unsigned amax = 0;
 #pragma unroll
     for (int e = 0; e < 8; ++e) amax = max(amax, (unsigned)abs(v[e]));
-#pragma unroll
-    for (int o = 16; o; o >>= 1) amax = max(amax, __shfl_xor_sync(FULL, amax, o));
+    amax = __reduce_max_sync(FULL, amax);
     // shift k so that |q| <= 2^(8L-2) (limbs never overflow): bitlen(amax) - k <= 8L - 2
     const int bl = 32 - __clz(amax);
     const int k = max(0, bl - (8 * L - 2));
@@ -185,13 +185,12 @@ __device__ void chain_rotate_to_smem(const float (&fin)[8], int L, uint8_t* img,
             if (l < L) {
                 const int lb = ((q + 128) & 255) - 128;
                 q = (q - lb) >> 8;
-                img[(e * 32 + 4 * l + tt) * 8 + half * 4 + beta] = (uint8_t)(int8_t)lb;
+                img[(e * 16 + 4 * l + tt) * 8 + half * 4 + beta] = (uint8_t)(int8_t)lb;
             }
         }
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) Q += __shfl_xor_sync(FULL, Q, o);
-    float* meta = reinterpret_cast<float*>(img + 8 * 32 * 8);  // f[0..7], corr[0..7]
+    Q = __reduce_add_sync(FULL, Q);
+    float* meta = reinterpret_cast<float*>(img + 8 * 16 * 8);  // f[0..7], corr[0..7]
     if (lane < L) {
         meta[lane] = ldexpf(1.0f, 8 * lane + ex - 4);
         meta[8 + lane] = lane == 0 ? ldexpf((float)Q, ex - 4) : 0.0f;
@@ -200,8 +199,8 @@ __device__ void chain_rotate_to_smem(const float (&fin)[8], int L, uint8_t* img,
 
 struct ChainSmem {
     uint8_t ring[kNumSlots][kSlotBytes];
-    uint8_t act[kUnitBlocks * kActSmemBlock];  // the CTA's K-chunk of the stage input (full fragments)
-    float part[kNumSlots][kChainConsumerWarps][16];       // per-segment row partials of a unit
+    uint8_t rot[kChainConsumerWarps][kActSmemBlock];   // per-warp rotation scratch (own block only)
+    float part[kNumSlots][kChainConsumerWarps][16];    // per-warp row partials of a unit
     uint64_t full[kNumSlots];
     uint64_t empty[kNumSlots];
     int partcnt[kNumSlots];
@@ -294,168 +293,132 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     }
 
     // ------------------------------ consumers ------------------------------
+    // K-stationary: warp w owns 256-block b0 + w of the CTA's K-chunk for the whole stage.  It
+    // rotates that block itself (no cross-warp hand-off, no flags) and keeps the activation
+    // fragments in registers for every unit; each unit's 16 per-warp partials are summed by the
+    // last warp to finish it, in warp order (deterministic).
     const int g = lane >> 2, t = lane & 3;
     int seq = 0;  // CTA-wide unit sequence number (ring slot = seq % kNumSlots)
+    uint8_t* rot = sm.rot[warp];
     for (int s = 0; s < S; ++s) {
         const ChainStage st = stages[s];
         StageSplit sp;
-        const bool active = stage_split(st, cta, G, s, sp);
-        if (!active) continue;
-        if (s > 0) consumer_sync();  // every warp is done reading sm.act of the previous stage
+        if (!stage_split(st, cta, G, s, sp)) continue;
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 0] = globaltimer();
         const int b0 = sp.ch * kUnitBlocks;
         const int nb = min(kUnitBlocks, st.NB - b0);
-        if (warp < nb) {
+        const bool has_block = warp < nb;
+        uint2 bf[8];
+        float fcx = 0.f, corr = 0.f;
+        if (has_block) {
             float f[8];
-            if (s == 0) {
+            if (s == 0 || st.xin) {
+                const float* xs = st.xin ? st.xin : x0;
 #pragma unroll
-                for (int e = 0; e < 8; ++e) f[e] = __ldg(x0 + 256 * (b0 + warp) + lane + 32 * e);
+                for (int e = 0; e < 8; ++e) f[e] = __ldg(xs + 256 * (b0 + warp) + lane + 32 * e);
             } else {
                 const ChainStage pv = stages[s - 1];
                 const int pn = (pv.NB + kUnitBlocks - 1) / kUnitBlocks;
                 load_tagged_block(pv.y + 256 * (b0 + warp), pn, pv.rows, epoch, lane, f);
             }
             if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 1] = globaltimer();
-            chain_rotate_to_smem(f, L, sm.act + warp * kActSmemBlock, lane);
+            chain_rotate_to_smem(f, L, rot, lane);
+            __syncwarp();
+            // fragments for lane (g, t): columns g < 4 hold limbs, columns >= 4 are zero
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                bf[q] = g < 4 ? reinterpret_cast<const uint2*>(rot)[(q * 4 + g) * 4 + t] : make_uint2(0u, 0u);
+            const float2 fc = reinterpret_cast<const float2*>(rot + 8 * 16 * 8)[t];       // f[2t], f[2t+1]
+            const float2 cc = reinterpret_cast<const float2*>(rot + 8 * 16 * 8 + 32)[t];  // corr[2t], corr[2t+1]
+            fcx = fc.x;  // columns 2t, 2t+1 = limbs 2t, 2t+1: factors differ by exactly 256
+            corr = cc.x + cc.y;
         }
-        consumer_sync();
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 2] = globaltimer();
-
-        // The stage's T = n_units * nb tiles (unit j = row tile rt0 + j*Gc, tiles in K order) are
-        // split into min(16, T) balanced contiguous ranges, one per warp, crossing unit boundaries.  A
-        // unit covered by several warps ("segments") is summed by its last segment in segment
-        // order (deterministic); every warp publishes the units it stored with one release.
-        const int n_units_all = (st.RT - 1 - sp.rt0) / sp.Gc + 1;
+        const int n_units = (st.RT - 1 - sp.rt0) / sp.Gc + 1;
         unsigned long long* yout = st.y + (int64_t)sp.ch * st.rows;
         const unsigned long long tag = (unsigned long long)epoch << 32;
-        unsigned stored = 0;
-        unsigned long long* wtr = (trace && cta == 0) ? trace + (int64_t)G * S * 4 + ((int64_t)s * 16 + warp) * 4 : nullptr;
-        // rounds of at most kNumSlots units: a warp never waits on a ring slot more than one
-        // mbarrier phase ahead of its last release (no parity aliasing for any stage size)
-        for (int u0 = 0; u0 < n_units_all; u0 += kNumSlots) {
-        if (u0 > 0) consumer_sync();
-        const int n_units = min(kNumSlots, n_units_all - u0);
-        const int T = n_units * nb;
-        const int nw = min(kChainConsumerWarps, T);  // every active warp gets >= 1 tile
-        const int tau0 = warp < nw ? warp * T / nw : 0, tau1 = warp < nw ? (warp + 1) * T / nw : 0;
-        auto warp_of = [&](int tau) { return (nw * (tau + 1) + T - 1) / T - 1; };
-        if (wtr && lane == 0 && u0 == 0) wtr[0] = globaltimer();
-        bool first_wait = u0 == 0;
-        int tau = tau0;
-        while (tau < tau1) {
-            const int j = tau / nb;
-            const int bb_lo = tau - j * nb;
-            const int bb_hi = min(nb, tau1 - j * nb);
-            const int rt = sp.rt0 + (u0 + j) * sp.Gc;
-            const int useq = seq + u0 + j;
-            const int slot = useq % kNumSlots;
-            const unsigned phase = (unsigned)(useq / kNumSlots) & 1u;
-            const int w_first = warp_of(j * nb), w_last = warp_of(j * nb + nb - 1);
-            const int nseg = w_last - w_first + 1;
-            mbar_wait(&sm.full[slot], phase);
-            if (wtr && lane == 0 && first_wait) wtr[1] = globaltimer();
-            first_wait = false;
-            const uint8_t* ring = sm.ring[slot];
-            float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
-#pragma unroll 2
-            for (int bb = bb_lo; bb < bb_hi; ++bb) {
-                const uint4 wa0 = reinterpret_cast<const uint4*>(ring + bb * 1024)[lane];
-                const uint4 wa1 = reinterpret_cast<const uint4*>(ring + bb * 1024 + 512)[lane];
-                const uint32_t sc = reinterpret_cast<const uint32_t*>(ring + kSlotCodes + bb * 32)[g];
-                const uint8_t* a = sm.act + bb * kActSmemBlock;
-                uint2 bf[8];
+        for (int u0 = 0; u0 < n_units; u0 += kNumSlots) {
+            // rounds of at most kNumSlots units: no warp waits a ring slot more than one phase ahead
+            if (u0 > 0) consumer_sync();
+            const int u1 = min(n_units, u0 + kNumSlots);
+            for (int j = u0; j < u1; ++j) {
+                const int rt = sp.rt0 + j * sp.Gc;
+                const int useq = seq + j;
+                const int slot = useq % kNumSlots;
+                mbar_wait(&sm.full[slot], (unsigned)(useq / kNumSlots) & 1u);
+                const uint8_t* ring = sm.ring[slot];
+                float r0 = 0.f, r1 = 0.f;
+                if (has_block) {
+                    const uint4 wa0 = reinterpret_cast<const uint4*>(ring + warp * 1024)[lane];
+                    const uint4 wa1 = reinterpret_cast<const uint4*>(ring + warp * 1024 + 512)[lane];
+                    const uint32_t sc = reinterpret_cast<const uint32_t*>(ring + kSlotCodes + warp * 32)[g];
+                    int C[4][4];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) bf[q] = reinterpret_cast<const uint2*>(a)[q * 32 + lane];
-                // columns 2t, 2t+1 are limbs 2t, 2t+1 of the token: factors differ by exactly 256
-                const float2 fc = reinterpret_cast<const float2*>(a + 8 * 32 * 8)[t];       // f[2t], f[2t+1]
-                const float2 cc = reinterpret_cast<const float2*>(a + 8 * 32 * 8 + 32)[t];  // corr[2t], corr[2t+1]
-                int C[4][4];
+                    for (int i = 0; i < 4; ++i) C[i][0] = C[i][1] = C[i][2] = C[i][3] = 0;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) C[i][0] = C[i][1] = C[i][2] = C[i][3] = 0;
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t mk = 0x03030303u << (2 * i);
+                        mma_u8s8_c(C[i], wa0.x & mk, wa0.y & mk, wa0.z & mk, wa0.w & mk, bf[i].x, bf[i].y);
+                    }
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const uint32_t mk = 0x03030303u << (2 * i);
-                    mma_u8s8_c(C[i], wa0.x & mk, wa0.y & mk, wa0.z & mk, wa0.w & mk, bf[i].x, bf[i].y);
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t mk = 0x03030303u << (2 * i);
+                        mma_u8s8_c(C[i], wa1.x & mk, wa1.y & mk, wa1.z & mk, wa1.w & mk, bf[4 + i].x, bf[4 + i].y);
+                    }
+                    int Cc[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) Cc[r] = C[0][r] + (C[1][r] >> 2) + (C[2][r] >> 4) + (C[3][r] >> 6);
+                    // |Cc| <= 2^16, so Cc[even] + 256 * Cc[odd] is exact in int32 (< 2^25)
+                    const float v0 = (float)(Cc[0] + 256 * Cc[1]), v1 = (float)(Cc[2] + 256 * Cc[3]);
+                    const float d0 = f16_bits_to_f32((uint16_t)(sc & 0xffffu));
+                    const float d1 = f16_bits_to_f32((uint16_t)(sc >> 16));
+                    float zf0 = 1.f, zf1 = 1.f;
+                    if (st.asym) {
+                        const uint16_t zz = reinterpret_cast<const uint16_t*>(ring + kSlotCodes + kSlotScales + warp * 16)[g];
+                        zf0 = (float)(1 + (int)(int8_t)(zz & 0xff));
+                        zf1 = (float)(1 + (int)(int8_t)(zz >> 8));
+                    }
+                    r0 = d0 * (fcx * v0 - zf0 * corr);
+                    r1 = d1 * (fcx * v1 - zf1 * corr);
+                    // combine the quad's limb-pair columns (lanes t = 0..3, fixed order)
+                    r0 += __shfl_xor_sync(FULL, r0, 1);
+                    r1 += __shfl_xor_sync(FULL, r1, 1);
+                    r0 += __shfl_xor_sync(FULL, r0, 2);
+                    r1 += __shfl_xor_sync(FULL, r1, 2);
                 }
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const uint32_t mk = 0x03030303u << (2 * i);
-                    mma_u8s8_c(C[i], wa1.x & mk, wa1.y & mk, wa1.z & mk, wa1.w & mk, bf[4 + i].x, bf[4 + i].y);
-                }
-                int Cc[4];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) Cc[r] = C[0][r] + (C[1][r] >> 2) + (C[2][r] >> 4) + (C[3][r] >> 6);
-                // |Cc| <= 2^16, so Cc[even] + 256 * Cc[odd] is exact in int32 (< 2^25)
-                const float v0 = (float)(Cc[0] + 256 * Cc[1]), v1 = (float)(Cc[2] + 256 * Cc[3]);
-                const float corr = cc.x + cc.y;
-                const float d0 = f16_bits_to_f32((uint16_t)(sc & 0xffffu));
-                const float d1 = f16_bits_to_f32((uint16_t)(sc >> 16));
-                float zf0 = 1.f, zf1 = 1.f;
-                if (st.asym) {
-                    const uint16_t zz = reinterpret_cast<const uint16_t*>(ring + kSlotCodes + kSlotScales + bb * 16)[g];
-                    zf0 = (float)(1 + (int)(int8_t)(zz & 0xff));
-                    zf1 = (float)(1 + (int)(int8_t)(zz >> 8));
-                }
-                acc[0][0] += d0 * (fc.x * v0 - zf0 * corr);
-                acc[1][0] += d1 * (fc.x * v1 - zf1 * corr);
-            }
-            // combine limb-pair columns over the quad (lanes t = 0..3, fixed order)
-            float r0 = acc[0][0], r1 = acc[1][0];
-            r0 += __shfl_xor_sync(FULL, r0, 1);
-            r1 += __shfl_xor_sync(FULL, r1, 1);
-            r0 += __shfl_xor_sync(FULL, r0, 2);
-            r1 += __shfl_xor_sync(FULL, r1, 2);
-            bool store = nseg == 1;
-            if (nseg > 1) {
-                const int segi = warp - w_first;
                 if (t == 0) {
-                    sm.part[slot][segi][g] = r0;
-                    sm.part[slot][segi][g + 8] = r1;
+                    sm.part[slot][warp][g] = r0;
+                    sm.part[slot][warp][g + 8] = r1;
                 }
                 __syncwarp();
                 int last = 0;
                 if (lane == 0) {
                     __threadfence_block();
-                    last = atomicAdd(&sm.partcnt[slot], 1) == nseg - 1;
+                    last = atomicAdd(&sm.partcnt[slot], 1) == kChainConsumerWarps - 1;
                 }
                 last = __shfl_sync(FULL, last, 0);
                 if (last) {
                     __threadfence_block();
-                    if (t == 0) {
-                        r0 = r1 = 0.f;
-                        for (int p2 = 0; p2 < nseg; ++p2) {
-                            r0 += sm.part[slot][p2][g];
-                            r1 += sm.part[slot][p2][g + 8];
-                        }
+                    if (lane < 16) {
+                        float part[kChainConsumerWarps];
+#pragma unroll
+                        for (int w = 0; w < kChainConsumerWarps; ++w) part[w] = sm.part[slot][w][lane];
+                        float sum = part[0];
+#pragma unroll
+                        for (int w = 1; w < kChainConsumerWarps; ++w) sum += part[w];
+                        const int64_t row = (int64_t)rt * 16 + lane;
+                        if (row < st.rows) st_u64_relaxed(yout + row, tag | __float_as_uint(sum));
                     }
                     if (lane == 0) sm.partcnt[slot] = 0;
-                    store = true;
+                    __syncwarp();
                 }
-                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.empty[slot]);
             }
-            // release the slot: every segment arrives once, the first also for absent warps
-            if (lane == 0) {
-                const unsigned cnt = warp == w_first ? (unsigned)(kChainConsumerWarps - nseg + 1) : 1u;
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&sm.empty[slot])), "r"(cnt)
-                             : "memory");
-            }
-            if (store) {
-                if (t == 0) {
-                    const int64_t row0 = (int64_t)rt * 16 + g;
-                    if (row0 < st.rows) st_u64_relaxed(yout + row0, tag | __float_as_uint(r0));
-                    if (row0 + 8 < st.rows) st_u64_relaxed(yout + row0 + 8, tag | __float_as_uint(r1));
-                }
-                ++stored;
-            }
-            tau = (j + 1) * nb;
         }
-        }  // rounds
-        if (wtr && lane == 0) wtr[2] = globaltimer();
-        if (wtr && lane == 0) wtr[3] = globaltimer();
-        seq += n_units_all;
+        seq += n_units;
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 3] = globaltimer();
     }
-    // publish the last stage, then fold its K-chunk partials into `out` (fixed order)
+    // fold the last stage's K-chunk partials into `out` (fixed order), waiting on the tags
     const ChainStage last = stages[S - 1];
     const int ln = (last.NB + kUnitBlocks - 1) / kUnitBlocks;
     for (int64_t r = (int64_t)cta * (32 * kChainConsumerWarps) + tid; r < last.rows;
@@ -486,7 +449,7 @@ extern "C" int64_t itq3_chain_desc_nbytes(void) { return (int64_t)sizeof(ChainSt
 extern "C" int itq3_chain_act_block_bytes(int limbs) { return act_block_bytes(limbs); }
 extern "C" int itq3_chain_smem_bytes(void) { return (int)sizeof(ChainSmem); }
 
-extern "C" int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* tiled, void* y, uint8_t* act,
+extern "C" int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* tiled, void* y, const float* xin,
                                      int64_t rows, int64_t cols, int asymmetric, int ycnt_off) {
     if (cols % 256 || cols / 256 > kMaxChainNB) {
         set_error("chain: stage %d needs cols %% 256 == 0 and cols <= %d (got %lld)", index, 256 * kMaxChainNB,
@@ -496,7 +459,7 @@ extern "C" int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* 
     ChainStage& st = reinterpret_cast<ChainStage*>(host_desc)[index];
     st.tiled = tiled;
     st.y = (unsigned long long*)y;
-    st.act = act;
+    st.xin = xin;
     st.rows = rows;
     st.cols = cols;
     st.NB = (int)(cols / 256);

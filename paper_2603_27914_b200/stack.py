@@ -23,7 +23,7 @@ class LinearStack:
     """mode="chain": one persistent cooperative kernel per step (csrc/chain.cu, default);
     mode="kernels": 2 launches per stage (K3 rotate_act + K4 gemv), for comparison."""
 
-    def __init__(self, qs: list[QuantizedTensor], limbs: int = 3, mode: str = "chain"):
+    def __init__(self, qs: list[QuantizedTensor], limbs: int = 3, mode: str = "chain", independent: bool = False):
         if not qs:
             raise ShapeError("LinearStack: no stages")
         for a, b in zip(qs, qs[1:]):
@@ -43,6 +43,7 @@ class LinearStack:
         self.ys = [torch.empty(q.rows, dtype=torch.float32, device=self.dev) for q in qs]
         self.graph = None
         self.mode = mode
+        self.independent = independent  # every stage reads x (no dependency): pure streaming
         if mode == "chain":
             self._setup_chain()
         elif mode != "kernels":
@@ -60,7 +61,11 @@ class LinearStack:
         self.yparts = [torch.zeros((c, q.rows), dtype=torch.int64, device=self.dev) for c, q in zip(self.nch, self.qs)]
         self.out = torch.empty(self.qs[-1].rows, dtype=torch.float32, device=self.dev)
         for i, q in enumerate(self.qs):
-            _lib.check(lib.itq3_chain_write_desc(host, i, _lib.ptr(self.tiled[i]), _lib.ptr(self.yparts[i]), None,
+            xin = None
+            if self.independent:
+                self._xin = getattr(self, "_xin", torch.randn(max(qq.cols for qq in self.qs), device=self.dev))
+                xin = _lib.ptr(self._xin)
+            _lib.check(lib.itq3_chain_write_desc(host, i, _lib.ptr(self.tiled[i]), _lib.ptr(self.yparts[i]), xin,
                                                  q.rows, q.cols, int(not q.symmetric), 0))
         self.epoch = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.trace = None
