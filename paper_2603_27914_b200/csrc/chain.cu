@@ -203,6 +203,7 @@ struct ChainSmem {
     float part[kNumSlots][kChainConsumerWarps][16];    // per-warp row partials of a unit
     uint64_t full[kNumSlots];
     uint64_t empty[kNumSlots];
+    uint64_t parts[kNumSlots];  // 16 warps' partials of the unit in this slot are written
     int partcnt[kNumSlots];
 };
 
@@ -254,6 +255,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         for (int i = 0; i < kNumSlots; ++i) {
             mbar_init(&sm.full[i], 1);
             mbar_init(&sm.empty[i], kChainConsumerWarps);
+            mbar_init(&sm.parts[i], kChainConsumerWarps);
             sm.partcnt[i] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -391,14 +393,10 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                     sm.part[slot][warp][g + 8] = r1;
                 }
                 __syncwarp();
-                int last = 0;
-                if (lane == 0) {
-                    __threadfence_block();
-                    last = atomicAdd(&sm.partcnt[slot], 1) == kChainConsumerWarps - 1;
-                }
-                last = __shfl_sync(FULL, last, 0);
-                if (last) {
-                    __threadfence_block();
+                if (lane == 0) mbar_arrive(&sm.parts[slot]);  // release: this warp's partials are in
+                if (warp == (useq & (kChainConsumerWarps - 1))) {
+                    // designated reducer of this unit (rotates over the warps): sum in warp order
+                    mbar_wait(&sm.parts[slot], (unsigned)(useq / kNumSlots) & 1u);
                     if (lane < 16) {
                         float part[kChainConsumerWarps];
 #pragma unroll
@@ -409,7 +407,6 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                         const int64_t row = (int64_t)rt * 16 + lane;
                         if (row < st.rows) st_u64_relaxed(yout + row, tag | __float_as_uint(sum));
                     }
-                    if (lane == 0) sm.partcnt[slot] = 0;
                     __syncwarp();
                 }
                 if (lane == 0) mbar_arrive(&sm.empty[slot]);
