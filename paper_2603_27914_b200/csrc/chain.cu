@@ -23,7 +23,8 @@
 namespace itq3 {
 
 constexpr int kChainConsumerWarps = 16;
-constexpr int kChainThreads = 32 * (kChainConsumerWarps + 1);
+constexpr int kChainThreads = 32 * (kChainConsumerWarps + 2);  // + producer warp + reducer warp
+constexpr int kProducerWarp = kChainConsumerWarps, kReducerWarp = kChainConsumerWarps + 1;
 constexpr int kUnitBlocks = 16;                          // 256-blocks per unit (one per consumer warp)
 constexpr int kSlotCodes = kUnitBlocks * 1024;           // 16 KB
 constexpr int kSlotScales = kUnitBlocks * 32;            // 512 B
@@ -238,7 +239,7 @@ __device__ __forceinline__ bool stage_split(const ChainStage& st, int cta, int G
 
 // trace (optional): per (cta, stage) globaltimer stamps
 //   0 stage entered, 1 input observed ready, 2 input rotated, 3 own units done
-// 17 warps: the per-SMSP register file (16K) caps a 5-warp SMSP at 96 registers/thread
+// 18 warps: the per-SMSP register file (16K) caps a 5-warp SMSP at 96 registers/thread
 __global__ void chain_epoch_kernel(unsigned* epoch) { *epoch += 1; }
 
 __global__ void __launch_bounds__(kChainThreads, 1)
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     if (tid == 0) {
         for (int i = 0; i < kNumSlots; ++i) {
             mbar_init(&sm.full[i], 1);
-            mbar_init(&sm.empty[i], kChainConsumerWarps);
+            mbar_init(&sm.empty[i], kChainConsumerWarps + 1);  // compute warps + reducer
             mbar_init(&sm.parts[i], kChainConsumerWarps);
             sm.partcnt[i] = 0;
         }
@@ -262,7 +263,41 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     }
     __syncthreads();
 
-    if (warp == kChainConsumerWarps) {
+    if (warp == kReducerWarp) {
+        // ------------------------------ reducer ------------------------------
+        // Sums each unit's 16 per-warp row partials in warp order (deterministic), stores the
+        // tagged outputs and releases the ring slot.  Runs behind the compute warps so they
+        // never wait on each other.
+        int seq = 0;
+        for (int s = 0; s < S; ++s) {
+            const ChainStage st = stages[s];
+            StageSplit sp;
+            if (!stage_split(st, cta, G, s, sp)) continue;
+            const int n_units = (st.RT - 1 - sp.rt0) / sp.Gc + 1;
+            unsigned long long* yout = st.y + (int64_t)sp.ch * st.rows;
+            const unsigned long long tag = (unsigned long long)epoch << 32;
+            for (int j = 0; j < n_units; ++j) {
+                const int useq = seq + j;
+                const int slot = useq % kNumSlots;
+                mbar_wait(&sm.parts[slot], (unsigned)(useq / kNumSlots) & 1u);
+                if (lane < 16) {
+                    float part[kChainConsumerWarps];
+#pragma unroll
+                    for (int w = 0; w < kChainConsumerWarps; ++w) part[w] = sm.part[slot][w][lane];
+                    float sum = part[0];
+#pragma unroll
+                    for (int w = 1; w < kChainConsumerWarps; ++w) sum += part[w];
+                    const int64_t row = (int64_t)(sp.rt0 + j * sp.Gc) * 16 + lane;
+                    if (row < st.rows) st_u64_relaxed(yout + row, tag | __float_as_uint(sum));
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.empty[slot]);
+            }
+            seq += n_units;
+        }
+        return;
+    }
+    if (warp == kProducerWarp) {
         // ------------------------------ producer ------------------------------
         if (lane == 0) {
             int slot = 0;
@@ -337,8 +372,6 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         }
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 2] = globaltimer();
         const int n_units = (st.RT - 1 - sp.rt0) / sp.Gc + 1;
-        unsigned long long* yout = st.y + (int64_t)sp.ch * st.rows;
-        const unsigned long long tag = (unsigned long long)epoch << 32;
         for (int u0 = 0; u0 < n_units; u0 += kNumSlots) {
             // rounds of at most kNumSlots units: no warp waits a ring slot more than one phase ahead
             if (u0 > 0) consumer_sync();
@@ -393,23 +426,10 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                     sm.part[slot][warp][g + 8] = r1;
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.parts[slot]);  // release: this warp's partials are in
-                if (warp == (useq & (kChainConsumerWarps - 1))) {
-                    // designated reducer of this unit (rotates over the warps): sum in warp order
-                    mbar_wait(&sm.parts[slot], (unsigned)(useq / kNumSlots) & 1u);
-                    if (lane < 16) {
-                        float part[kChainConsumerWarps];
-#pragma unroll
-                        for (int w = 0; w < kChainConsumerWarps; ++w) part[w] = sm.part[slot][w][lane];
-                        float sum = part[0];
-#pragma unroll
-                        for (int w = 1; w < kChainConsumerWarps; ++w) sum += part[w];
-                        const int64_t row = (int64_t)rt * 16 + lane;
-                        if (row < st.rows) st_u64_relaxed(yout + row, tag | __float_as_uint(sum));
-                    }
-                    __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&sm.parts[slot]);  // release: this warp's partials are in
+                    mbar_arrive(&sm.empty[slot]);  // done reading the slot (reducer arrives too)
                 }
-                if (lane == 0) mbar_arrive(&sm.empty[slot]);
             }
         }
         seq += n_units;
