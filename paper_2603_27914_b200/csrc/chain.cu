@@ -198,6 +198,42 @@ __device__ void chain_rotate_to_smem(const float (&fin)[8], int L, uint8_t* img,
     }
 }
 
+// One 16-row x 256-k tile of the warp's block from a ring slot: returns the (row g, row g+8)
+// contributions of this lane's limb-pair columns (before the quad combine).
+__device__ __forceinline__ float2 chain_tile(const uint8_t* ring, int warp, int lane, int g, const uint2 (&bf)[8],
+                                             float fcx, float corr, int asym) {
+    const uint4 wa0 = reinterpret_cast<const uint4*>(ring + warp * 1024)[lane];
+    const uint4 wa1 = reinterpret_cast<const uint4*>(ring + warp * 1024 + 512)[lane];
+    const uint32_t sc = reinterpret_cast<const uint32_t*>(ring + kSlotCodes + warp * 32)[g];
+    int C[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) C[i][0] = C[i][1] = C[i][2] = C[i][3] = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t mk = 0x03030303u << (2 * i);
+        mma_u8s8_c(C[i], wa0.x & mk, wa0.y & mk, wa0.z & mk, wa0.w & mk, bf[i].x, bf[i].y);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t mk = 0x03030303u << (2 * i);
+        mma_u8s8_c(C[i], wa1.x & mk, wa1.y & mk, wa1.z & mk, wa1.w & mk, bf[4 + i].x, bf[4 + i].y);
+    }
+    int Cc[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) Cc[r] = C[0][r] + (C[1][r] >> 2) + (C[2][r] >> 4) + (C[3][r] >> 6);
+    // |Cc| <= 2^16, so Cc[even] + 256 * Cc[odd] is exact in int32 (< 2^25)
+    const float v0 = (float)(Cc[0] + 256 * Cc[1]), v1 = (float)(Cc[2] + 256 * Cc[3]);
+    const float d0 = f16_bits_to_f32((uint16_t)(sc & 0xffffu));
+    const float d1 = f16_bits_to_f32((uint16_t)(sc >> 16));
+    float zf0 = 1.f, zf1 = 1.f;
+    if (asym) {
+        const uint16_t zz = reinterpret_cast<const uint16_t*>(ring + kSlotCodes + kSlotScales + warp * 16)[g];
+        zf0 = (float)(1 + (int)(int8_t)(zz & 0xff));
+        zf1 = (float)(1 + (int)(int8_t)(zz >> 8));
+    }
+    return make_float2(d0 * (fcx * v0 - zf0 * corr), d1 * (fcx * v1 - zf1 * corr));
+}
+
 struct ChainSmem {
     uint8_t ring[kNumSlots][kSlotBytes];
     uint8_t rot[kChainConsumerWarps][kActSmemBlock];   // per-warp rotation scratch (own block only)
@@ -337,6 +373,8 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     const int g = lane >> 2, t = lane & 3;
     int seq = 0;  // CTA-wide unit sequence number (ring slot = seq % kNumSlots)
     uint8_t* rot = sm.rot[warp];
+    const bool prof = trace != nullptr && cta == 0;
+    long long c_wait = 0, c_tile = 0, c_rot = 0, c_start = clock64();
     for (int s = 0; s < S; ++s) {
         const ChainStage st = stages[s];
         StageSplit sp;
@@ -347,6 +385,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         const bool has_block = warp < nb;
         uint2 bf[8];
         float fcx = 0.f, corr = 0.f;
+        long long c0 = prof ? clock64() : 0;
         if (has_block) {
             float f[8];
             if (s == 0 || st.xin) {
@@ -370,70 +409,70 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             fcx = fc.x;  // columns 2t, 2t+1 = limbs 2t, 2t+1: factors differ by exactly 256
             corr = cc.x + cc.y;
         }
+        if (prof) c_rot += clock64() - c0;
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 2] = globaltimer();
         const int n_units = (st.RT - 1 - sp.rt0) / sp.Gc + 1;
         for (int u0 = 0; u0 < n_units; u0 += kNumSlots) {
             // rounds of at most kNumSlots units: no warp waits a ring slot more than one phase ahead
             if (u0 > 0) consumer_sync();
             const int u1 = min(n_units, u0 + kNumSlots);
-            for (int j = u0; j < u1; ++j) {
-                const int rt = sp.rt0 + j * sp.Gc;
-                const int useq = seq + j;
-                const int slot = useq % kNumSlots;
-                mbar_wait(&sm.full[slot], (unsigned)(useq / kNumSlots) & 1u);
-                const uint8_t* ring = sm.ring[slot];
-                float r0 = 0.f, r1 = 0.f;
+            // two units per iteration: their independent dependency chains interleave in the
+            // warp's in-order issue stream (software pipelining across ring slots)
+            for (int j = u0; j < u1; j += 2) {
+                const bool two = j + 1 < u1;
+                const int useq0 = seq + j, useq1 = seq + j + 1;
+                const int slot0 = useq0 % kNumSlots, slot1 = useq1 % kNumSlots;
+                long long c1 = prof ? clock64() : 0;
+                mbar_wait(&sm.full[slot0], (unsigned)(useq0 / kNumSlots) & 1u);
+                if (two) mbar_wait(&sm.full[slot1], (unsigned)(useq1 / kNumSlots) & 1u);
+                if (prof) {
+                    const long long c2 = clock64();
+                    c_wait += c2 - c1;
+                    c1 = c2;
+                }
+                float2 ra = make_float2(0.f, 0.f), rb = make_float2(0.f, 0.f);
                 if (has_block) {
-                    const uint4 wa0 = reinterpret_cast<const uint4*>(ring + warp * 1024)[lane];
-                    const uint4 wa1 = reinterpret_cast<const uint4*>(ring + warp * 1024 + 512)[lane];
-                    const uint32_t sc = reinterpret_cast<const uint32_t*>(ring + kSlotCodes + warp * 32)[g];
-                    int C[4][4];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) C[i][0] = C[i][1] = C[i][2] = C[i][3] = 0;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const uint32_t mk = 0x03030303u << (2 * i);
-                        mma_u8s8_c(C[i], wa0.x & mk, wa0.y & mk, wa0.z & mk, wa0.w & mk, bf[i].x, bf[i].y);
-                    }
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const uint32_t mk = 0x03030303u << (2 * i);
-                        mma_u8s8_c(C[i], wa1.x & mk, wa1.y & mk, wa1.z & mk, wa1.w & mk, bf[4 + i].x, bf[4 + i].y);
-                    }
-                    int Cc[4];
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) Cc[r] = C[0][r] + (C[1][r] >> 2) + (C[2][r] >> 4) + (C[3][r] >> 6);
-                    // |Cc| <= 2^16, so Cc[even] + 256 * Cc[odd] is exact in int32 (< 2^25)
-                    const float v0 = (float)(Cc[0] + 256 * Cc[1]), v1 = (float)(Cc[2] + 256 * Cc[3]);
-                    const float d0 = f16_bits_to_f32((uint16_t)(sc & 0xffffu));
-                    const float d1 = f16_bits_to_f32((uint16_t)(sc >> 16));
-                    float zf0 = 1.f, zf1 = 1.f;
-                    if (st.asym) {
-                        const uint16_t zz = reinterpret_cast<const uint16_t*>(ring + kSlotCodes + kSlotScales + warp * 16)[g];
-                        zf0 = (float)(1 + (int)(int8_t)(zz & 0xff));
-                        zf1 = (float)(1 + (int)(int8_t)(zz >> 8));
-                    }
-                    r0 = d0 * (fcx * v0 - zf0 * corr);
-                    r1 = d1 * (fcx * v1 - zf1 * corr);
+                    ra = chain_tile(sm.ring[slot0], warp, lane, g, bf, fcx, corr, st.asym);
+                    if (two) rb = chain_tile(sm.ring[slot1], warp, lane, g, bf, fcx, corr, st.asym);
                     // combine the quad's limb-pair columns (lanes t = 0..3, fixed order)
-                    r0 += __shfl_xor_sync(FULL, r0, 1);
-                    r1 += __shfl_xor_sync(FULL, r1, 1);
-                    r0 += __shfl_xor_sync(FULL, r0, 2);
-                    r1 += __shfl_xor_sync(FULL, r1, 2);
+                    ra.x += __shfl_xor_sync(FULL, ra.x, 1);
+                    ra.y += __shfl_xor_sync(FULL, ra.y, 1);
+                    rb.x += __shfl_xor_sync(FULL, rb.x, 1);
+                    rb.y += __shfl_xor_sync(FULL, rb.y, 1);
+                    ra.x += __shfl_xor_sync(FULL, ra.x, 2);
+                    ra.y += __shfl_xor_sync(FULL, ra.y, 2);
+                    rb.x += __shfl_xor_sync(FULL, rb.x, 2);
+                    rb.y += __shfl_xor_sync(FULL, rb.y, 2);
                 }
                 if (t == 0) {
-                    sm.part[slot][warp][g] = r0;
-                    sm.part[slot][warp][g + 8] = r1;
+                    sm.part[slot0][warp][g] = ra.x;
+                    sm.part[slot0][warp][g + 8] = ra.y;
+                    if (two) {
+                        sm.part[slot1][warp][g] = rb.x;
+                        sm.part[slot1][warp][g + 8] = rb.y;
+                    }
                 }
                 __syncwarp();
+                if (prof) c_tile += clock64() - c1;
                 if (lane == 0) {
-                    mbar_arrive(&sm.parts[slot]);  // release: this warp's partials are in
-                    mbar_arrive(&sm.empty[slot]);  // done reading the slot (reducer arrives too)
+                    mbar_arrive(&sm.parts[slot0]);  // release: this warp's partials are in
+                    mbar_arrive(&sm.empty[slot0]);  // done reading the slot (reducer arrives too)
+                    if (two) {
+                        mbar_arrive(&sm.parts[slot1]);
+                        mbar_arrive(&sm.empty[slot1]);
+                    }
                 }
             }
         }
         seq += n_units;
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 3] = globaltimer();
+    }
+    if (prof && lane == 0) {
+        unsigned long long* pt = trace + (int64_t)G * S * 4 + (int64_t)S * 64 + warp * 4;
+        pt[0] = c_wait;
+        pt[1] = c_tile;
+        pt[2] = c_rot;
+        pt[3] = clock64() - c_start;
     }
     // fold the last stage's K-chunk partials into `out` (fixed order), waiting on the tags
     const ChainStage last = stages[S - 1];

@@ -24,13 +24,23 @@ def main():
     st = bench.build_stack(args.layers, 1000, dev, "chain")
     tr = st.enable_trace()
     x = np.random.default_rng(0).standard_normal(st.x.numel()).astype(np.float32)
+    ap2 = os.environ.get("TRACE_INDEPENDENT")
+    if ap2:
+        from paper_2603_27914_b200.stack import LinearStack
+        st = LinearStack(st.qs, limbs=3, mode="chain", independent=True)
+        tr = st.enable_trace()
     for _ in range(3):
         st.forward(x)
     raw = tr.cpu().numpy().astype(np.float64)
     S = len(st.qs)
-    G = (raw.size - S * 64) // (S * 4)
+    G = (raw.size - S * 64 - 64) // (S * 4)
     t = raw[: G * S * 4].reshape(G, S, 4)
-    wt = raw[G * S * 4:].reshape(S, 16, 4)
+    wt = raw[G * S * 4: G * S * 4 + S * 64].reshape(S, 16, 4)
+    cyc = raw[G * S * 4 + S * 64:].reshape(16, 4)
+    tot = cyc[:, 3].mean()
+    print("CTA0 compute-warp cycle split (mean over warps): wait_full %.1f%%  tiles %.1f%%  rotate+input %.1f%%  "
+          "(total %.0f cycles)" % (100 * cyc[:, 0].mean() / tot, 100 * cyc[:, 1].mean() / tot,
+                                   100 * cyc[:, 2].mean() / tot, tot))
     t0 = t[:, 0, 0].min()
     t = (t - t0) / 1000.0  # us
     wt = np.where(wt > 0, (wt - t0) / 1000.0, np.nan)
