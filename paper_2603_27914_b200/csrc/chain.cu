@@ -95,7 +95,9 @@ __device__ __forceinline__ void mma_u8s8_c(int (&c)[4], uint32_t a0, uint32_t a1
 // scale s_in = 2^(ilogb(max|y|) - 21) (|y_int| < 2^22, as fine as fp32's own rounding of the
 // largest elements), exact int32 butterfly (|x'| < 2^30), then x' rounded to the limb range
 // |q| <= 2^(8L-2) with one more power-of-two shift k (tests/test_gpu_stack.py chain_bound).
-__device__ __forceinline__ float pow2f(int e) { return __int_as_float((e + 127) << 23); }  // e in [-126, 127]
+__device__ __forceinline__ float pow2f(int e) {  // exact 2^e, bit-built on the normal range
+    return (e >= -126 && e <= 127) ? __int_as_float((e + 127) << 23) : ldexpf(1.0f, e);
+}
 
 __device__ __forceinline__ unsigned long long ld_u64_relaxed(const unsigned long long* p) {
     unsigned long long v;
@@ -174,27 +176,26 @@ __device__ void chain_rotate_to_smem(const float (&fin)[8], int L, uint8_t* img,
     const int ex = e_in + k;
     int Q = 0;
     const int tt = (lane & 15) >> 2, beta = lane & 3, half = lane >> 4;
-    // zero the record (unused columns must read as 0), then scatter the limb bytes
-    for (int i = lane; i < kActSmemBlock / 16; i += 32) reinterpret_cast<uint4*>(img)[i] = make_uint4(0, 0, 0, 0);
-    __syncwarp();
+    // Class folding: chunk e = 4G + i pairs with the A operand c * 4^i (bit pair i of the code
+    // bytes), so its activations are stored pre-scaled by 4^(3-i); every IMMA of a tile then
+    // accumulates 64 * sum(c x') into ONE integer accumulator (no per-tile class recombination).
+    // |q| <= 2^22 -> |q 4^(3-i)| <= 2^28: four balanced base-256 limbs = the bytes of
+    // (qs + 0x80808080) ^ 0x80808080, all four record columns used.
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-        int q = k ? ((v[e] + (1 << (k - 1))) >> k) : v[e];
+        const int q = k ? ((v[e] + (1 << (k - 1))) >> k) : v[e];
         Q += q;
+        const int qs = q << (2 * (3 - (e & 3)));
+        const uint32_t limbs = (uint32_t)(qs + (int)0x80808080u) ^ 0x80808080u;
+        uint8_t* dst = img + (e * 16 + tt) * 8 + half * 4 + beta;  // (chunk e, column 0, t, byte)
 #pragma unroll
-        for (int l = 0; l < kMaxLimbs; ++l) {
-            if (l < L) {
-                const int lb = ((q + 128) & 255) - 128;
-                q = (q - lb) >> 8;
-                img[(e * 16 + 4 * l + tt) * 8 + half * 4 + beta] = (uint8_t)(int8_t)lb;
-            }
-        }
+        for (int l = 0; l < 4; ++l) dst[l * 32] = (uint8_t)(limbs >> (8 * l));  // column l: +4*8 B
     }
     Q = __reduce_add_sync(FULL, Q);
     float* meta = reinterpret_cast<float*>(img + 8 * 16 * 8);  // f[0..7], corr[0..7]
-    if (lane < L) {
-        meta[lane] = ldexpf(1.0f, 8 * lane + ex - 4);
-        meta[8 + lane] = lane == 0 ? ldexpf((float)Q, ex - 4) : 0.0f;
+    if (lane < 8) {
+        meta[lane] = lane < 4 ? pow2f(8 * lane + ex - 10) : 0.0f;  // 256^l 2^ex / 16 / 64
+        meta[8 + lane] = lane == 0 ? (float)Q * pow2f(ex - 4) : 0.0f;
     }
 }
 
@@ -205,24 +206,17 @@ __device__ __forceinline__ float2 chain_tile(const uint8_t* ring, int warp, int 
     const uint4 wa0 = reinterpret_cast<const uint4*>(ring + warp * 1024)[lane];
     const uint4 wa1 = reinterpret_cast<const uint4*>(ring + warp * 1024 + 512)[lane];
     const uint32_t sc = reinterpret_cast<const uint32_t*>(ring + kSlotCodes + warp * 32)[g];
-    int C[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) C[i][0] = C[i][1] = C[i][2] = C[i][3] = 0;
+    int C0[4] = {0, 0, 0, 0}, C1[4] = {0, 0, 0, 0};  // group 0 / group 1 (two 4-deep chains)
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const uint32_t mk = 0x03030303u << (2 * i);
-        mma_u8s8_c(C[i], wa0.x & mk, wa0.y & mk, wa0.z & mk, wa0.w & mk, bf[i].x, bf[i].y);
+        mma_u8s8_c(C0, wa0.x & mk, wa0.y & mk, wa0.z & mk, wa0.w & mk, bf[i].x, bf[i].y);
+        mma_u8s8_c(C1, wa1.x & mk, wa1.y & mk, wa1.z & mk, wa1.w & mk, bf[4 + i].x, bf[4 + i].y);
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const uint32_t mk = 0x03030303u << (2 * i);
-        mma_u8s8_c(C[i], wa1.x & mk, wa1.y & mk, wa1.z & mk, wa1.w & mk, bf[4 + i].x, bf[4 + i].y);
-    }
-    int Cc[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) Cc[r] = C[0][r] + (C[1][r] >> 2) + (C[2][r] >> 4) + (C[3][r] >> 6);
-    // |Cc| <= 2^16, so Cc[even] + 256 * Cc[odd] is exact in int32 (< 2^25)
-    const float v0 = (float)(Cc[0] + 256 * Cc[1]), v1 = (float)(Cc[2] + 256 * Cc[3]);
+    // columns 2t, 2t+1 = limbs 2t, 2t+1 (factors differ by 256); |C| < 2^22, so the pair
+    // combination stays below 2^31
+    const float v0 = (float)((C0[0] + C1[0]) + 256 * (C0[1] + C1[1]));
+    const float v1 = (float)((C0[2] + C1[2]) + 256 * (C0[3] + C1[3]));
     const float d0 = f16_bits_to_f32((uint16_t)(sc & 0xffffu));
     const float d1 = f16_bits_to_f32((uint16_t)(sc >> 16));
     float zf0 = 1.f, zf1 = 1.f;
