@@ -85,7 +85,11 @@ class CpuArm:
 
         self.procs = procs or len(os.sched_getaffinity(0))
         self.rows = rows_per_stage
-        ctx = mp.get_context("fork")
+        # fresh interpreters with single-threaded BLAS: one core per worker, no inherited
+        # thread pools or CUDA state from the parent
+        for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[var] = "1"
+        ctx = mp.get_context("spawn")
         self.pool = ctx.Pool(self.procs, initializer=_cpu_init, initargs=(rows_per_stage, 1234))
         self.weights_per_step = self.procs * rows_per_stage * sum(c for _, _, c in LAYER_SHAPES)
 
