@@ -109,8 +109,11 @@ int itq3_mmq_block_n(int64_t m);
 int64_t itq3_mmq_act_nbytes(int64_t cols, int64_t m);
 int itq3_rotate_act_f16(const void* x, int x_dtype, int64_t cols, int64_t m, int64_t stride_k, int64_t stride_m,
                         uint8_t* out, void* stream);
+/* workspace: itq3_mmq_ws_nbytes(rows, cols, m) bytes (may be 0 -> pass NULL); with a workspace,
+ * small problems are split along K across CTAs and reduced in fixed order (deterministic). */
+int64_t itq3_mmq_ws_nbytes(int64_t rows, int64_t cols, int64_t m);
 int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asymmetric, const uint8_t* act, int64_t m, void* y,
-             int y_dtype, int64_t stride_r, int64_t stride_m, void* stream);
+             int y_dtype, int64_t stride_r, int64_t stride_m, void* workspace, void* stream);
 
 /* ---- generic fused matmul for every other layout (any block_n, variant ss,
  * row-straddling blocks): fp64 exact decode + fp64 dot, deterministic block order.

@@ -42,8 +42,11 @@ def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, 
         _lib.call("itq3_rotate_act_f16", _lib.ptr(X), _lib.TORCH_DTYPE_CODE[X.dtype], cols, k, X.stride(0),
                   X.stride(1), _lib.ptr(act), s)
         Y = torch.empty((rows, k), dtype=out_dtype, device=dev)
+        wsn = _lib.load().itq3_mmq_ws_nbytes(rows, cols, k)
+        ws = torch.empty(wsn, dtype=torch.uint8, device=dev) if wsn else None
         _lib.call("itq3_mmq", _lib.ptr(mmq), rows, cols, int(not q.symmetric), _lib.ptr(act), k, _lib.ptr(Y),
-                  _lib.TORCH_DTYPE_CODE[out_dtype], Y.stride(0), Y.stride(1), s)
+                  _lib.TORCH_DTYPE_CODE[out_dtype], Y.stride(0), Y.stride(1), _lib.ptr(ws) if ws is not None else None,
+                  s)
         return Y
     if q.fast_layout():
         tiled = q.tiled()

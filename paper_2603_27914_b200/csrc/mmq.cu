@@ -21,7 +21,8 @@ namespace itq3 {
 
 constexpr int kMmqBM = 128;
 constexpr int kMmqBK = 64;  // one 128-byte swizzle atom of f16 per row
-constexpr int kMmqThreads = 192;
+constexpr int kMmqExpWarps = 8;  // 2 per weight row (each half of the 64-k chunk)
+constexpr int kMmqThreads = 32 * (2 + kMmqExpWarps);
 constexpr int kMmqCodeChunk = kMmqBM * 16;  // 2 KB: 128 rows x 64 codes x 2 bits
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -68,8 +69,10 @@ struct MmqSmem {
     uint8_t a[STAGES][kMmqBM * 128];   // expanded f16 A tiles (1024-aligned)
     uint8_t b[STAGES][BN * 128];       // activation tiles (pre-swizzled in global)
     uint8_t codes[STAGES][kMmqCodeChunk];
-    uint64_t full[STAGES];   // codes + B landed (TMA)
-    uint64_t aready[STAGES]; // A expanded (128 expander threads)
+    uint16_t scl[STAGES][kMmqBM];  // f16 scales of the chunk's 256-block (bulk-copied with the codes)
+    int8_t zp[STAGES][kMmqBM];
+    uint64_t full[STAGES];   // codes + scales + B landed (TMA)
+    uint64_t aready[STAGES]; // A expanded (all expander threads)
     uint64_t empty[STAGES];  // MMA consumed the slot (tcgen05.commit)
     uint64_t accum;          // all MMAs done
     uint32_t tmem_base;
@@ -84,18 +87,21 @@ template <int BN, int STAGES, typename TY>
 __global__ void __launch_bounds__(kMmqThreads, 1)
     mmq_kernel(const uint8_t* __restrict__ codes, const uint16_t* __restrict__ scales, const int8_t* __restrict__ zps,
                int rows_pad, int NC, const uint8_t* __restrict__ act, int64_t rows, int64_t M, TY* __restrict__ y,
-               int64_t stride_r, int64_t stride_m) {
+               int64_t stride_r, int64_t stride_m, int64_t slab) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for the swizzled tiles
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     MmqSmem<BN, STAGES>& sm = *reinterpret_cast<MmqSmem<BN, STAGES>*>(base);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rt = blockIdx.x, nt = blockIdx.y;
+    // split-K: this CTA reduces K-chunks [kc0, kc1); partial outputs go to slab blockIdx.z
+    const int kc0 = (int)((int64_t)blockIdx.z * NC / gridDim.z), kc1 = (int)((int64_t)(blockIdx.z + 1) * NC / gridDim.z);
+    y += (int64_t)blockIdx.z * slab;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init_(&sm.full[s], 1);
-            mbar_init_(&sm.aready[s], 128);
+            mbar_init_(&sm.aready[s], 32 * kMmqExpWarps);
             mbar_init_(&sm.empty[s], 1);
         }
         mbar_init_(&sm.accum, 1);
@@ -115,21 +121,24 @@ __global__ void __launch_bounds__(kMmqThreads, 1)
         if (lane == 0) {
             const uint8_t* cbase = codes + (int64_t)rt * kMmqCodeChunk;
             const uint8_t* bbase = act + (int64_t)nt * NC * BN * 128;
-            for (int kc = 0; kc < NC; ++kc) {
-                const int s = kc % STAGES;
-                const unsigned ph = (unsigned)(kc / STAGES) & 1u;
+            for (int kc = kc0; kc < kc1; ++kc) {
+                const int s = (kc - kc0) % STAGES;
+                const unsigned ph = (unsigned)((kc - kc0) / STAGES) & 1u;
                 mbar_wait_(&sm.empty[s], ph ^ 1u);
-                mbar_expect_tx_(&sm.full[s], kMmqCodeChunk + BN * 128);
+                const int64_t soff = (int64_t)(kc >> 2) * rows_pad + (int64_t)rt * kMmqBM;
+                mbar_expect_tx_(&sm.full[s], kMmqCodeChunk + BN * 128 + kMmqBM * 2 + (zps ? kMmqBM : 0));
                 bulk_g2s_(sm.codes[s], cbase + (int64_t)kc * rows_pad * 16, kMmqCodeChunk, &sm.full[s]);
                 bulk_g2s_(sm.b[s], bbase + (int64_t)kc * BN * 128, BN * 128, &sm.full[s]);
+                bulk_g2s_(sm.scl[s], scales + soff, kMmqBM * 2, &sm.full[s]);
+                if (zps) bulk_g2s_(sm.zp[s], zps + soff, kMmqBM, &sm.full[s]);
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             const uint32_t idesc = umma_idesc_f16<BN>();
-            for (int kc = 0; kc < NC; ++kc) {
-                const int s = kc % STAGES;
-                const unsigned ph = (unsigned)(kc / STAGES) & 1u;
+            for (int kc = kc0; kc < kc1; ++kc) {
+                const int s = (kc - kc0) % STAGES;
+                const unsigned ph = (unsigned)((kc - kc0) / STAGES) & 1u;
                 mbar_wait_(&sm.aready[s], ph);
                 mbar_wait_(&sm.full[s], ph);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -137,7 +146,7 @@ __global__ void __launch_bounds__(kMmqThreads, 1)
 #pragma unroll
                 for (int k = 0; k < kMmqBK / 16; ++k) {
                     const uint64_t ad = umma_desc_sw128(a0 + 32 * k), bd = umma_desc_sw128(b0 + 32 * k);
-                    const uint32_t acc = (kc | k) != 0;
+                    const uint32_t acc = ((kc - kc0) | k) != 0;
                     asm volatile(
                         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
                         " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
@@ -152,54 +161,51 @@ __global__ void __launch_bounds__(kMmqThreads, 1)
                          : "memory");
         }
     } else {
-        // ---- expanders: thread -> row r (TMEM lane quarter of this warp) ----
+        // ---- expanders: 2 threads per row r (TMEM lane quarter of the warp), half h of the chunk ----
         const int quarter = warp & 3;
+        const int h = (warp - 2) >> 2;  // warps 2-5: h = 0, warps 6-9: h = 1
         const int r = quarter * 32 + lane;
         const int64_t grow = (int64_t)rt * kMmqBM + r;
-        uint32_t d2 = 0, ndz2 = 0;
-        int cur_b = -1;
-        for (int kc = 0; kc < NC; ++kc) {
-            const int s = kc % STAGES;
-            const unsigned ph = (unsigned)(kc / STAGES) & 1u;
-            const int b = kc >> 2;  // 256-block (4 chunks of 64)
-            if (b != cur_b) {
-                cur_b = b;
-                const uint16_t dh = __ldg(scales + (int64_t)b * rows_pad + rt * kMmqBM + r);
-                const int z = zps ? (int)__ldg(zps + (int64_t)b * rows_pad + rt * kMmqBM + r) : 0;
-                const __half d = __ushort_as_half(dh);
-                const __half ndz = __hmul(d, __int2half_rn(-1 - z));  // exact: -(1 + z) in {0,-1,-2}
-                d2 = (uint32_t)dh | ((uint32_t)dh << 16);
-                ndz2 = (uint32_t)__half_as_ushort(ndz) * 0x10001u;
-            }
-            // wait for the slot to be free for A (previous MMA on this slot done) and codes landed
+        for (int kc = kc0; kc < kc1; ++kc) {
+            const int s = (kc - kc0) % STAGES;
+            const unsigned ph = (unsigned)((kc - kc0) / STAGES) & 1u;
+            // the A slot is free once the MMA that read it committed; codes/scales landed
             mbar_wait_(&sm.empty[s], ph ^ 1u);
             mbar_wait_(&sm.full[s], ph);
-            const uint4 w4 = reinterpret_cast<const uint4*>(sm.codes[s])[r];
-            const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+            const uint16_t dh = sm.scl[s][r];
+            const int z = zps ? (int)sm.zp[s][r] : 0;
+            const __half d = __ushort_as_half(dh);
+            const __half ndz = __hmul(d, __int2half_rn(-1 - z));  // exact: -(1 + z) in {0,-1,-2}
+            const uint32_t d2 = (uint32_t)dh | ((uint32_t)dh << 16);
+            const uint32_t ndz2 = (uint32_t)__half_as_ushort(ndz) * 0x10001u;
+            const uint2 w2 = reinterpret_cast<const uint2*>(sm.codes[s])[r * 2 + h];
+            const uint32_t wv[2] = {w2.x, w2.y};
             uint8_t* atile = sm.a[s];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {  // 16-byte chunk j = k in [8j, 8j+8)
-                const uint32_t w = wv[j >> 1];
+            for (int jj = 0; jj < 4; ++jj) {  // 16-byte chunk j = 4h + jj: k in [8j, 8j+8)
+                const int j = 4 * h + jj;
+                const uint32_t w = wv[jj >> 1];
                 uint32_t out[4];
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
-                    const int m = 4 * (j & 1) + p;  // pair (k, k+1) = (16*(j/2) + 2m, +1)
+                    const int m = 4 * (jj & 1) + p;  // pair (k, k+1) = (16*(j/2) + 2m, +1)
                     const uint32_t v = ((w >> (2 * m)) & 0x00030003u) | 0x64006400u;  // f16x2 1024 + c
-                    __half2 h = __hsub2(*reinterpret_cast<const __half2*>(&v), __floats2half2_rn(1024.f, 1024.f));
+                    __half2 hv = __hsub2(*reinterpret_cast<const __half2*>(&v), __floats2half2_rn(1024.f, 1024.f));
                     // d * c - d * (1 + z) = d * t: the exact result is an f16, so the FMA returns it
-                    h = __hfma2(h, *reinterpret_cast<const __half2*>(&d2), *reinterpret_cast<const __half2*>(&ndz2));
-                    out[p] = *reinterpret_cast<uint32_t*>(&h);
+                    hv = __hfma2(hv, *reinterpret_cast<const __half2*>(&d2), *reinterpret_cast<const __half2*>(&ndz2));
+                    out[p] = *reinterpret_cast<uint32_t*>(&hv);
                 }
                 *reinterpret_cast<uint4*>(atile + sw128_off(r, j)) = make_uint4(out[0], out[1], out[2], out[3]);
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
             mbar_arrive_(&sm.aready[s]);
         }
-        // ---- epilogue: TMEM lane r, columns = tokens ----
+        // ---- epilogue: TMEM lane r, this warp's half of the token columns ----
         mbar_wait_(&sm.accum, 0);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        constexpr int HALF = BN / 2;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = h * HALF; c0 < (h + 1) * HALF; c0 += 32) {
             uint32_t v[32];
             const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0;
             asm volatile(
@@ -318,6 +324,17 @@ __global__ void rotate_act_f16_kernel(const TX* __restrict__ x, int64_t NB, int6
     }
 }
 
+template <typename TY>
+__global__ void mmq_splitk_reduce(const float* __restrict__ ws, int ks, int64_t rows, int64_t M, TY* __restrict__ y,
+                                  int64_t stride_r, int64_t stride_m) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows * M) return;
+    const int64_t r = i / M, m = i % M;
+    float v = ws[i];
+    for (int z = 1; z < ks; ++z) v += ws[(int64_t)z * rows * M + i];  // fixed order
+    y[r * stride_r + m * stride_m] = (TY)v;
+}
+
 }  // namespace itq3
 
 using namespace itq3;
@@ -385,9 +402,20 @@ extern "C" int itq3_rotate_act_f16(const void* x, int x_dtype, int64_t cols, int
     return check_launch("itq3_rotate_act_f16");
 }
 
+static int mmq_splits(int64_t rows, int64_t cols, int64_t m) {
+    // split K only when the output tiles fill less than half of the 148 SMs (one wave), so the
+    // fp32 partial traffic never costs more than the idle SMs it recovers; >= 8 K-chunks per split
+    const int64_t tiles = (int64_t)(mmq_rows_pad(rows) / kMmqBM) * ((m + itq3_mmq_block_n(m) - 1) / itq3_mmq_block_n(m));
+    if (tiles > 74) return 1;
+    const int64_t NC = cols / 64;
+    int64_t ks = 148 / tiles;
+    ks = ks < NC / 8 ? ks : NC / 8;
+    return (int)(ks < 1 ? 1 : ks);
+}
+
 template <int BN, typename TY>
 static int launch_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym, const uint8_t* act, int64_t m, TY* y,
-                      int64_t sr, int64_t sm_, cudaStream_t s) {
+                      int64_t sr, int64_t sm_, float* ws, cudaStream_t s) {
     constexpr int STAGES = BN == 256 ? 3 : 4;
     const int smem = (int)sizeof(MmqSmem<BN, STAGES>) + 1024;
     static bool attr = false;
@@ -402,29 +430,52 @@ static int launch_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym, 
     const uint8_t* codes = mmq;
     const uint16_t* scales = reinterpret_cast<const uint16_t*>(mmq + (int64_t)NC * rp * 16);
     const int8_t* zps = asym ? reinterpret_cast<const int8_t*>(mmq + (int64_t)NC * rp * 16 + (int64_t)NB * rp * 2) : nullptr;
-    const dim3 grid((unsigned)(rp / kMmqBM), (unsigned)((m + BN - 1) / BN));
-    mmq_kernel<BN, STAGES, TY><<<grid, kMmqThreads, smem, s>>>(codes, scales, zps, rp, NC, act, rows, m, y, sr, sm_);
-    return check_launch("itq3_mmq");
+    const int ks = ws ? mmq_splits(rows, cols, m) : 1;
+    const dim3 grid((unsigned)(rp / kMmqBM), (unsigned)((m + BN - 1) / BN), (unsigned)ks);
+    if (ks == 1) {
+        mmq_kernel<BN, STAGES, TY><<<grid, kMmqThreads, smem, s>>>(codes, scales, zps, rp, NC, act, rows, m, y, sr, sm_, 0);
+        return check_launch("itq3_mmq");
+    }
+    static bool attr32 = false;
+    if (!attr32) {
+        if (cudaFuncSetAttribute(mmq_kernel<BN, STAGES, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+            cudaSuccess)
+            return check_launch("itq3_mmq: smem attribute");
+        attr32 = true;
+    }
+    mmq_kernel<BN, STAGES, float><<<grid, kMmqThreads, smem, s>>>(codes, scales, zps, rp, NC, act, rows, m, ws, m, 1,
+                                                                  rows * m);
+    int rc = check_launch("itq3_mmq (split-K)");
+    if (rc) return rc;
+    const int64_t n = rows * m;
+    mmq_splitk_reduce<TY><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ws, ks, rows, m, y, sr, sm_);
+    return check_launch("itq3_mmq (split-K reduce)");
+}
+
+extern "C" int64_t itq3_mmq_ws_nbytes(int64_t rows, int64_t cols, int64_t m) {
+    const int ks = mmq_splits(rows, cols, m);
+    return ks > 1 ? (int64_t)ks * rows * m * (int64_t)sizeof(float) : 0;
 }
 
 extern "C" int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asymmetric, const uint8_t* act, int64_t m,
-                        void* y, int y_dtype, int64_t stride_r, int64_t stride_m, void* stream) {
+                        void* y, int y_dtype, int64_t stride_r, int64_t stride_m, void* workspace, void* stream) {
     if (rows <= 0 || cols <= 0 || cols % 256 || m <= 0) {
         set_error("itq3_mmq: bad shape");
         return ITQ3_E_SHAPE;
     }
     cudaStream_t s = (cudaStream_t)stream;
     const int BN = itq3_mmq_block_n(m);
+    float* ws = (float*)workspace;
     if (y_dtype == ITQ3_F32) {
-        if (BN == 64) return launch_mmq<64>(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, s);
-        if (BN == 128) return launch_mmq<128>(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, s);
-        return launch_mmq<256>(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, s);
+        if (BN == 64) return launch_mmq<64>(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, ws, s);
+        if (BN == 128) return launch_mmq<128>(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, ws, s);
+        return launch_mmq<256>(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, ws, s);
     }
     if (y_dtype == ITQ3_BF16) {
-        if (BN == 64) return launch_mmq<64>(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, s);
+        if (BN == 64) return launch_mmq<64>(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s);
         if (BN == 128)
-            return launch_mmq<128>(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, s);
-        return launch_mmq<256>(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, s);
+            return launch_mmq<128>(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s);
+        return launch_mmq<256>(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s);
     }
     set_error("itq3_mmq: output dtype must be float32 or bfloat16");
     return ITQ3_E_DOMAIN;

@@ -43,13 +43,15 @@ def main():
             X = torch.randn((K, M), generator=g, device=dev)
             act = torch.empty(lib.itq3_mmq_act_nbytes(K, M), dtype=torch.uint8, device=dev)
             Y = torch.empty((rows, M), dtype=torch.float32, device=dev)
+            wsn = lib.itq3_mmq_ws_nbytes(rows, K, M)
+            ws = torch.empty(max(wsn, 1), dtype=torch.uint8, device=dev)
             s = _lib.stream_ptr(dev)
 
             def run(i):
                 _lib.call("itq3_rotate_act_f16", _lib.ptr(X), _lib.F32, K, M, X.stride(0), X.stride(1),
                           _lib.ptr(act), s)
                 _lib.call("itq3_mmq", _lib.ptr(copies[i % len(copies)]), rows, K, 0, _lib.ptr(act), M, _lib.ptr(Y),
-                          _lib.F32, Y.stride(0), Y.stride(1), s)
+                          _lib.F32, Y.stride(0), Y.stride(1), _lib.ptr(ws) if wsn else None, s)
 
             for i in range(3):
                 run(i)
