@@ -31,12 +31,23 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-LAYER_SHAPES = [("qkv", 12288, 4096), ("o", 4096, 4096), ("gate_up", 22016, 4096), ("down", 4096, 11008)]
-N_LAYERS = 32
-WEIGHTS_PER_TOKEN = N_LAYERS * sum(r * c for _, r, c in LAYER_SHAPES)  # 6,476,005,376
-METRIC = "decode tokens/sec (batch-1 fused IFWHT-dequant GEMV chain, Llama-2-7B linear shapes)"
-WORKLOAD = "llama2-7b linear stack decode: 32 layers x (qkv 12288x4096, o 4096x4096, gate_up 22016x4096, " \
-           "down 4096x11008), batch 1"
+# linear shapes (rows x K) per decoder layer; q/k/v and gate/up concatenated as serving engines do
+MODELS = {
+    "llama2-7b": (32, [("qkv", 12288, 4096), ("o", 4096, 4096), ("gate_up", 22016, 4096), ("down", 4096, 11008)]),
+    "llama3-8b": (32, [("qkv", 6144, 4096), ("o", 4096, 4096), ("gate_up", 28672, 4096), ("down", 4096, 14336)]),
+    "llama3-70b": (80, [("qkv", 10240, 8192), ("o", 8192, 8192), ("gate_up", 57344, 8192), ("down", 8192, 28672)]),
+}
+MODEL = os.environ.get("ITQ3_BENCH_MODEL", "llama2-7b")
+for _i, _a in enumerate(sys.argv):  # resolved before argparse so module constants follow --model
+    if _a == "--model" and _i + 1 < len(sys.argv):
+        MODEL = sys.argv[_i + 1]
+    elif _a.startswith("--model="):
+        MODEL = _a.split("=", 1)[1]
+N_LAYERS, LAYER_SHAPES = MODELS[MODEL]
+WEIGHTS_PER_TOKEN = N_LAYERS * sum(r * c for _, r, c in LAYER_SHAPES)  # llama2-7b: 6,476,005,376
+METRIC = "decode tokens/sec (batch-1 fused IFWHT-dequant GEMV chain, %s linear shapes)" % MODEL
+WORKLOAD = "%s linear stack decode: %d layers x (%s), batch 1" % (
+    MODEL, N_LAYERS, ", ".join(f"{n} {r}x{c}" for n, r, c in LAYER_SHAPES))
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -327,7 +338,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8xs8->s32 mma + fp32",
         "data": "synthetic: random-init N(0,1/K) weights quantized to ITQ3_S on the GPU (K1), random fp32 x0",
-        "config": {"workload": WORKLOAD, "model": "llama-2-7b (linear layers)", "global_batch": world,
+        "config": {"workload": WORKLOAD, "model": f"{MODEL} (linear layers)", "global_batch": world,
                    "seq_len": 1, "parallelism": f"replicas{world}" if world > 1 else "single",
                    "stages_per_step": n_st, "activation_limbs": stack.limbs,
                    "l2": f"{tiled_bytes / 1e9:.2f} GB of tiled weights per step > 126 MB L2; no flush needed"},
@@ -358,15 +369,18 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--layers", type=int, default=N_LAYERS)
+    ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--cpu-rows", type=int, default=64)
     ap.add_argument("--cpu-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compare", action="store_true")
     ap.add_argument("--mode", choices=["chain", "kernels"], default="chain")
+    ap.add_argument("--model", choices=sorted(MODELS), default=MODEL)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.layers is None:
+        args.layers = N_LAYERS
     if args.impl == "reference":
         run_reference(args)
     else:
