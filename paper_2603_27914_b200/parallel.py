@@ -92,3 +92,70 @@ class ShardedChain:
         for st in self.stages:
             x = st(x[: st.cols])
         return x
+
+
+class TPStack:
+    """Tensor-parallel decode chain on CUDA: every stage is row-sharded over the process group,
+    computed with the K3 rotate + K4 GEMV kernels on the local rows, and all-gathered with NCCL
+    (all_gather_into_tensor over NVLink) into the replicated input of the next stage.  The whole
+    step -- 2 kernels + 1 collective per stage -- is captured in one CUDA graph.
+
+    `local_qs[i]` is this rank's QuantizedTensor of rows shard_bounds(rows_i, world, rank) of stage i
+    (quantized locally: row shards encode bit-exactly like the full matrix, tests/test_parallel_gloo.py);
+    `rows[i]`/`cols[i]` are the full stage shapes.
+    """
+
+    def __init__(self, local_qs, rows, cols, group=None, limbs: int = 3):
+        from . import _lib
+
+        self._lib = _lib
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.qs, self.rows, self.cols, self.limbs = local_qs, list(rows), list(cols), limbs
+        for i in range(1, len(rows)):
+            if cols[i] > rows[i - 1]:
+                raise ShapeError("TPStack: stage input longer than the previous output")
+        self.dev = _lib.device()
+        lib = _lib.load()
+        self.per = [-(-r // self.world) for r in rows]
+        self.tiled = [q.tiled() for q in local_qs]
+        self.x = torch.zeros(cols[0], dtype=torch.float32, device=self.dev)
+        self.acts = [torch.empty(lib.itq3_act_nbytes(c, 1, limbs), dtype=torch.uint8, device=self.dev) for c in cols]
+        self.ylocal = [torch.zeros(p, dtype=torch.float32, device=self.dev) for p in self.per]
+        self.yfull = [torch.zeros(p * self.world, dtype=torch.float32, device=self.dev) for p in self.per]
+        self.graph = None
+
+    def launch_all(self):
+        lib = self._lib
+        s = lib.stream_ptr(self.dev)
+        for i, q in enumerate(self.qs):
+            xin = self.x if i == 0 else self.yfull[i - 1]
+            lib.call("itq3_rotate_act", lib.ptr(xin), lib.F32, self.cols[i], 1, 1, self.cols[i], self.limbs,
+                     lib.ptr(self.acts[i]), s)
+            if q.rows > 0:
+                lib.call("itq3_gemv", lib.ptr(self.tiled[i]), q.rows, q.cols, int(not q.symmetric), lib.ptr(self.acts[i]),
+                         1, self.limbs, lib.ptr(self.ylocal[i]), lib.F32, 1, 1, s)
+            if self.world > 1:
+                dist.all_gather_into_tensor(self.yfull[i], self.ylocal[i], group=self.group)
+            else:
+                self.yfull[i].copy_(self.ylocal[i])
+
+    def capture(self):
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(side):
+            self.launch_all()
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.launch_all()
+        self.graph = g
+
+    def replay(self):
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+
+    def output(self) -> torch.Tensor:
+        return self.yfull[-1][: self.rows[-1]]
