@@ -153,6 +153,40 @@ int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* tiled, void
 int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch, float* out,
                    int grid, void* d_trace, void* stream);
 
+/* ---- K8 evaluation harness: replaces eval_error / eval_container / rotation_benefit
+ * (compute.py:221-356).  One call quantises (payload == NULL: eval_error with the given
+ * policy) or reads the stored blocks (payload != NULL: eval_container; the payload must
+ * have passed itq3_validate), computes both baselines (unrotated ternary, uniform 3-bit),
+ * and writes the 11 ErrorReport fields as doubles to d_report, in the order
+ * mse, frobenius_rel, linf_in, linf_rot, bound_slack, clamp_fraction, zero_fraction,
+ * mse_uniform3, mse_ternary_noro, n_blocks, unclamped_blocks, plus a 12th word that is 1.0
+ * when a rotated grid value was inf/NaN (binary16 scale overflow: the reference's fwht_inverse
+ * raises DomainError, transform.py:36-42, and so must the caller).  Every field but
+ * frobenius_rel (BLAS ddot order in the reference) is bit-exact.  workspace:
+ * itq3_eval_ws_nbytes(n_blocks, block_n) bytes; its per-block fields stay readable after the
+ * call at itq3_eval_ws_offset(...) (rotation_benefit takes the medians of ERR2/NORO2/UNI2). */
+enum itq3_eval_field {
+    ITQ3_EVAL_E_ROT = 0,   /* [nb*n] f64 squared error, rotated codec       */
+    ITQ3_EVAL_E_NORO = 1,  /* [nb*n] f64 squared error, unrotated ternary   */
+    ITQ3_EVAL_E_UNI = 2,   /* [nb*n] f64 squared error, uniform 3-bit       */
+    ITQ3_EVAL_IN_MAX = 3,  /* [nb] f64 max |w| per block                    */
+    ITQ3_EVAL_ROT_MAX = 4, /* [nb] f64 max |Hw| per block                   */
+    ITQ3_EVAL_A2 = 5,      /* [nb] f64 sum w^2 per block                    */
+    ITQ3_EVAL_ERR2 = 6,    /* [nb] f64 pairwise sum of E_ROT per block      */
+    ITQ3_EVAL_NORO2 = 7,   /* [nb] f64 pairwise sum of E_NORO per block     */
+    ITQ3_EVAL_UNI2 = 8,    /* [nb] f64 pairwise sum of E_UNI per block      */
+    ITQ3_EVAL_SLACK = 9,   /* [nb] f64 budget - err2 (unclamped) or +inf    */
+    ITQ3_EVAL_CLAMP = 10,  /* [nb] i32 clamped codes per block              */
+    ITQ3_EVAL_ZERO = 11,   /* [nb] i32 zero codes per block                 */
+    ITQ3_EVAL_NODES = 12,  /* reduction scratch                             */
+    ITQ3_EVAL_FLAG = 13,   /* i32 non-finite rotated grid value seen        */
+    ITQ3_EVAL_NFIELDS = 14
+};
+size_t itq3_eval_ws_nbytes(int64_t n_blocks, int block_n);
+int64_t itq3_eval_ws_offset(int64_t n_blocks, int block_n, int field);
+int itq3_eval(const void* w, int w_dtype, int64_t numel, int block_n, int sub_scales, int policy, double coeff,
+              int symmetric, const uint8_t* payload, void* workspace, double* d_report, void* stream);
+
 /* ---- scalar binary16 codec (host): encode_f16 / decode_f16 (packing.py:87-109) */
 uint16_t itq3_f16_encode(double x);
 double itq3_f16_decode(uint16_t bits);

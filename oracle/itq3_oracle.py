@@ -322,3 +322,183 @@ def eval_error(w, payload, n, ss):
     wn = float(np.linalg.norm(a))
     return {"mse": float(np.mean(err ** 2)),
             "frobenius_rel": float(np.linalg.norm(err) / wn) if wn > 0 else 0.0}
+
+
+# --- full evaluation harness (compute.py:136-356) -------------------------------------------------
+# The reference's evaluation path is its *vectorised* encoder (compute.py:136-218), which casts
+# scales with astype(float16) (inf on overflow) instead of encode_f16's saturation.
+ERROR_FIELDS = ("mse", "frobenius_rel", "linf_in", "linf_rot", "bound_slack", "clamp_fraction",
+                "zero_fraction", "mse_uniform3", "mse_ternary_noro", "n_blocks", "unclamped_blocks")
+
+
+def f16_round_cast(d):
+    """compute.py:146-147: float64 -> float16 -> float64 (RNE, overflow -> inf)."""
+    with np.errstate(over="ignore"):
+        return np.asarray(d, dtype=np.float64).astype(np.float16).astype(np.float64)
+
+
+def _zero_points_vec(mu, d_eff, symmetric):
+    """compute.py:162-166 (no +0.0 normalisation: the value only enters arithmetic here)."""
+    if symmetric:
+        return np.zeros_like(mu)
+    r = mu / d_eff
+    return np.clip(-np.copysign(np.floor(np.abs(r) + 0.5), r), -1.0, 1.0)
+
+
+def ternary_blocks(y, variant="s", symmetric=True, kind="constant", constant=DEFAULT_SCALE_COEFF):
+    """compute.py:169-201: grid-quantise (nb, n) coefficient rows.
+
+    Returns (recon, codes int8, clamp bool, budget) where budget is the per-block grid bound
+    of compute.py:246-249 (n*d^2/4, or (n/8)*sum(d_m^2)/4 for SS).
+    """
+    nb, n = y.shape
+    mu = np.mean(y, axis=1)
+    if variant == "s":
+        d_raw = policy_scales(y, kind, constant)
+        d16 = f16_round_cast(d_raw)
+        d_eff = np.where(d16 > 0, d16, d_raw)
+        z = _zero_points_vec(mu, d_eff, symmetric)[:, None]
+        pre = round_half_away(y / d_eff[:, None]) + z
+        codes = np.clip(pre, -1.0, 1.0)
+        with np.errstate(invalid="ignore"):
+            recon = d16[:, None] * (codes - z)
+        return recon, codes.astype(np.int8), np.abs(pre) > 1.0, n * d16 ** 2 / 4.0
+    m = n // SUB_BLOCKS
+    subs = y.reshape(nb, SUB_BLOCKS, m)
+    d_raw = policy_scales(subs.reshape(nb * SUB_BLOCKS, m), kind, constant).reshape(nb, SUB_BLOCKS)
+    d16 = f16_round_cast(d_raw)
+    d_eff = np.where(d16 > 0, d16, d_raw)
+    mean_raw = np.mean(d_raw, axis=1)
+    db = f16_round_cast(mean_raw)
+    db = np.where(db > 0, db, mean_raw)
+    z = _zero_points_vec(mu, db, symmetric)[:, None, None]
+    pre = round_half_away(subs / d_eff[:, :, None]) + z
+    codes = np.clip(pre, -1.0, 1.0)
+    with np.errstate(invalid="ignore"):
+        recon = (d16[:, :, None] * (codes - z)).reshape(nb, n)
+    budget = m * np.sum(d16 ** 2, axis=1) / 4.0
+    return recon, codes.reshape(nb, n).astype(np.int8), (np.abs(pre) > 1.0).reshape(nb, n), budget
+
+
+def uniform3_blocks(blocks):
+    """compute.py:204-211: per-block uniform 3-bit (7 steps over [min, max]); constant rows pass."""
+    lo = blocks.min(axis=1, keepdims=True)
+    hi = blocks.max(axis=1, keepdims=True)
+    ok = hi > lo
+    step = np.where(ok, (hi - lo) / 7.0, 1.0)
+    rec = np.clip(step * np.floor(blocks / step + 0.5), lo, hi)
+    return np.where(ok, rec, blocks)
+
+
+class NonFiniteError(ValueError):
+    """fwht_inverse's input check (transform.py:36-42 via _as_block), raised as DomainError there."""
+
+
+def _check_inverse_input(ry):
+    if not np.all(np.isfinite(ry)):
+        raise NonFiniteError("fwht_inverse: input contains non-finite values")
+
+
+def _report(a, blocks, y, recon, codes, clamp, budget, noro, size):
+    """Shared tail of eval_error / eval_container (compute.py:241-269, 310-338)."""
+    diff = recon - blocks
+    err = diff.reshape(-1)[:size]
+    wn = float(np.linalg.norm(a))
+    block_err2 = np.sum(diff ** 2, axis=1)
+    unclamped = ~clamp.any(axis=1)
+    slack = float(np.min(budget[unclamped] - block_err2[unclamped])) if unclamped.any() else 0.0
+    noro_err = (noro - blocks).reshape(-1)[:size]
+    uni_err = (uniform3_blocks(blocks) - blocks).reshape(-1)[:size]
+    return {"mse": float(np.mean(err ** 2)),
+            "frobenius_rel": float(np.linalg.norm(err) / wn) if wn > 0 else 0.0,
+            "linf_in": float(np.mean(np.max(np.abs(blocks), axis=1))),
+            "linf_rot": float(np.mean(np.max(np.abs(y), axis=1))),
+            "bound_slack": slack,
+            "clamp_fraction": float(np.mean(clamp)),
+            "zero_fraction": float(np.mean(codes == 0)),
+            "mse_uniform3": float(np.mean(uni_err ** 2)),
+            "mse_ternary_noro": float(np.mean(noro_err ** 2)),
+            "n_blocks": int(blocks.shape[0]),
+            "unclamped_blocks": int(np.sum(unclamped))}
+
+
+def error_report(w, block_n=256, variant="s", symmetric=True, kind="constant", constant=DEFAULT_SCALE_COEFF):
+    """eval_error (compute.py:221-269) -> dict of the ErrorReport fields."""
+    a = np.asarray(w, dtype=np.float64)
+    blocks, _ = blockify(a, block_n)
+    y = fwht(blocks)
+    ry, codes, clamp, budget = ternary_blocks(y, variant, symmetric, kind, constant)
+    _check_inverse_input(ry)
+    recon = fwht(ry)
+    noro = ternary_blocks(blocks, variant, symmetric, kind, constant)[0]
+    return _report(a, blocks, y, recon, codes, clamp, budget, noro, a.size)
+
+
+def container_report(w, payload, n, variant, symmetric, kind="constant", constant=DEFAULT_SCALE_COEFF):
+    """eval_container (compute.py:272-338): grid values from the payload, clamp re-derived."""
+    a = np.asarray(w, dtype=np.float64)
+    blocks, _ = blockify(a, n)
+    y = fwht(blocks)
+    ss = variant == "ss"
+    quants, sb, zb, sub = split_payload(payload, n, ss)
+    codes, _ = unpack_planes(quants, n)
+    cf = codes.astype(np.float64)
+    z = np.trunc(f16_value(zb))[:, None]
+    if not ss:
+        d16 = f16_value(sb)
+        scales = d16[:, None]
+        budget = n * d16 ** 2 / 4.0
+    else:
+        d16 = f16_value(sub)
+        scales = np.repeat(d16, n // SUB_BLOCKS, axis=1)
+        budget = (n // SUB_BLOCKS) * np.sum(d16 ** 2, axis=1) / 4.0
+    ry = scales * (cf - z)
+    _check_inverse_input(ry)
+    pre = np.where(scales > 0, round_half_away(y / np.where(scales > 0, scales, 1.0)) + z, 2.0 * cf)
+    clamp = np.abs(pre) > 1.0
+    recon = fwht(ry)
+    noro = ternary_blocks(blocks, variant, symmetric, kind, constant)[0]
+    return _report(a, blocks, y, recon, codes, clamp, budget, noro, a.size)
+
+
+def rotation_benefit(w, block_n=256, variant="s", symmetric=True, kind="constant", constant=DEFAULT_SCALE_COEFF):
+    """compute.py:340-356: medians of the per-block MSEs of the three codecs."""
+    a = np.asarray(w, dtype=np.float64)
+    blocks, _ = blockify(a, block_n)
+    ry = ternary_blocks(fwht(blocks), variant, symmetric, kind, constant)[0]
+    _check_inverse_input(ry)
+    rot = fwht(ry)
+    noro = ternary_blocks(blocks, variant, symmetric, kind, constant)[0]
+    uni = uniform3_blocks(blocks)
+    med = lambda r: float(np.median(np.mean((r - blocks) ** 2, axis=1)))  # noqa: E731
+    return {"rotated": med(rot), "unrotated": med(noro), "uniform3": med(uni)}
+
+
+def pairwise_sum(v) -> float:
+    """numpy's add.reduce over a contiguous float64 vector (numpy/_core/src/umath/loops_utils.h.src):
+    n < 8 sequential; n <= 128 eight strided accumulators + tree + tail; else split at
+    (n/2 rounded down to a multiple of 8) and recurse.  The GPU reduction replays this tree."""
+    v = np.asarray(v, dtype=np.float64)
+
+    def rec(lo, n):
+        if n < 8:
+            s = 0.0
+            for i in range(n):
+                s += float(v[lo + i])
+            return s
+        if n <= 128:
+            r = [float(x) for x in v[lo:lo + 8]]
+            i = 8
+            while i < n - (n % 8):
+                for k in range(8):
+                    r[k] += float(v[lo + i + k])
+                i += 8
+            s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+            while i < n:
+                s += float(v[lo + i])
+                i += 1
+            return s
+        n2 = (n // 2) - (n // 2) % 8
+        return rec(lo, n2) + rec(lo + n2, n - n2)
+
+    return 0.0 + rec(0, v.size)

@@ -7,6 +7,8 @@ See DESIGN.md for the path, the boundary and the kernels; INTEGRATION.md for the
 from .codec import (BLOCK_SIZES, HEADER, MAGIC, VERSION, QuantConfig, QuantizedTensor, decode_block,
                     dequantize_tensor, encode_block, quantize_tensor, read_container, write_container)
 from .compute import fused_matmul, fused_matvec
+from .evaluate import (AblationRow, ErrorReport, ablate_block_size, eval_container, eval_error, generate_weights,
+                       report_csv, report_json, rotation_benefit)
 from .errors import (BadMagicError, ContainerError, CorruptionError, DomainError, ItqError, KernelError, LengthError,
                      ShapeError, SizeMismatchError, TruncatedStreamError, UnsupportedVersionError)
 from .packing import (PackedBlock, block_nbytes, decode_f16, deserialize_block, encode_f16, pack_ternary,
@@ -17,6 +19,8 @@ from .transform import fwht_forward, fwht_inverse
 __version__ = "0.1.0"
 
 __all__ = [
+    "AblationRow", "ErrorReport", "ablate_block_size", "eval_container", "eval_error", "generate_weights",
+    "report_csv", "report_json", "rotation_benefit",
     "BLOCK_SIZES", "HEADER", "MAGIC", "VERSION", "DEFAULT_SCALE_COEFF", "EPSILON_D",
     "BadMagicError", "ContainerError", "CorruptionError", "DomainError", "ItqError", "KernelError", "LengthError",
     "PackedBlock", "QuantConfig", "QuantizedTensor", "ScalePolicy", "ShapeError", "SizeMismatchError", "TernaryGrid",

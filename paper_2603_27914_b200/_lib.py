@@ -33,6 +33,9 @@ SIGNATURES = {
     "itq3_validate": (_i32, [_vp, _i64, _i32, _i32, _u32, _vp, _vp]),
     "itq3_dequant": (_i32, [_vp, _i64, _i32, _i32, _i64, _vp, _i32, _vp]),
     "itq3_fwht": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp]),
+    "itq3_eval_ws_nbytes": (ctypes.c_size_t, [_i64, _i32]),
+    "itq3_eval_ws_offset": (_i64, [_i64, _i32, _i32]),
+    "itq3_eval": (_i32, [_vp, _i32, _i64, _i32, _i32, _i32, _dbl, _i32, _vp, _vp, _vp, _vp]),
     "itq3_tiled_nbytes": (_i64, [_i64, _i64, _i32]),
     "itq3_repack_tiled": (_i32, [_vp, _i64, _i64, _i32, _vp, _vp]),
     "itq3_act_nbytes": (_i64, [_i64, _i64, _i32]),

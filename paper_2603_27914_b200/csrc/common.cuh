@@ -139,4 +139,39 @@ __device__ __forceinline__ double round_half_away(double v) {
 
 __device__ __forceinline__ double clip1(double v) { return fmin(fmax(v, -1.0), 1.0); }
 
+// ------------------------------------------------------------------------------------------
+// Butterfly helpers (generic over float / double)
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+
+// Unnormalised butterfly over N = 32*E elements held in stride layout.
+template <int E, typename T>
+__device__ __forceinline__ void warp_butterfly(T (&v)[E], int lane) {
+#pragma unroll
+    for (int h = 1; h < 32 && h < 32 * E; h <<= 1) {
+        const bool high = (lane & h) != 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const T p = __shfl_xor_sync(FULL, v[e], h);
+            v[e] = high ? sub_rn(p, v[e]) : add_rn(v[e], p);  // high lane: lo - hi
+        }
+    }
+#pragma unroll
+    for (int hh = 1; hh < E; hh <<= 1) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if ((e & hh) == 0) {
+                const T lo = v[e], hi = v[e + hh];
+                v[e] = add_rn(lo, hi);
+                v[e + hh] = sub_rn(lo, hi);
+            }
+        }
+    }
+}
+
 }  // namespace itq3

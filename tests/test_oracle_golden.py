@@ -79,3 +79,57 @@ def test_full_c1_digests(golden):
         err = O.eval_error(w, pay, 256, c["variant"] == "ss")
         assert err["mse"] == pytest.approx(c["mse"], rel=1e-12)
         assert err["frobenius_rel"] == pytest.approx(c["frobenius_rel"], rel=1e-12)
+
+
+# --- evaluation harness (compute.py:136-400) pinned to tests/golden/eval_cases.json -------------
+def _eval_golden():
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "eval_cases.json")) as f:
+        return json.load(f)
+
+
+def _eval_inputs(case):
+    dist, rows, cols, seed, scale = case[:5]
+    return O.generate_weights(dist, rows, cols, seed) * scale
+
+
+def _cmp_report(got: dict, want: dict, where: str):
+    """Exact equality for every field; frobenius_rel to rounding (BLAS ddot order)."""
+    for k, v in want.items():
+        ref = float.fromhex(v) if isinstance(v, str) else v
+        if k == "frobenius_rel":
+            assert got[k] == pytest.approx(ref, rel=1e-13, abs=0.0), (where, k)
+        elif isinstance(ref, float) and np.isnan(ref):
+            assert np.isnan(got[k]), (where, k)
+        else:
+            assert got[k] == ref, (where, k, got[k], ref)
+
+
+@pytest.mark.parametrize("i", range(11))
+def test_oracle_eval_reports(i):
+    g = _eval_golden()["cases"][i]
+    case = g["case"]
+    w = _eval_inputs(case)
+    n, variant, sym, kind = case[5:]
+    calls = {"eval_error": lambda: O.error_report(w, n, variant, sym, kind),
+             "eval_container": lambda: O.container_report(w, O.quantize_payload(w, n, variant, sym, kind)[0], n,
+                                                          variant, sym, kind),
+             "rotation_benefit": lambda: O.rotation_benefit(w, n, variant, sym, kind)}
+    for key, fn in calls.items():
+        want = g[key]
+        if "raises" in want:
+            with pytest.raises(O.NonFiniteError, match=want["message"]):
+                with np.errstate(all="ignore"):
+                    fn()
+        else:
+            with np.errstate(all="ignore"):
+                _cmp_report(fn(), want, f"{case}:{key}")
+
+
+def test_oracle_pairwise_sum_matches_numpy():
+    rng = np.random.default_rng(5)
+    for n in (1, 7, 8, 100, 128, 129, 1000, 4099, 65536 + 13):
+        v = rng.standard_normal(n) ** 2
+        assert O.pairwise_sum(v) == np.sum(v), n
