@@ -12,6 +12,8 @@ tiled GEMV layout (``itq3_repack_tiled``).
 
 from __future__ import annotations
 
+import io
+import os
 import struct
 from dataclasses import dataclass, field
 
@@ -335,42 +337,129 @@ def write_container(q: QuantizedTensor, sink) -> int:
     return len(header) + len(body)
 
 
+_STAGE_BYTES = 64 << 20  # pinned staging chunk for container ingest
+
+
+class _Staging:
+    """Two reusable pinned host chunks: chunk i+1 is filled from the file while chunk i's H2D copy runs."""
+
+    def __init__(self):
+        self.bufs = []
+        self.events = []
+
+    def get(self, i: int, dev) -> tuple[torch.Tensor, torch.cuda.Event]:
+        while len(self.bufs) < 2:
+            self.bufs.append(torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True))
+            self.events.append(torch.cuda.Event())
+        ev = self.events[i % 2]
+        ev.synchronize()  # the previous copy out of this chunk has finished
+        return self.bufs[i % 2], ev
+
+
+_staging = _Staging()
+
+
+def _ingest(reader, nbytes: int, dev) -> torch.Tensor:
+    """Stream nbytes from reader(memoryview) -> count into a device tensor through pinned chunks."""
+    out = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    off, i = 0, 0
+    while off < nbytes:
+        buf, ev = _staging.get(i, dev)
+        take = min(buf.numel(), nbytes - off)
+        view = memoryview(buf.numpy())[:take]
+        got = 0
+        while got < take:
+            k = reader(view[got:])
+            if not k:
+                break
+            got += k
+        if got < take:
+            return out[:off + got]  # short read: caller reports truncation
+        out[off:off + take].copy_(buf[:take], non_blocking=True)
+        ev.record(stream)
+        off += take
+        i += 1
+    return out
+
+
 def read_container(source) -> QuantizedTensor:
-    """Parse the header on the host, upload the payload, validate every block with K7."""
+    """Parse the header on the host, stream the payload to the GPU through pinned staging
+    (file reads overlap the H2D copies), and validate every block with one K7 pass."""
+    close = None
+    if hasattr(source, "read") and not (hasattr(source, "seekable") and source.seekable()):
+        source = source.read()  # pipes / unseekable streams: the length is only known at EOF
     if isinstance(source, (bytes, bytearray, memoryview)):
-        data = bytes(source)
-    elif hasattr(source, "read"):
-        data = source.read()
+        mv = memoryview(source).cast("B")
+        pos = [0]
+
+        def reader(dst):
+            k = min(len(dst), len(mv) - pos[0])
+            dst[:k] = mv[pos[0]:pos[0] + k]
+            pos[0] += k
+            return k
+
+        remaining = lambda: len(mv) - pos[0]  # noqa: E731
     else:
-        with open(source, "rb") as f:
-            data = f.read()
-    if len(data) < HEADER.size:
-        raise TruncatedStreamError(f"container header needs {HEADER.size} bytes, got {len(data)}")
-    magic, version, flags, rows, cols, block_n, pad = HEADER.unpack_from(data, 0)
-    if magic != MAGIC:
-        raise BadMagicError(f"bad magic {magic!r}, expected {MAGIC!r}")
-    if version != VERSION:
-        raise UnsupportedVersionError(f"unsupported container version {version}")
-    if flags & ~KNOWN_FLAGS:
-        raise ContainerError(f"unknown flag bits 0x{flags & ~KNOWN_FLAGS:x}")
-    if block_n not in BLOCK_SIZES:
-        raise ContainerError(f"invalid block_n {block_n}")
-    if rows == 0 or cols == 0:
-        raise ContainerError(f"empty tensor dims {rows}x{cols}")
-    n_blocks = -(-rows * cols // block_n)
-    if pad != n_blocks * block_n - rows * cols:
-        raise ContainerError(f"pad {pad} inconsistent with {rows}x{cols} at block_n {block_n}")
-    ss = bool(flags & FLAG_SUB_SCALES)
-    bsize = block_nbytes(block_n, ss)
-    expected = HEADER.size + n_blocks * bsize
-    if len(data) < expected:
-        raise TruncatedStreamError(f"container truncated: expected {expected} bytes, got {len(data)}")
-    if len(data) > expected:
-        raise SizeMismatchError(
-            f"container has {len(data) - expected} trailing bytes (expected {expected}, got {len(data)})")
-    dev = _lib.device()
-    host = np.frombuffer(data, np.uint8, count=n_blocks * bsize, offset=HEADER.size).reshape(n_blocks, bsize)
-    payload = torch.from_numpy(host.copy()).pin_memory().to(dev, non_blocking=True)
+        f = source if hasattr(source, "read") else open(source, "rb")
+        close = None if f is source else f
+        if hasattr(f, "readinto"):
+            reader = f.readinto
+        else:
+            def reader(dst):
+                b = f.read(len(dst))
+                dst[:len(b)] = b
+                return len(b)
+
+        def remaining():
+            try:
+                return os.fstat(f.fileno()).st_size - f.tell()
+            except (AttributeError, OSError, io.UnsupportedOperation):
+                here = f.tell()
+                end = f.seek(0, io.SEEK_END)
+                f.seek(here)
+                return end - here
+    try:
+        head = bytearray(HEADER.size)
+        got = 0
+        while got < HEADER.size:
+            k = reader(memoryview(head)[got:])
+            if not k:
+                break
+            got += k
+        if got < HEADER.size:
+            raise TruncatedStreamError(f"container header needs {HEADER.size} bytes, got {got}")
+        magic, version, flags, rows, cols, block_n, pad = HEADER.unpack_from(head, 0)
+        if magic != MAGIC:
+            raise BadMagicError(f"bad magic {magic!r}, expected {MAGIC!r}")
+        if version != VERSION:
+            raise UnsupportedVersionError(f"unsupported container version {version}")
+        if flags & ~KNOWN_FLAGS:
+            raise ContainerError(f"unknown flag bits 0x{flags & ~KNOWN_FLAGS:x}")
+        if block_n not in BLOCK_SIZES:
+            raise ContainerError(f"invalid block_n {block_n}")
+        if rows == 0 or cols == 0:
+            raise ContainerError(f"empty tensor dims {rows}x{cols}")
+        n_blocks = -(-rows * cols // block_n)
+        if pad != n_blocks * block_n - rows * cols:
+            raise ContainerError(f"pad {pad} inconsistent with {rows}x{cols} at block_n {block_n}")
+        ss = bool(flags & FLAG_SUB_SCALES)
+        bsize = block_nbytes(block_n, ss)
+        expected = HEADER.size + n_blocks * bsize
+        have = HEADER.size + remaining()
+        if have < expected:
+            raise TruncatedStreamError(f"container truncated: expected {expected} bytes, got {have}")
+        if have > expected:
+            raise SizeMismatchError(f"container has {have - expected} trailing bytes (expected {expected}, got {have})")
+        dev = _lib.device()
+        flat = _ingest(reader, n_blocks * bsize, dev)
+        if flat.numel() < n_blocks * bsize:
+            raise TruncatedStreamError(f"container truncated: expected {expected} bytes, "
+                                       f"got {HEADER.size + flat.numel()}")
+    finally:
+        if close is not None:
+            close.close()
+    payload = flat.view(n_blocks, bsize)
     validate_payload(payload, block_n, ss, full=True, prefix=True)
     return QuantizedTensor(rows, cols, block_n, "ss" if ss else "s", not (flags & FLAG_ASYMMETRIC), pad,
                            payload=payload, validated=True)
