@@ -140,8 +140,8 @@ int itq3_unpack_codes(const uint8_t* planes, int64_t n_rows, int n, int8_t* code
  * rows-vectors of 64-bit tagged words ([nch][rows] u64: low = fp32 bits, high = step epoch,
  * zero-initialised once) that the consumer sums in fixed order.  The caller fills a host
  * descriptor array with itq3_chain_write_desc (itq3_chain_desc_nbytes() bytes/stage), copies
- * it to device memory and passes one device u32 epoch word (zero-initialised once; the call
- * increments it on the stream before the launch).  `out` receives the last stage's outputs.
+ * it to device memory and passes two device u32 words (zero-initialised once): the step epoch
+ * and a check-in counter; the kernel advances the epoch itself at the end of each launch.  `out` receives the last stage's outputs.
  * A stage whose descriptor has a non-NULL `xin` reads that fp32 vector instead of the previous
  * stage's output (independent stages: pure weight streaming, used to measure the roofline).  d_trace (optional):
  * n_ctas*n_stages*4 u64 globaltimer stamps for profiling. */

@@ -72,6 +72,7 @@ class QuantizedTensor:
         self._validated = validated  # planes + zero-point checked (decode paths)
         self._tiled = {}
         self._mmq = {}
+        self._chain1 = {}  # device -> one-stage chain context of the k = 1 path (compute.py)
 
     # -- reference-compatible surface ------------------------------------------------------------
     @property

@@ -30,11 +30,55 @@ def perf_limbs(m: int) -> int:
     return 3 if m == 1 else 2
 
 
+class _ChainGemv:
+    """A one-stage decode chain (csrc/chain.cu) bound to one tensor and device: the k = 1 perf path.
+    One cooperative launch streams the weights through the TMA ring while every CTA rotates its own
+    K-chunk of x in registers -- no separate rotation kernel, no host sync.  Calls are ordered by
+    the step epoch on the stream they are issued to, so a tensor's k = 1 products must not run
+    concurrently on two streams (CUDA-graph capture and replay are fine)."""
+
+    def __init__(self, q: QuantizedTensor, dev: torch.device):
+        import ctypes
+
+        lib = _lib.load()
+        host = ctypes.create_string_buffer(lib.itq3_chain_desc_nbytes())
+        self.tiled = q.tiled()
+        nch = -(-q.cols // 4096)
+        self.yparts = torch.zeros((nch, q.rows), dtype=torch.int64, device=dev)  # tagged (value | epoch << 32)
+        _lib.check(lib.itq3_chain_write_desc(host, 0, _lib.ptr(self.tiled), _lib.ptr(self.yparts), None, q.rows,
+                                             q.cols, int(not q.symmetric), 0))
+        self.desc = torch.frombuffer(bytearray(host.raw), dtype=torch.uint8).to(dev)
+        self.epoch = torch.zeros(2, dtype=torch.int32, device=dev)  # (step epoch, check-in count)
+
+    def __call__(self, x: torch.Tensor, out: torch.Tensor, stream: int) -> None:
+        _lib.call("itq3_chain_run", _lib.ptr(self.desc), 1, _lib.ptr(x), CHAIN_LIMBS, _lib.ptr(self.epoch),
+                  _lib.ptr(out), 0, None, stream)
+
+
+CHAIN_LIMBS = 3
+
+
+def _matvec_chain(q: QuantizedTensor, x: torch.Tensor) -> torch.Tensor:
+    dev = x.device
+    stream = _lib.stream_ptr(dev)
+    ctx = q._chain1.get(dev)
+    if ctx is None:
+        ctx = q._chain1[dev] = _ChainGemv(q, dev)
+    xf = x.reshape(-1)
+    if xf.dtype != torch.float32 or not xf.is_contiguous():
+        xf = xf.to(torch.float32).contiguous()
+    out = torch.empty((q.rows, 1), dtype=torch.float32, device=dev)
+    ctx(xf, out, stream)
+    return out
+
+
 def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, limbs: int) -> torch.Tensor:
     """Y (rows x k) = w_hat @ X for a CUDA X (cols x k, any strides)."""
     dev = X.device
     rows, cols = q.rows, q.cols
     k = X.shape[1]
+    if q.fast_layout() and out_dtype == torch.float32 and k == 1 and limbs == CHAIN_LIMBS:
+        return _matvec_chain(q, X)
     if q.fast_layout() and out_dtype != torch.float64 and k >= MMQ_MIN_TOKENS:
         mmq = q.mmq_layout()
         s = _lib.stream_ptr(dev)

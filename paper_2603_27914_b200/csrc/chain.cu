@@ -270,17 +270,20 @@ __device__ __forceinline__ bool stage_split(const ChainStage& st, int cta, int G
 // trace (optional): per (cta, stage) globaltimer stamps
 //   0 stage entered, 1 input observed ready, 2 input rotated, 3 own units done
 // 18 warps: the per-SMSP register file (16K) caps a 5-warp SMSP at 96 registers/thread
-__global__ void chain_epoch_kernel(unsigned* epoch) { *epoch += 1; }
 
 __global__ void __launch_bounds__(kChainThreads, 1)
     chain_kernel(const ChainStage* __restrict__ stages, int S, const float* __restrict__ x0, int L,
-                 const unsigned* __restrict__ epoch_ptr, float* __restrict__ out,
+                 unsigned* __restrict__ epoch_ptr, float* __restrict__ out,
                  unsigned long long* __restrict__ trace) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     ChainSmem& sm = *reinterpret_cast<ChainSmem*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int cta = blockIdx.x, G = gridDim.x;
-    const unsigned epoch = *epoch_ptr;
+    // Step epoch: tags of this launch = stored epoch + 1; every CTA checks in on epoch_ptr[1] after
+    // reading it, and CTA 0 publishes the new epoch at the very end, once all CTAs have read the
+    // old one (no separate bump kernel on the stream).
+    const unsigned epoch = *reinterpret_cast<volatile unsigned*>(epoch_ptr) + 1u;
+    if (threadIdx.x == 0) atomicAdd(epoch_ptr + 1, 1u);
 
     if (tid == 0) {
         for (int i = 0; i < kNumSlots; ++i) {
@@ -489,6 +492,11 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         }
         out[r] = v;
     }
+    if (cta == 0 && tid == 0) {
+        while (atomicAdd(epoch_ptr + 1, 0u) < (unsigned)G) __nanosleep(32);
+        epoch_ptr[1] = 0u;
+        *reinterpret_cast<volatile unsigned*>(epoch_ptr) = epoch;
+    }
 }
 
 }  // namespace itq3
@@ -538,7 +546,6 @@ extern "C" int itq3_chain_run(const void* d_desc, int n_stages, const float* x0,
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         grid = sms;
     }
-    chain_epoch_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(d_epoch);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kChainThreads);
@@ -550,7 +557,7 @@ extern "C" int itq3_chain_run(const void* d_desc, int n_stages, const float* x0,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, chain_kernel, (const ChainStage*)d_desc, n_stages, x0, limbs,
-                                             (const unsigned*)d_epoch, out, (unsigned long long*)d_trace);
+                                             d_epoch, out, (unsigned long long*)d_trace);
     if (e != cudaSuccess) {
         set_error("chain: launch failed: %s", cudaGetErrorString(e));
         return ITQ3_E_CUDA;

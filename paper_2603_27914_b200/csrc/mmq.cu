@@ -5,12 +5,14 @@
 // the whole K reduction stays in one fp32 TMEM accumulator with no per-block promotion; the
 // only approximation is B = f16(H x / 16).
 //
-// Per CTA: 128 weight rows x BN tokens.  Warp roles (6 warps):
+// Per CTA: 128 weight rows x BN tokens.  Warp roles (10 warps):
 //   warp 0    producer: cp.async.bulk of the 2-bit code slab (128 rows x 64 k = 2 KB) and of the
-//             pre-swizzled activation tile (BN x 64 k f16) per K-chunk into a STAGES-deep ring;
+//             pre-swizzled activation tile (BN x 64 k f16) per K-chunk into an NL-deep LOAD ring
+//             (12 slots at BN = 64: enough bytes in flight to hide HBM latency at small M);
 //   warp 1    MMA issuer (one thread): 4 x tcgen05.mma (K = 16) per chunk, tcgen05.commit frees
-//             the slot; the final commit signals the epilogue;
-//   warps 2-5 expanders, one weight row per thread: 2-bit codes -> f16 d*t written in the
+//             the A slot and the load slot; the final commit signals the epilogue;
+//   warps 2-9 expanders, two threads per weight row: 2-bit codes -> f16 d*t written into an
+//             NA-deep ring of A tiles in the
 //             SWIZZLE_128B K-major canonical layout (magic-number decode: 4 ops per f16x2; exact
 //             while 2|d| < 65504),
 //             then the epilogue (tcgen05.ld 32x32b -> fp32/bf16 stores).
@@ -64,17 +66,21 @@ __device__ __forceinline__ uint32_t umma_idesc_f16() {
     return (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kMmqBM >> 4) << 24);
 }
 
-template <int BN, int STAGES>
+// Two rings: LOAD slots (codes + scales + zero-points + the B tile of one 64-k chunk, filled by TMA,
+// freed by the MMA commit) are many and small, so enough bulk copies are in flight to cover the
+// HBM latency even when the chunk's compute is short (small M); A slots (expanded f16 tiles) are few.
+template <int BN, int NL, int NA>
 struct MmqSmem {
-    uint8_t a[STAGES][kMmqBM * 128];   // expanded f16 A tiles (1024-aligned)
-    uint8_t b[STAGES][BN * 128];       // activation tiles (pre-swizzled in global)
-    uint8_t codes[STAGES][kMmqCodeChunk];
-    uint16_t scl[STAGES][kMmqBM];  // f16 scales of the chunk's 256-block (bulk-copied with the codes)
-    int8_t zp[STAGES][kMmqBM];
-    uint64_t full[STAGES];   // codes + scales + B landed (TMA)
-    uint64_t aready[STAGES]; // A expanded (all expander threads)
-    uint64_t empty[STAGES];  // MMA consumed the slot (tcgen05.commit)
-    uint64_t accum;          // all MMAs done
+    uint8_t a[NA][kMmqBM * 128];   // expanded f16 A tiles (1024-aligned)
+    uint8_t b[NL][BN * 128];       // activation tiles (pre-swizzled in global)
+    uint8_t codes[NL][kMmqCodeChunk];
+    uint16_t scl[NL][kMmqBM];  // f16 scales of the chunk's 256-block (bulk-copied with the codes)
+    int8_t zp[NL][kMmqBM];
+    uint64_t full[NL];    // codes + scales + B landed (TMA)
+    uint64_t lempty[NL];  // MMA consumed the load slot (tcgen05.commit)
+    uint64_t aready[NA];  // A expanded (all expander threads)
+    uint64_t aempty[NA];  // MMA consumed the A slot (tcgen05.commit)
+    uint64_t accum;       // all MMAs done
     uint32_t tmem_base;
 };
 
@@ -83,7 +89,7 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int j) {
     return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((j ^ (r & 7)) << 4));
 }
 
-template <int BN, int STAGES, typename TY>
+template <int BN, int NL, int NA, typename TY>
 __global__ void __launch_bounds__(kMmqThreads, 1)
     mmq_kernel(const uint8_t* __restrict__ codes, const uint16_t* __restrict__ scales, const int8_t* __restrict__ zps,
                int rows_pad, int NC, const uint8_t* __restrict__ act, int64_t rows, int64_t M, TY* __restrict__ y,
@@ -91,7 +97,7 @@ __global__ void __launch_bounds__(kMmqThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for the swizzled tiles
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    MmqSmem<BN, STAGES>& sm = *reinterpret_cast<MmqSmem<BN, STAGES>*>(base);
+    MmqSmem<BN, NL, NA>& sm = *reinterpret_cast<MmqSmem<BN, NL, NA>*>(base);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rt = blockIdx.x, nt = blockIdx.y;
     // split-K: this CTA reduces K-chunks [kc0, kc1); partial outputs go to slab blockIdx.z
@@ -99,10 +105,13 @@ __global__ void __launch_bounds__(kMmqThreads, 1)
     y += (int64_t)blockIdx.z * slab;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < NL; ++s) {
             mbar_init_(&sm.full[s], 1);
+            mbar_init_(&sm.lempty[s], 1);
+        }
+        for (int s = 0; s < NA; ++s) {
             mbar_init_(&sm.aready[s], 32 * kMmqExpWarps);
-            mbar_init_(&sm.empty[s], 1);
+            mbar_init_(&sm.aempty[s], 1);
         }
         mbar_init_(&sm.accum, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -122,9 +131,9 @@ __global__ void __launch_bounds__(kMmqThreads, 1)
             const uint8_t* cbase = codes + (int64_t)rt * kMmqCodeChunk;
             const uint8_t* bbase = act + (int64_t)nt * NC * BN * 128;
             for (int kc = kc0; kc < kc1; ++kc) {
-                const int s = (kc - kc0) % STAGES;
-                const unsigned ph = (unsigned)((kc - kc0) / STAGES) & 1u;
-                mbar_wait_(&sm.empty[s], ph ^ 1u);
+                const int s = (kc - kc0) % NL;
+                const unsigned ph = (unsigned)((kc - kc0) / NL) & 1u;
+                mbar_wait_(&sm.lempty[s], ph ^ 1u);
                 const int64_t soff = (int64_t)(kc >> 2) * rows_pad + (int64_t)rt * kMmqBM;
                 mbar_expect_tx_(&sm.full[s], kMmqCodeChunk + BN * 128 + kMmqBM * 2 + (zps ? kMmqBM : 0));
                 bulk_g2s_(sm.codes[s], cbase + (int64_t)kc * rows_pad * 16, kMmqCodeChunk, &sm.full[s]);
@@ -137,12 +146,11 @@ __global__ void __launch_bounds__(kMmqThreads, 1)
         if (lane == 0) {
             const uint32_t idesc = umma_idesc_f16<BN>();
             for (int kc = kc0; kc < kc1; ++kc) {
-                const int s = (kc - kc0) % STAGES;
-                const unsigned ph = (unsigned)((kc - kc0) / STAGES) & 1u;
-                mbar_wait_(&sm.aready[s], ph);
-                mbar_wait_(&sm.full[s], ph);
+                const int s = (kc - kc0) % NL, sa = (kc - kc0) % NA;
+                mbar_wait_(&sm.aready[sa], (unsigned)((kc - kc0) / NA) & 1u);
+                mbar_wait_(&sm.full[s], (unsigned)((kc - kc0) / NL) & 1u);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t a0 = smem_addr(sm.a[s]), b0 = smem_addr(sm.b[s]);
+                const uint32_t a0 = smem_addr(sm.a[sa]), b0 = smem_addr(sm.b[s]);
 #pragma unroll
                 for (int k = 0; k < kMmqBK / 16; ++k) {
                     const uint64_t ad = umma_desc_sw128(a0 + 32 * k), bd = umma_desc_sw128(b0 + 32 * k);
@@ -153,7 +161,10 @@ __global__ void __launch_bounds__(kMmqThreads, 1)
                         "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                 smem_addr(&sm.empty[s]))
+                                 smem_addr(&sm.aempty[sa]))
+                             : "memory");
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_addr(&sm.lempty[s]))
                              : "memory");
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -167,11 +178,10 @@ __global__ void __launch_bounds__(kMmqThreads, 1)
         const int r = quarter * 32 + lane;
         const int64_t grow = (int64_t)rt * kMmqBM + r;
         for (int kc = kc0; kc < kc1; ++kc) {
-            const int s = (kc - kc0) % STAGES;
-            const unsigned ph = (unsigned)((kc - kc0) / STAGES) & 1u;
+            const int s = (kc - kc0) % NL, sa = (kc - kc0) % NA;
             // the A slot is free once the MMA that read it committed; codes/scales landed
-            mbar_wait_(&sm.empty[s], ph ^ 1u);
-            mbar_wait_(&sm.full[s], ph);
+            mbar_wait_(&sm.aempty[sa], ((unsigned)((kc - kc0) / NA) & 1u) ^ 1u);
+            mbar_wait_(&sm.full[s], (unsigned)((kc - kc0) / NL) & 1u);
             const uint16_t dh = sm.scl[s][r];
             const int z = zps ? (int)sm.zp[s][r] : 0;
             const __half d = __ushort_as_half(dh);
@@ -180,7 +190,7 @@ __global__ void __launch_bounds__(kMmqThreads, 1)
             const uint32_t ndz2 = (uint32_t)__half_as_ushort(ndz) * 0x10001u;
             const uint2 w2 = reinterpret_cast<const uint2*>(sm.codes[s])[r * 2 + h];
             const uint32_t wv[2] = {w2.x, w2.y};
-            uint8_t* atile = sm.a[s];
+            uint8_t* atile = sm.a[sa];
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {  // 16-byte chunk j = 4h + jj: k in [8j, 8j+8)
                 const int j = 4 * h + jj;
@@ -198,7 +208,7 @@ __global__ void __launch_bounds__(kMmqThreads, 1)
                 *reinterpret_cast<uint4*>(atile + sw128_off(r, j)) = make_uint4(out[0], out[1], out[2], out[3]);
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
-            mbar_arrive_(&sm.aready[s]);
+            mbar_arrive_(&sm.aready[sa]);
         }
         // ---- epilogue: TMEM lane r, this warp's half of the token columns ----
         mbar_wait_(&sm.accum, 0);
@@ -416,11 +426,12 @@ static int mmq_splits(int64_t rows, int64_t cols, int64_t m) {
 template <int BN, typename TY>
 static int launch_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym, const uint8_t* act, int64_t m, TY* y,
                       int64_t sr, int64_t sm_, float* ws, cudaStream_t s) {
-    constexpr int STAGES = BN == 256 ? 3 : 4;
-    const int smem = (int)sizeof(MmqSmem<BN, STAGES>) + 1024;
+    constexpr int NL = BN == 256 ? 4 : (BN == 128 ? 8 : 12);  // load slots: ~150 KB of bulk copies in flight
+    constexpr int NA = BN == 256 ? 2 : 3;
+    const int smem = (int)sizeof(MmqSmem<BN, NL, NA>) + 1024;
     static bool attr = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(mmq_kernel<BN, STAGES, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        if (cudaFuncSetAttribute(mmq_kernel<BN, NL, NA, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
             cudaSuccess)
             return check_launch("itq3_mmq: smem attribute");
         attr = true;
@@ -433,17 +444,17 @@ static int launch_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym, 
     const int ks = ws ? mmq_splits(rows, cols, m) : 1;
     const dim3 grid((unsigned)(rp / kMmqBM), (unsigned)((m + BN - 1) / BN), (unsigned)ks);
     if (ks == 1) {
-        mmq_kernel<BN, STAGES, TY><<<grid, kMmqThreads, smem, s>>>(codes, scales, zps, rp, NC, act, rows, m, y, sr, sm_, 0);
+        mmq_kernel<BN, NL, NA, TY><<<grid, kMmqThreads, smem, s>>>(codes, scales, zps, rp, NC, act, rows, m, y, sr, sm_, 0);
         return check_launch("itq3_mmq");
     }
     static bool attr32 = false;
     if (!attr32) {
-        if (cudaFuncSetAttribute(mmq_kernel<BN, STAGES, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        if (cudaFuncSetAttribute(mmq_kernel<BN, NL, NA, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
             cudaSuccess)
             return check_launch("itq3_mmq: smem attribute");
         attr32 = true;
     }
-    mmq_kernel<BN, STAGES, float><<<grid, kMmqThreads, smem, s>>>(codes, scales, zps, rp, NC, act, rows, m, ws, m, 1,
+    mmq_kernel<BN, NL, NA, float><<<grid, kMmqThreads, smem, s>>>(codes, scales, zps, rp, NC, act, rows, m, ws, m, 1,
                                                                   rows * m);
     int rc = check_launch("itq3_mmq (split-K)");
     if (rc) return rc;

@@ -67,7 +67,7 @@ class LinearStack:
                 xin = _lib.ptr(self._xin)
             _lib.check(lib.itq3_chain_write_desc(host, i, _lib.ptr(self.tiled[i]), _lib.ptr(self.yparts[i]), xin,
                                                  q.rows, q.cols, int(not q.symmetric), 0))
-        self.epoch = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.epoch = torch.zeros(2, dtype=torch.int32, device=self.dev)  # (step epoch, check-in count)
         self.trace = None
         self.desc = torch.frombuffer(bytearray(host.raw), dtype=torch.uint8).to(self.dev)
 
@@ -81,7 +81,7 @@ class LinearStack:
 
     @property
     def launches_per_step(self) -> int:
-        return 2 if self.mode == "chain" else 2 * len(self.qs)  # chain: epoch bump + chain kernel
+        return 1 if self.mode == "chain" else 2 * len(self.qs)  # chain: one cooperative kernel
 
     def step_bytes(self) -> int:
         """Algorithmic bytes of one step: all tiled weights + rotated activations + outputs."""

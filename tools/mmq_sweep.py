@@ -1,7 +1,8 @@
 """C3 sweep: batched MMQ (tcgen05, csrc/mmq.cu) at Llama-3-8B shapes x M = 16..2048.
 
     python tools/mmq_sweep.py [--out profiles/r01/mmq_sweep.json]
-Times itq3_rotate_act_f16 + itq3_mmq with CUDA events (20 reps after 3 warm-ups, weights of
+Times itq3_rotate_act_f16 + itq3_mmq with CUDA events over a CUDA graph of 20 calls (host launch
+overhead excluded; weights of
 >= 2 distinct copies rotated to defeat L2 at small M), reports TFLOPS = 2*rows*K*M / t and the
 fraction of the measured dense bf16/f16 peak (MEASURED_PEAKS.json).
 """
@@ -11,6 +12,29 @@ import os
 import sys
 
 import torch
+
+
+def graph_time(fn, reps):
+    """GPU time per call of fn(i): the reps calls are captured in one CUDA graph and replayed, so host
+    launch overhead (ctypes + driver, ~5-7 us per launch) is off the measured path."""
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for i in range(3):
+            fn(i)
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(reps):
+            fn(i)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -45,24 +69,15 @@ def main():
             Y = torch.empty((rows, M), dtype=torch.float32, device=dev)
             wsn = lib.itq3_mmq_ws_nbytes(rows, K, M)
             ws = torch.empty(max(wsn, 1), dtype=torch.uint8, device=dev)
-            s = _lib.stream_ptr(dev)
 
             def run(i):
+                s = _lib.stream_ptr(dev)
                 _lib.call("itq3_rotate_act_f16", _lib.ptr(X), _lib.F32, K, M, X.stride(0), X.stride(1),
                           _lib.ptr(act), s)
                 _lib.call("itq3_mmq", _lib.ptr(copies[i % len(copies)]), rows, K, 0, _lib.ptr(act), M, _lib.ptr(Y),
                           _lib.F32, Y.stride(0), Y.stride(1), _lib.ptr(ws) if wsn else None, s)
 
-            for i in range(3):
-                run(i)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            e0.record()
-            for i in range(args.reps):
-                run(i)
-            e1.record()
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / args.reps
+            ms = graph_time(run, args.reps)
             tf = 2.0 * rows * K * M / (ms * 1e-3) / 1e12
             wbytes = rows * K * 66 / 256
             r = {"rows": rows, "K": K, "M": M, "us": ms * 1e3, "tflops": tf, "frac_of_bf16_peak": tf / peak,
