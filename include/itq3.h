@@ -133,6 +133,20 @@ int itq3_pack_codes(const int8_t* codes, int64_t n_rows, int n, uint8_t* planes,
 int itq3_unpack_codes(const uint8_t* planes, int64_t n_rows, int n, int8_t* codes, unsigned long long* d_bad,
                       void* stream);
 
+/* ---- K5b small-batch MMQ on tcgen05.mma kind::i8 (0 < m <= 64 tokens): raw 2-bit codes as the
+ * TMEM A operand, activations as two s8 limbs of a 16-bit fixed point per (token, block)
+ * (itq3_rotate_act_i8), one s32 accumulator per block folded with the f16 scale in the epilogue.
+ * Weights: itq3_repack_mmq8 (itq3_mmq8_nbytes bytes).  Workspace: itq3_mmq8_ws_nbytes (split-K). */
+int itq3_mmq8_block_n(int64_t m);
+int64_t itq3_mmq8_nbytes(int64_t rows, int64_t cols);
+int itq3_repack_mmq8(const uint8_t* payload, int64_t rows, int64_t cols, int asymmetric, uint8_t* out, void* stream);
+int64_t itq3_mmq8_act_nbytes(int64_t cols, int64_t m);
+int itq3_rotate_act_i8(const void* x, int x_dtype, int64_t cols, int64_t m, int64_t stride_k, int64_t stride_m,
+                       uint8_t* out, void* stream);
+int64_t itq3_mmq8_ws_nbytes(int64_t rows, int64_t cols, int64_t m);
+int itq3_mmq8(const uint8_t* w, int64_t rows, int64_t cols, const uint8_t* act, int64_t m, void* y, int y_dtype,
+              int64_t stride_r, int64_t stride_m, void* workspace, void* stream);
+
 /* ---- persistent chain kernel: a dependent chain of fused GEMVs (decode step) in ONE
  * cooperative launch (csrc/chain.cu).  Stage i multiplies its tiled weights by the first
  * cols_i entries of stage i-1's output (stage 0: x0).  A stage with K > 16 blocks is split in

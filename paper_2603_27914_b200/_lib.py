@@ -52,6 +52,13 @@ SIGNATURES = {
     "itq3_mmq": (_i32, [_vp, _i64, _i64, _i32, _vp, _i64, _vp, _i32, _i64, _i64, _vp, _vp]),
     "itq3_pack_codes": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp]),
     "itq3_unpack_codes": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp]),
+    "itq3_mmq8_block_n": (_i32, [_i64]),
+    "itq3_mmq8_nbytes": (_i64, [_i64, _i64]),
+    "itq3_repack_mmq8": (_i32, [_vp, _i64, _i64, _i32, _vp, _vp]),
+    "itq3_mmq8_act_nbytes": (_i64, [_i64, _i64]),
+    "itq3_rotate_act_i8": (_i32, [_vp, _i32, _i64, _i64, _i64, _i64, _vp, _vp]),
+    "itq3_mmq8_ws_nbytes": (_i64, [_i64, _i64, _i64]),
+    "itq3_mmq8": (_i32, [_vp, _i64, _i64, _vp, _i64, _vp, _i32, _i64, _i64, _vp, _vp]),
     "itq3_chain_desc_nbytes": (_i64, []),
     "itq3_chain_act_block_bytes": (_i32, [_i32]),
     "itq3_chain_smem_bytes": (_i32, []),

@@ -72,6 +72,7 @@ class QuantizedTensor:
         self._validated = validated  # planes + zero-point checked (decode paths)
         self._tiled = {}
         self._mmq = {}
+        self._mmq8 = {}
         self._chain1 = {}  # device -> one-stage chain context of the k = 1 path (compute.py)
 
     # -- reference-compatible surface ------------------------------------------------------------
@@ -157,6 +158,17 @@ class QuantizedTensor:
                       _lib.stream_ptr(p.device))
             self._tiled[key] = t
         return self._tiled[key]
+
+    def mmq8_layout(self) -> torch.Tensor:
+        """Small-batch tcgen05 i8 MMQ layout (csrc/mmq.cu K5b: 128-row x 256-k records)."""
+        p = self.ensure_decodable()
+        if p.device not in self._mmq8:
+            asym = 0 if self.symmetric else 1
+            t = torch.empty(_lib.load().itq3_mmq8_nbytes(self.rows, self.cols), dtype=torch.uint8, device=p.device)
+            _lib.call("itq3_repack_mmq8", _lib.ptr(p), self.rows, self.cols, asym, _lib.ptr(t),
+                      _lib.stream_ptr(p.device))
+            self._mmq8[p.device] = t
+        return self._mmq8[p.device]
 
     def mmq_layout(self) -> torch.Tensor:
         """tcgen05 MMQ layout (csrc/mmq.cu: 2-bit codes in 64-k slabs, rows padded to 128)."""

@@ -23,7 +23,8 @@ from .codec import QuantizedTensor
 from .errors import DomainError, ShapeError
 
 PARITY_LIMBS = 6
-MMQ_MIN_TOKENS = 16  # perf mode: k >= 16 columns go to the tcgen05 MMQ kernel (csrc/mmq.cu)
+MMQ_MIN_TOKENS = 16  # perf mode: k >= 16 columns go to the tcgen05 MMQ kernels (csrc/mmq.cu)
+MMQ8_MAX_TOKENS = 64  # ... 16 <= k <= 64 to the kind::i8 one (K5b), larger k to the kind::f16 one (K5)
 
 
 def perf_limbs(m: int) -> int:
@@ -79,6 +80,20 @@ def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, 
     k = X.shape[1]
     if q.fast_layout() and out_dtype == torch.float32 and k == 1 and limbs == CHAIN_LIMBS:
         return _matvec_chain(q, X)
+    if q.fast_layout() and out_dtype != torch.float64 and MMQ_MIN_TOKENS <= k <= MMQ8_MAX_TOKENS \
+            and X.dtype != torch.float64:
+        lib = _lib.load()
+        s = _lib.stream_ptr(dev)
+        act = torch.empty(lib.itq3_mmq8_act_nbytes(cols, k), dtype=torch.uint8, device=dev)
+        _lib.call("itq3_rotate_act_i8", _lib.ptr(X), _lib.TORCH_DTYPE_CODE[X.dtype], cols, k, X.stride(0),
+                  X.stride(1), _lib.ptr(act), s)
+        Y = torch.empty((rows, k), dtype=out_dtype, device=dev)
+        wsn = lib.itq3_mmq8_ws_nbytes(rows, cols, k)
+        ws = torch.empty(wsn, dtype=torch.uint8, device=dev) if wsn else None
+        _lib.call("itq3_mmq8", _lib.ptr(q.mmq8_layout()), rows, cols, _lib.ptr(act), k, _lib.ptr(Y),
+                  _lib.TORCH_DTYPE_CODE[out_dtype], Y.stride(0), Y.stride(1), _lib.ptr(ws) if ws is not None else None,
+                  s)
+        return Y
     if q.fast_layout() and out_dtype != torch.float64 and k >= MMQ_MIN_TOKENS:
         mmq = q.mmq_layout()
         s = _lib.stream_ptr(dev)

@@ -491,3 +491,460 @@ extern "C" int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym
     set_error("itq3_mmq: output dtype must be float32 or bfloat16");
     return ITQ3_E_DOMAIN;
 }
+
+// ==========================================================================================
+// K5b: small-batch MMQ on tcgen05.mma kind::i8 (M <= 64 tokens).
+//
+// The f16 path above spends ~3 thread instructions per weight expanding codes into d*t tiles,
+// which caps it far below HBM speed at small M.  Here the weight operand is the raw code
+// c = q + 1 in {0, 1, 2} (u8), one SHF + LOP per 4 weights, written to TMEM with one
+// tcgen05.st per row and block; the activations are 16-bit fixed point per (token, block)
+// (the K3/chain rotation: exact int32 butterfly, |q| <= 2^14) split into two s8 limbs that form
+// the N = 2 BN columns of the MMA (B, shared memory, SWIZZLE_128B).  Because scales differ per
+// (row, block), every block gets its own s32 accumulator in TMEM and the epilogue folds it:
+//     y[r, m] += d_rb * ( 2^(ex_bm - 4) * (D0 + 256 D1) - (1 + z_rb) * Q_bm 2^(ex_bm - 4) ).
+// Per CTA: 128 rows x BN tokens x a K-range of blocks.  Warps: 0 producer (one bulk copy of the
+// weight record and one of the activation record per block), 1 MMA issuer + TMEM allocator,
+// 2-5 expanders (one row per thread), 6-13 epilogue (lane quarter x token half).
+// ==========================================================================================
+namespace itq3 {
+
+constexpr int kQ8Rec = 8192 + 256 + 128;  // codes [c][row][16 B] | f16 scales [row] | int8 zps [row]
+constexpr int kQ8Threads = 32 * 14;
+constexpr int kQ8NA = 2, kQ8ND = 2;
+
+__host__ __device__ constexpr int q8_act_bytes(int BN) { return 512 * BN + 8 * BN; }  // B tile + (f, corr)/token
+__host__ __device__ constexpr int q8_slot_bytes(int BN) { return (q8_act_bytes(BN) + kQ8Rec + 1023) / 1024 * 1024; }
+template <int BN>
+__host__ __device__ constexpr int q8_slots() { return BN >= 64 ? 4 : (BN == 32 ? 6 : 8); }
+
+template <int BN>
+struct Q8Smem {
+    uint8_t slot[q8_slots<BN>()][q8_slot_bytes(BN)];  // [B tile (1024-aligned) | meta | weight record]
+    uint64_t full[q8_slots<BN>()];
+    uint64_t empty[q8_slots<BN>()];
+    uint64_t aready[kQ8NA], aempty[kQ8NA];
+    uint64_t dfull[kQ8ND], dempty[kQ8ND];
+    uint32_t tmem_base;
+};
+
+template <int BN, typename TY>
+__global__ void __launch_bounds__(kQ8Threads, 1)
+    mmq8_kernel(const uint8_t* __restrict__ wrec, int NB, const uint8_t* __restrict__ act, int64_t rows, int64_t M,
+                TY* __restrict__ y, int64_t stride_r, int64_t stride_m, int64_t slab) {
+    constexpr int NS = q8_slots<BN>();
+    constexpr int N = 2 * BN;
+    constexpr uint32_t kCols = 2 * 64 + 2 * N <= 256 ? 256 : 512;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    Q8Smem<BN>& sm = *reinterpret_cast<Q8Smem<BN>*>(base);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rt = blockIdx.x, tt = blockIdx.y;
+    const int b0 = (int)((int64_t)blockIdx.z * NB / gridDim.z), b1 = (int)((int64_t)(blockIdx.z + 1) * NB / gridDim.z);
+    y += (int64_t)blockIdx.z * slab;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init_(&sm.full[s], 1);
+            mbar_init_(&sm.empty[s], 8);  // epilogue warps (the last readers of a slot)
+        }
+        for (int s = 0; s < kQ8NA; ++s) {
+            mbar_init_(&sm.aready[s], 4);
+            mbar_init_(&sm.aempty[s], 1);
+        }
+        for (int s = 0; s < kQ8ND; ++s) {
+            mbar_init_(&sm.dfull[s], 1);
+            mbar_init_(&sm.dempty[s], 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&sm.tmem_base)),
+                     "r"(kCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = sm.tmem_base;
+    const int nblk = b1 - b0;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int i = 0; i < nblk; ++i) {
+                const int s = i % NS;
+                mbar_wait_(&sm.empty[s], ((unsigned)(i / NS) & 1u) ^ 1u);
+                mbar_expect_tx_(&sm.full[s], q8_act_bytes(BN) + kQ8Rec);
+                const int b = b0 + i;
+                bulk_g2s_(sm.slot[s], act + ((int64_t)tt * NB + b) * q8_act_bytes(BN), q8_act_bytes(BN), &sm.full[s]);
+                bulk_g2s_(sm.slot[s] + q8_act_bytes(BN), wrec + ((int64_t)rt * NB + b) * kQ8Rec, kQ8Rec, &sm.full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // D s32, A u8, B s8, K-major, N = 2 BN, M = 128
+            const uint32_t idesc = (2u << 4) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
+            for (int i = 0; i < nblk; ++i) {
+                const int s = i % NS, sa = i % kQ8NA, sd = i % kQ8ND;
+                mbar_wait_(&sm.aready[sa], (unsigned)(i / kQ8NA) & 1u);
+                mbar_wait_(&sm.full[s], (unsigned)(i / NS) & 1u);
+                mbar_wait_(&sm.dempty[sd], ((unsigned)(i / kQ8ND) & 1u) ^ 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t bt = smem_addr(sm.slot[s]);
+                const uint32_t ta = tmem + 64u * sa, td = tmem + 128u + (uint32_t)N * sd;
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    const uint64_t bd = umma_desc_sw128(bt + (m >> 2) * (N * 128) + 32 * (m & 3));
+                    const uint32_t acc = m > 0;
+                    asm volatile(
+                        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                        " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(td),
+                        "r"(ta + 8u * m), "l"(bd), "r"(idesc), "r"(acc));
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_addr(&sm.aempty[sa]))
+                             : "memory");
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_addr(&sm.dfull[sd]))
+                             : "memory");
+            }
+        }
+    } else if (warp < 6) {
+        // ---- expanders: row r = TMEM lane; A column 8 m + c = code word (8 (m & 1) + c) >> 2 (m >> 1) & 3s
+        const int q = warp & 3, r = 32 * q + lane;
+        const uint32_t ta_row = tmem + ((uint32_t)(32 * q) << 16);
+        for (int i = 0; i < nblk; ++i) {
+            const int s = i % NS, sa = i % kQ8NA;
+            mbar_wait_(&sm.full[s], (unsigned)(i / NS) & 1u);
+            const uint8_t* rec = sm.slot[s] + q8_act_bytes(BN);
+            uint32_t w[16];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint4 v = reinterpret_cast<const uint4*>(rec + c * 2048)[r];
+                w[4 * c] = v.x;
+                w[4 * c + 1] = v.y;
+                w[4 * c + 2] = v.z;
+                w[4 * c + 3] = v.w;
+            }
+            mbar_wait_(&sm.aempty[sa], ((unsigned)(i / kQ8NA) & 1u) ^ 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            uint32_t a[64];
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) a[8 * m + c] = (w[8 * (m & 1) + c] >> (2 * (m >> 1))) & 0x03030303u;
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+                "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,"
+                "%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,"
+                "%61,%62,%63,%64};" ::"r"(ta_row + 64u * sa),
+                "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]),
+                "r"(a[8]), "r"(a[9]), "r"(a[10]), "r"(a[11]), "r"(a[12]), "r"(a[13]), "r"(a[14]), "r"(a[15]),
+                "r"(a[16]), "r"(a[17]), "r"(a[18]), "r"(a[19]), "r"(a[20]), "r"(a[21]), "r"(a[22]), "r"(a[23]),
+                "r"(a[24]), "r"(a[25]), "r"(a[26]), "r"(a[27]), "r"(a[28]), "r"(a[29]), "r"(a[30]), "r"(a[31]),
+                "r"(a[32]), "r"(a[33]), "r"(a[34]), "r"(a[35]), "r"(a[36]), "r"(a[37]), "r"(a[38]), "r"(a[39]),
+                "r"(a[40]), "r"(a[41]), "r"(a[42]), "r"(a[43]), "r"(a[44]), "r"(a[45]), "r"(a[46]), "r"(a[47]),
+                "r"(a[48]), "r"(a[49]), "r"(a[50]), "r"(a[51]), "r"(a[52]), "r"(a[53]), "r"(a[54]), "r"(a[55]),
+                "r"(a[56]), "r"(a[57]), "r"(a[58]), "r"(a[59]), "r"(a[60]), "r"(a[61]), "r"(a[62]), "r"(a[63])
+                : "memory");
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_(&sm.aready[sa]);
+        }
+    } else {
+        // ---- epilogue: rows 32 q + lane, tokens [hh BN/2, (hh + 1) BN/2) ----
+        constexpr int H = BN / 2;
+        const int q = warp & 3, hh = (warp - 6) >> 2;  // TMEM lane quarter = warp % 4
+        const int r = 32 * q + lane;
+        const int64_t grow = (int64_t)rt * 128 + r;
+        const uint32_t td_row = tmem + ((uint32_t)(32 * q) << 16) + 128u;
+        float acc[H];
+#pragma unroll
+        for (int j = 0; j < H; ++j) acc[j] = 0.f;
+        for (int i = 0; i < nblk; ++i) {
+            const int s = i % NS, sd = i % kQ8ND;
+            mbar_wait_(&sm.dfull[sd], (unsigned)(i / kQ8ND) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            uint32_t c0[H], c1[H];
+            const uint32_t t0 = td_row + (uint32_t)N * sd + (uint32_t)(hh * H);
+#pragma unroll
+            for (int j = 0; j < H; j += 8) {
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                             : "=r"(c0[j]), "=r"(c0[j + 1]), "=r"(c0[j + 2]), "=r"(c0[j + 3]), "=r"(c0[j + 4]),
+                               "=r"(c0[j + 5]), "=r"(c0[j + 6]), "=r"(c0[j + 7])
+                             : "r"(t0 + j));
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                             : "=r"(c1[j]), "=r"(c1[j + 1]), "=r"(c1[j + 2]), "=r"(c1[j + 3]), "=r"(c1[j + 4]),
+                               "=r"(c1[j + 5]), "=r"(c1[j + 6]), "=r"(c1[j + 7])
+                             : "r"(t0 + BN + j));
+            }
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_(&sm.dempty[sd]);
+            const uint8_t* slot = sm.slot[s];
+            const uint8_t* rec = slot + q8_act_bytes(BN);
+            const float d = __half2float(__ushort_as_half(reinterpret_cast<const uint16_t*>(rec + 8192)[r]));
+            const float zf = (float)(1 + (int)reinterpret_cast<const int8_t*>(rec + 8192 + 256)[r]);
+            const float2* meta = reinterpret_cast<const float2*>(slot + 512 * BN) + hh * H;
+#pragma unroll
+            for (int j = 0; j < H; ++j) {
+                const float2 fc = meta[j];  // (2^(ex-4), Q 2^(ex-4)) of token hh H + j
+                const float v = (float)((int)c0[j] + 256 * (int)c1[j]);
+                acc[j] += d * (fc.x * v - zf * fc.y);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_(&sm.empty[s]);
+        }
+        if (grow < rows) {
+#pragma unroll
+            for (int j = 0; j < H; ++j) {
+                const int64_t m = (int64_t)tt * BN + hh * H + j;
+                if (m < M) y[grow * stride_r + m * stride_m] = (TY)acc[j];
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+    }
+}
+
+// Weight records [RT][NB][kQ8Rec]: codes [c 0..3][row 0..127][16 B] (code byte B of a row holds
+// elements B, 64+B, 128+B, 192+B at bit pairs 0..3, value q + 1), f16 scales [row], int8 zps [row].
+__global__ void repack_mmq8_kernel(const uint8_t* __restrict__ payload, int64_t rows, int NB, int RT, int asym,
+                                   uint8_t* __restrict__ out) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (record, row, byte B)
+    if (idx >= (int64_t)RT * NB * 128 * 64) return;
+    const int B = (int)(idx & 63), r = (int)((idx >> 6) & 127);
+    const int64_t rec = idx >> 13;
+    const int b = (int)(rec % NB);
+    const int64_t row = (rec / NB) * 128 + r;
+    uint8_t* o = out + rec * kQ8Rec;
+    uint8_t byte = 0;
+    uint16_t sb = 0;
+    int8_t z = 0;
+    if (row < rows) {
+        const uint8_t* p = payload + (row * NB + b) * 100;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int e = 64 * i + B;
+            const int c = ((p[e >> 3] >> (e & 7)) & 1) | (((p[32 + (e >> 3)] >> (e & 7)) & 1) << 1);
+            byte |= (uint8_t)(c << (2 * i));
+        }
+        sb = *reinterpret_cast<const uint16_t*>(p + 96);
+        if (asym) z = (int8_t)(int)f16_bits_to_f32(*reinterpret_cast<const uint16_t*>(p + 98));
+    }
+    o[(B >> 4) * 2048 + r * 16 + (B & 15)] = byte;
+    if (B == 0) {
+        *reinterpret_cast<uint16_t*>(o + 8192 + 2 * r) = sb;
+        reinterpret_cast<int8_t*>(o + 8192 + 256)[r] = z;
+    }
+}
+
+// Activation records [token tile][NB][q8_act_bytes(BN)]: B tile rows n = l BN + m (limb l of token
+// m), 256 k bytes as 2 SW128 k-atoms of N rows; then (2^(ex-4), Q 2^(ex-4)) per token.  One warp
+// per (block, token); the chain kernel's integer rotation with |q| <= 2^14 (two balanced limbs).
+template <typename TX>
+__global__ void rotate_act_i8_kernel(const TX* __restrict__ x, int64_t NB, int64_t M, int64_t M_pad,
+                                     int64_t stride_k, int64_t stride_m, int BN, uint8_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wid >= NB * M_pad) return;
+    const int64_t b = wid % NB, m = wid / NB;
+    const int N = 2 * BN;
+    uint8_t* rec = out + ((m / BN) * NB + b) * (int64_t)(512 * BN + 8 * BN);
+    const int mm = (int)(m % BN);
+    int v[8];
+    int ex = 0, Q = 0;
+    if (m < M) {
+        float f[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[e] = (float)x[(b * 256 + lane + 32 * e) * stride_k + m * stride_m];
+        unsigned fb = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) fb = max(fb, __float_as_uint(fabsf(f[e])));
+        fb = __reduce_max_sync(FULL, fb);
+        const float fm = __uint_as_float(fb);
+        const int e_in = fm > 0.f ? ilogbf(fm) - 21 : 0;
+        const float sc = ldexpf(1.0f, -e_in);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = __float2int_rn(f[e] * sc);
+#pragma unroll
+        for (int h = 1; h < 32; h <<= 1) {
+            const bool high = (lane & h) != 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int p = __shfl_xor_sync(FULL, v[e], h);
+                v[e] = high ? p - v[e] : v[e] + p;
+            }
+        }
+#pragma unroll
+        for (int hh = 1; hh < 8; hh <<= 1)
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if ((e & hh) == 0) {
+                    const int lo = v[e], hi = v[e + hh];
+                    v[e] = lo + hi;
+                    v[e + hh] = lo - hi;
+                }
+        unsigned amax = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) amax = max(amax, (unsigned)abs(v[e]));
+        amax = __reduce_max_sync(FULL, amax);
+        const int bl = 32 - __clz(amax);
+        const int k = max(0, bl - 14);
+        ex = e_in + k;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            v[e] = k ? ((v[e] + (1 << (k - 1))) >> k) : v[e];
+            Q += v[e];
+        }
+        Q = __reduce_add_sync(FULL, Q);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = 0;
+    }
+#pragma unroll
+    for (int e8 = 0; e8 < 8; ++e8) {
+        const int e = lane + 32 * e8;
+        const int l0 = ((v[e8] + 128) & 255) - 128;
+        const int l1 = (v[e8] - l0) >> 8;
+        const int kb = e & 127;
+        uint8_t* atom = rec + (e >> 7) * (N * 128) + (kb & 15);
+        atom[sw128_off(mm, kb >> 4)] = (uint8_t)(int8_t)l0;
+        atom[sw128_off(BN + mm, kb >> 4)] = (uint8_t)(int8_t)l1;
+    }
+    if (lane == 0) {
+        float2* meta = reinterpret_cast<float2*>(rec + 512 * BN);
+        const float f = m < M ? ldexpf(1.0f, ex - 4) : 0.f;
+        meta[mm] = make_float2(f, (float)Q * f);
+    }
+}
+
+}  // namespace itq3
+
+using namespace itq3;
+
+extern "C" int itq3_mmq8_block_n(int64_t m) { return m <= 16 ? 16 : (m <= 32 ? 32 : 64); }
+
+extern "C" int64_t itq3_mmq8_nbytes(int64_t rows, int64_t cols) {
+    return (rows + 127) / 128 * (cols / 256) * (int64_t)kQ8Rec;
+}
+
+extern "C" int itq3_repack_mmq8(const uint8_t* payload, int64_t rows, int64_t cols, int asymmetric, uint8_t* out,
+                                void* stream) {
+    if (rows <= 0 || cols <= 0 || cols % 256) {
+        set_error("itq3_repack_mmq8: needs cols %% 256 == 0 (got %lld x %lld)", (long long)rows, (long long)cols);
+        return ITQ3_E_UNSUPPORTED;
+    }
+    const int NB = (int)(cols / 256), RT = (int)((rows + 127) / 128);
+    const int64_t n = (int64_t)RT * NB * 128 * 64;
+    repack_mmq8_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(payload, rows, NB, RT, asymmetric,
+                                                                                      out);
+    return check_launch("itq3_repack_mmq8");
+}
+
+extern "C" int64_t itq3_mmq8_act_nbytes(int64_t cols, int64_t m) {
+    const int BN = itq3_mmq8_block_n(m);
+    return (m + BN - 1) / BN * (cols / 256) * (int64_t)q8_act_bytes(BN);
+}
+
+extern "C" int itq3_rotate_act_i8(const void* x, int x_dtype, int64_t cols, int64_t m, int64_t stride_k,
+                                  int64_t stride_m, uint8_t* out, void* stream) {
+    if (cols <= 0 || cols % 256 || m <= 0 || m > 64) {
+        set_error("itq3_rotate_act_i8: need cols %% 256 == 0 and 0 < m <= 64");
+        return ITQ3_E_SHAPE;
+    }
+    const int BN = itq3_mmq8_block_n(m);
+    const int64_t NB = cols / 256, M_pad = (m + BN - 1) / BN * BN;
+    const unsigned grid = (unsigned)((NB * M_pad * 32 + 255) / 256);
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (x_dtype) {
+        case ITQ3_F32:
+            rotate_act_i8_kernel<float><<<grid, 256, 0, s>>>((const float*)x, NB, m, M_pad, stride_k, stride_m, BN, out);
+            break;
+        case ITQ3_BF16:
+            rotate_act_i8_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, NB, m, M_pad, stride_k,
+                                                                     stride_m, BN, out);
+            break;
+        case ITQ3_F16:
+            rotate_act_i8_kernel<__half><<<grid, 256, 0, s>>>((const __half*)x, NB, m, M_pad, stride_k, stride_m, BN,
+                                                              out);
+            break;
+        default:
+            set_error("itq3_rotate_act_i8: unsupported dtype %d", x_dtype);
+            return ITQ3_E_DOMAIN;
+    }
+    return check_launch("itq3_rotate_act_i8");
+}
+
+static int mmq8_splits(int64_t rows, int64_t cols, int64_t m) {
+    const int BN = itq3_mmq8_block_n(m);
+    const int64_t tiles = (rows + 127) / 128 * ((m + BN - 1) / BN);
+    const int64_t NB = cols / 256;
+    int64_t ks = 148 / tiles;                 // one wave (one CTA per SM): tiles x ks <= 148
+    ks = ks < NB / 2 ? ks : NB / 2;           // >= 2 blocks per split
+    return (int)(ks < 1 ? 1 : ks);
+}
+
+extern "C" int64_t itq3_mmq8_ws_nbytes(int64_t rows, int64_t cols, int64_t m) {
+    const int ks = mmq8_splits(rows, cols, m);
+    return ks > 1 ? (int64_t)ks * rows * m * (int64_t)sizeof(float) : 0;
+}
+
+template <int BN, typename TY>
+static int launch_mmq8(const uint8_t* w, int64_t rows, int64_t cols, const uint8_t* act, int64_t m, TY* y,
+                       int64_t sr, int64_t sm_, float* ws, cudaStream_t s) {
+    const int smem = (int)sizeof(Q8Smem<BN>) + 1024;
+    static bool attr = false, attr32 = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(mmq8_kernel<BN, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+            return check_launch("itq3_mmq8: smem attribute");
+        attr = true;
+    }
+    const int NB = (int)(cols / 256);
+    const int ks = ws ? mmq8_splits(rows, cols, m) : 1;
+    const dim3 grid((unsigned)((rows + 127) / 128), (unsigned)((m + BN - 1) / BN), (unsigned)ks);
+    if (ks == 1) {
+        mmq8_kernel<BN, TY><<<grid, kQ8Threads, smem, s>>>(w, NB, act, rows, m, y, sr, sm_, 0);
+        return check_launch("itq3_mmq8");
+    }
+    if (!attr32) {
+        if (cudaFuncSetAttribute(mmq8_kernel<BN, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+            cudaSuccess)
+            return check_launch("itq3_mmq8: smem attribute");
+        attr32 = true;
+    }
+    mmq8_kernel<BN, float><<<grid, kQ8Threads, smem, s>>>(w, NB, act, rows, m, ws, m, 1, rows * m);
+    int rc = check_launch("itq3_mmq8 (split-K)");
+    if (rc) return rc;
+    const int64_t n = rows * m;
+    mmq_splitk_reduce<TY><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ws, ks, rows, m, y, sr, sm_);
+    return check_launch("itq3_mmq8 (split-K reduce)");
+}
+
+extern "C" int itq3_mmq8(const uint8_t* w, int64_t rows, int64_t cols, const uint8_t* act, int64_t m, void* y,
+                         int y_dtype, int64_t stride_r, int64_t stride_m, void* workspace, void* stream) {
+    if (rows <= 0 || cols <= 0 || cols % 256 || m <= 0 || m > 64) {
+        set_error("itq3_mmq8: bad shape (needs cols %% 256 == 0, 0 < m <= 64)");
+        return ITQ3_E_SHAPE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const int BN = itq3_mmq8_block_n(m);
+    float* ws = (float*)workspace;
+    if (y_dtype == ITQ3_F32) {
+        if (BN == 16) return launch_mmq8<16>(w, rows, cols, act, m, (float*)y, stride_r, stride_m, ws, s);
+        if (BN == 32) return launch_mmq8<32>(w, rows, cols, act, m, (float*)y, stride_r, stride_m, ws, s);
+        return launch_mmq8<64>(w, rows, cols, act, m, (float*)y, stride_r, stride_m, ws, s);
+    }
+    if (y_dtype == ITQ3_BF16) {
+        if (BN == 16) return launch_mmq8<16>(w, rows, cols, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s);
+        if (BN == 32) return launch_mmq8<32>(w, rows, cols, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s);
+        return launch_mmq8<64>(w, rows, cols, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s);
+    }
+    set_error("itq3_mmq8: output dtype must be float32 or bfloat16");
+    return ITQ3_E_DOMAIN;
+}

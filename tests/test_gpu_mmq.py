@@ -1,4 +1,7 @@
-"""GPU: K5 tcgen05 MMQ (csrc/mmq.cu) vs the exact fp64 product of the oracle-decoded weights.
+"""GPU: K5 / K5b tcgen05 MMQ (csrc/mmq.cu) vs the exact fp64 product of the oracle-decoded weights.
+
+fused_matmul sends 16 <= M <= 64 tokens to K5b (kind::i8, 16-bit fixed-point activations per
+(token, block): test_gpu_stack.chain_bound at L = 2 per column) and M > 64 to K5 (kind::f16):
 
 Tolerance: A = d*t is exact in f16, so the error comes only from the f16
 rounding of the rotated activations x'' = H x / 16 (relative 2^-11 per element) and the fp32
@@ -31,6 +34,17 @@ def mmq_bound(payload, rows, cols, X):
     return deq @ Xd, a @ term + 1e-5 * (np.abs(deq) @ np.abs(Xd))
 
 
+def matmul_bound(payload, rows, cols, X):
+    """The a-priori bound of the path fused_matmul takes for X's token count (compute.py)."""
+    m = X.shape[1]
+    if P.compute.MMQ_MIN_TOKENS <= m <= P.compute.MMQ8_MAX_TOKENS:
+        from test_gpu_stack import chain_bound
+
+        cols_ = [chain_bound(payload, rows, cols, np.asarray(X, np.float64)[:, j], limbs=2) for j in range(m)]
+        return np.stack([c[0] for c in cols_], axis=1), np.stack([c[1] for c in cols_], axis=1)
+    return mmq_bound(payload, rows, cols, X)
+
+
 @pytest.mark.parametrize("rows,cols", [(300, 512), (128, 1024), (1000, 256)])
 @pytest.mark.parametrize("m", [16, 64, 100, 256, 300])
 @pytest.mark.parametrize("asym", [False, True])
@@ -40,7 +54,7 @@ def test_mmq_matches_exact(rows, cols, m, asym):
     q = P.quantize_tensor(w, P.QuantConfig(symmetric=not asym))
     X = rng.standard_normal((cols, m)).astype(np.float32)
     Y = P.fused_matmul(q, torch.from_numpy(X).cuda()).cpu().numpy().astype(np.float64)
-    exact, bound = mmq_bound(q.payload().cpu().numpy(), rows, cols, X)
+    exact, bound = matmul_bound(q.payload().cpu().numpy(), rows, cols, X)
     assert np.all(np.abs(Y - exact) <= bound), np.max(np.abs(Y - exact) / bound)
 
 
@@ -51,7 +65,7 @@ def test_mmq_dtypes_and_strides():
     Y = P.fused_matmul(q, X)
     for dt in (torch.bfloat16, torch.float16):
         Yd = P.fused_matmul(q, X.to(dt)).cpu().numpy()
-        exact, bound = mmq_bound(q.payload().cpu().numpy(), 256, 768, X.to(dt).float().cpu().numpy())
+        exact, bound = matmul_bound(q.payload().cpu().numpy(), 256, 768, X.to(dt).float().cpu().numpy())
         assert np.all(np.abs(Yd - exact) <= bound)
     # token-major activations (M x K transposed view) -> identical result
     Y2 = P.fused_matmul(q, X.t().contiguous().t())

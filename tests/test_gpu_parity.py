@@ -135,10 +135,10 @@ def test_mmq_sample_against_reference(golden):
     q = P.quantize_tensor(w)
     Y_ref = np.load(f"tests/golden/{c['y_file']}")
     np.testing.assert_allclose(P.fused_matmul(q, X), Y_ref, rtol=1e-5, atol=1e-12)
-    Yp = P.fused_matmul(q, torch.from_numpy(X).cuda()).cpu().numpy()  # M = 16 -> tcgen05 MMQ
-    from test_gpu_mmq import mmq_bound
+    Yp = P.fused_matmul(q, torch.from_numpy(X).cuda()).cpu().numpy()  # M = 16 -> tcgen05 MMQ (kind::i8)
+    from test_gpu_mmq import matmul_bound
 
-    _, bound = mmq_bound(q.payload().cpu().numpy(), 256, 4096, X)
+    _, bound = matmul_bound(q.payload().cpu().numpy(), 256, 4096, X)
     assert np.all(np.abs(Yp - Y_ref) <= bound)
 
 

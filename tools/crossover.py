@@ -53,6 +53,7 @@ def main():
         qs = [P.quantize_tensor(torch.randn((rows, K), generator=g, device=dev) / K ** 0.5) for _ in range(ncopy)]
         tiled = [q.tiled() for q in qs]
         mmq = [q.mmq_layout() for q in qs]
+        mmq8 = [q.mmq8_layout() for q in qs]
         for M in MS:
             X = torch.randn((K, M), generator=g, device=dev)
             Y = torch.empty((rows, M), dtype=torch.float32, device=dev)
@@ -76,12 +77,26 @@ def main():
                 _lib.call("itq3_mmq", _lib.ptr(mmq[i % ncopy]), rows, K, 0, _lib.ptr(actf), M, _lib.ptr(Y), _lib.F32,
                           Y.stride(0), Y.stride(1), _lib.ptr(ws) if wsn else None, s)
 
+            act8 = torch.empty(lib.itq3_mmq8_act_nbytes(K, M), dtype=torch.uint8, device=dev) if M <= 64 else None
+            ws8n = lib.itq3_mmq8_ws_nbytes(rows, K, M) if M <= 64 else 0
+            ws8 = torch.empty(max(ws8n, 1), dtype=torch.uint8, device=dev)
+
+            def mmq8f(i):
+                s = _lib.stream_ptr(dev)
+                _lib.call("itq3_rotate_act_i8", _lib.ptr(X), _lib.F32, K, M, X.stride(0), X.stride(1), _lib.ptr(act8), s)
+                _lib.call("itq3_mmq8", _lib.ptr(mmq8[i % ncopy]), rows, K, _lib.ptr(act8), M, _lib.ptr(Y), _lib.F32,
+                          Y.stride(0), Y.stride(1), _lib.ptr(ws8) if ws8n else None, s)
+
             row = {"rows": rows, "K": K, "M": M}
-            for name, fn in (("gemv_us", gemv), ("mmq_us", mmqf)):
+            for name, fn in (("gemv_us", gemv), ("mmq_us", mmqf), ("mmq8_us", mmq8f)):
                 if name == "mmq_us" and M < 8:
+                    continue
+                if name == "mmq8_us" and M > 64:
                     continue
                 row[name] = graph_time(fn, 20) * 1000
             row["weight_gbps_gemv"] = rows * K * 66 / 256 / (row["gemv_us"] * 1e-6) / 1e9
+            if "mmq8_us" in row:
+                row["weight_gbps_mmq8"] = rows * K * 67 / 256 / (row["mmq8_us"] * 1e-6) / 1e9
             print(json.dumps(row), flush=True)
             out.append(row)
     return out

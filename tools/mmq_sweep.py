@@ -45,6 +45,10 @@ SHAPES = [(4096, 4096), (1024, 4096), (14336, 4096), (4096, 14336)]
 MS = [16, 32, 64, 128, 256, 512, 1024, 2048]
 
 
+def M_SMALL(m):
+    return P.compute.MMQ_MIN_TOKENS <= m <= P.compute.MMQ8_MAX_TOKENS
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
@@ -62,25 +66,33 @@ def main():
         ncopy = max(2, int(160e6 // (rows * K * 66 / 256)) + 1)
         for c in range(min(ncopy, 8)):
             q = P.quantize_tensor(torch.randn((rows, K), generator=g, device=dev) / K ** 0.5)
-            copies.append(q.mmq_layout())
+            copies.append((q.mmq_layout(), q.mmq8_layout()))
         for M in MS:
             X = torch.randn((K, M), generator=g, device=dev)
-            act = torch.empty(lib.itq3_mmq_act_nbytes(K, M), dtype=torch.uint8, device=dev)
+            small = M_SMALL(M)
+            act = torch.empty(lib.itq3_mmq8_act_nbytes(K, M) if small else lib.itq3_mmq_act_nbytes(K, M),
+                              dtype=torch.uint8, device=dev)
             Y = torch.empty((rows, M), dtype=torch.float32, device=dev)
-            wsn = lib.itq3_mmq_ws_nbytes(rows, K, M)
+            wsn = lib.itq3_mmq8_ws_nbytes(rows, K, M) if small else lib.itq3_mmq_ws_nbytes(rows, K, M)
             ws = torch.empty(max(wsn, 1), dtype=torch.uint8, device=dev)
 
             def run(i):
                 s = _lib.stream_ptr(dev)
+                if small:  # K5b, kind::i8 (compute.py routes 16 <= M <= 64 here)
+                    _lib.call("itq3_rotate_act_i8", _lib.ptr(X), _lib.F32, K, M, X.stride(0), X.stride(1),
+                              _lib.ptr(act), s)
+                    _lib.call("itq3_mmq8", _lib.ptr(copies[i % len(copies)][1]), rows, K, _lib.ptr(act), M,
+                              _lib.ptr(Y), _lib.F32, Y.stride(0), Y.stride(1), _lib.ptr(ws) if wsn else None, s)
+                    return
                 _lib.call("itq3_rotate_act_f16", _lib.ptr(X), _lib.F32, K, M, X.stride(0), X.stride(1),
                           _lib.ptr(act), s)
-                _lib.call("itq3_mmq", _lib.ptr(copies[i % len(copies)]), rows, K, 0, _lib.ptr(act), M, _lib.ptr(Y),
+                _lib.call("itq3_mmq", _lib.ptr(copies[i % len(copies)][0]), rows, K, 0, _lib.ptr(act), M, _lib.ptr(Y),
                           _lib.F32, Y.stride(0), Y.stride(1), _lib.ptr(ws) if wsn else None, s)
 
             ms = graph_time(run, args.reps)
             tf = 2.0 * rows * K * M / (ms * 1e-3) / 1e12
             wbytes = rows * K * 66 / 256
-            r = {"rows": rows, "K": K, "M": M, "us": ms * 1e3, "tflops": tf, "frac_of_bf16_peak": tf / peak,
+            r = {"rows": rows, "K": K, "M": M, "kernel": "K5b kind::i8" if small else "K5 kind::f16", "us": ms * 1e3, "tflops": tf, "frac_of_bf16_peak": tf / peak,
                  "weight_gbps": wbytes / (ms * 1e-3) / 1e9}
             res.append(r)
             print(json.dumps(r), flush=True)
