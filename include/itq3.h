@@ -112,6 +112,9 @@ int itq3_rotate_act_f16(const void* x, int x_dtype, int64_t cols, int64_t m, int
 /* workspace: itq3_mmq_ws_nbytes(rows, cols, m) bytes (may be 0 -> pass NULL); with a workspace,
  * small problems are split along K across CTAs and reduced in fixed order (deterministic). */
 int64_t itq3_mmq_ws_nbytes(int64_t rows, int64_t cols, int64_t m);
+/* diagnostics: device buffer of 16 u64 counters per CTA (cycle accounting per warp role of the next
+ * itq3_mmq launches; tools/mmq_trace.py), or NULL to switch the accounting off. */
+int itq3_mmq_set_trace(void* buf);
 int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asymmetric, const uint8_t* act, int64_t m, void* y,
              int y_dtype, int64_t stride_r, int64_t stride_m, void* workspace, void* stream);
 

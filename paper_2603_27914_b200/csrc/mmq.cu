@@ -5,17 +5,30 @@
 // the whole K reduction stays in one fp32 TMEM accumulator with no per-block promotion; the
 // only approximation is B = f16(H x / 16).
 //
-// Per CTA: 128 weight rows x BN tokens.  Warp roles (10 warps):
-//   warp 0    producer: cp.async.bulk of the 2-bit code slab (128 rows x 64 k = 2 KB) and of the
-//             pre-swizzled activation tile (BN x 64 k f16) per K-chunk into an NL-deep LOAD ring
-//             (12 slots at BN = 64: enough bytes in flight to hide HBM latency at small M);
-//   warp 1    MMA issuer (one thread): 4 x tcgen05.mma (K = 16) per chunk, tcgen05.commit frees
-//             the A slot and the load slot; the final commit signals the epilogue;
-//   warps 2-9 expanders, two threads per weight row: 2-bit codes -> f16 d*t written into an
-//             NA-deep ring of A tiles in the
-//             SWIZZLE_128B K-major canonical layout (magic-number decode: 4 ops per f16x2; exact
-//             while 2|d| < 65504),
-//             then the epilogue (tcgen05.ld 32x32b -> fp32/bf16 stores).
+// One persistent CTA PAIR (cluster of 2, cta_group::2) per TPC computes 256 weight rows x 256
+// tokens per tile with M = 256, N = 256, K = 16 MMAs issued by the leader CTA.  Each SM holds
+//   * its 128 rows of A in TMEM (expanded there from the 2-bit codes by tcgen05.st, so the weight
+//     operand never touches shared memory: smem carries B and a 4.4 KB weight record per stage),
+//   * its 128-token half of the B tile (f16, SWIZZLE_128B K-major),
+//   * its 128 rows of the 256-column fp32 accumulator.
+// The K loop runs in 128-k stages with exactly TWO bulk copies per stage and CTA (weight record,
+// B half): a cp.async.bulk costs ~76 cycles of producer issue whatever its size
+// (tools/probes/bulk_issue_probe.cu).  N = 256 per MMA halves the per-flop instruction load of the
+// MMA issuer and of the expanders, which share the SM sub-partitions' issue slots (N = 128 tiles ran
+// at ~55% of the tensor rate for that reason; tools/mmq_trace.py).
+// Warp roles (14 warps per CTA):
+//   warp 0     producer: the two bulk copies per stage into a 4-deep ring (full/lempty mbarriers;
+//              lempty is signalled by the pair's multicast tcgen05.commit);
+//   warp 1     TMEM allocation (cta_group::2, all 512 columns: D = [0, 256), A ring = 4 x 64 columns);
+//              in the leader CTA lane 0 issues the 8 MMAs of a stage once both CTAs' expanders
+//              arrived on the leader's `ready` (relaxed remote mbarrier arrivals: no MEMBAR.GPU);
+//   warps 2-9  expanders, two quads taking alternate stages, one weight row per thread (TMEM lane
+//              quarter = warp % 4): codes -> f16 d*t (magic-number decode, 4 ops per f16x2),
+//              two tcgen05.st.32x32b.x32 per stage;
+//   warps 10-13 epilogue: tcgen05.ld of the row's 256 fp32 columns in two halves, each staged in smem
+//              and written with ONE bulk store (cp.async.bulk shared -> global) per row and half,
+//              or plain stores for ragged/strided outputs; the accumulator is released to the
+//              leader as soon as it is read.
 // Layouts written by itq3_repack_mmq / itq3_rotate_act_f16 (host ABI below).
 #include "common.cuh"
 
@@ -23,8 +36,9 @@ namespace itq3 {
 
 constexpr int kMmqBM = 128;
 constexpr int kMmqBK = 64;  // one 128-byte swizzle atom of f16 per row
-constexpr int kMmqExpWarps = 8;  // 2 per weight row (each half of the 64-k chunk)
-constexpr int kMmqThreads = 32 * (2 + kMmqExpWarps);
+constexpr int kMmqExpGroups = 2;  // expander warp quads; group e decodes the chunks g with g % 2 == e
+constexpr int kMmqEpiWarp = 2 + 4 * kMmqExpGroups;
+constexpr int kMmqThreads = 32 * (kMmqEpiWarp + 4);  // producer, MMA, expander quads, 4 epilogue warps
 constexpr int kMmqCodeChunk = kMmqBM * 16;  // 2 KB: 128 rows x 64 codes x 2 bits
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -66,203 +80,409 @@ __device__ __forceinline__ uint32_t umma_idesc_f16() {
     return (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kMmqBM >> 4) << 24);
 }
 
-// Two rings: LOAD slots (codes + scales + zero-points + the B tile of one 64-k chunk, filled by TMA,
-// freed by the MMA commit) are many and small, so enough bulk copies are in flight to cover the
-// HBM latency even when the chunk's compute is short (small M); A slots (expanded f16 tiles) are few.
-template <int BN, int NL, int NA>
-struct MmqSmem {
-    uint8_t a[NA][kMmqBM * 128];   // expanded f16 A tiles (1024-aligned)
-    uint8_t b[NL][BN * 128];       // activation tiles (pre-swizzled in global)
-    uint8_t codes[NL][kMmqCodeChunk];
-    uint16_t scl[NL][kMmqBM];  // f16 scales of the chunk's 256-block (bulk-copied with the codes)
-    int8_t zp[NL][kMmqBM];
-    uint64_t full[NL];    // codes + scales + B landed (TMA)
-    uint64_t lempty[NL];  // MMA consumed the load slot (tcgen05.commit)
-    uint64_t aready[NA];  // A expanded (all expander threads)
-    uint64_t aempty[NA];  // MMA consumed the A slot (tcgen05.commit)
-    uint64_t accum;       // all MMAs done
-    uint32_t tmem_base;
-};
-
 // swizzled byte offset of (row r, 16-byte chunk j) inside a K-major SW128 tile
 __device__ __forceinline__ uint32_t sw128_off(int r, int j) {
     return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((j ^ (r & 7)) << 4));
 }
 
-template <int BN, int NL, int NA, typename TY>
-__global__ void __launch_bounds__(kMmqThreads, 1)
-    mmq_kernel(const uint8_t* __restrict__ codes, const uint16_t* __restrict__ scales, const int8_t* __restrict__ zps,
-               int rows_pad, int NC, const uint8_t* __restrict__ act, int64_t rows, int64_t M, TY* __restrict__ y,
-               int64_t stride_r, int64_t stride_m, int64_t slab) {
+// ---- cluster / pair helpers ----
+__device__ __forceinline__ uint32_t cta_rank_in_cluster() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// acquire at cluster scope: the barrier also collects arrivals from the peer CTA
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "W_%=:\n"
+        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra W_%=;\n}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+// arrive on the barrier at the same smem offset in CTA `cta` of the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(bar)), "r"(cta));
+    // relaxed: what the arrival publishes is TMEM (tcgen05.wait + fence::before_thread_sync) or
+    // TMA-landed smem, never generic stores, so no release fence (MEMBAR.GPU) is needed
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint16_t lds16(uint32_t a) {
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int lds_s8(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.s8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+// tcgen05.commit of the pair's MMAs to the barrier at this offset in both CTAs
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_addr(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
+// Optional per-CTA cycle accounting (tools/mmq_trace.py): 16 counters per CTA, null = off.
+__device__ unsigned long long* g_mmq_trace = nullptr;
+#define MMQ_T0() const long long _t0 = clock64()
+#define MMQ_ACC(slot, var) var += clock64() - _t0
+
+// Per CTA of the pair: 128 weight rows (A, expanded into TMEM) and 64 of the tile's 128 tokens (B, smem).
+// The K loop runs in STAGES of 128 k: per stage and CTA exactly two bulk copies (a 4480-byte weight
+// record and a 16 KB B half tile), because every cp.async.bulk costs ~76 cycles of issue in the
+// producer thread whatever its size (tools/probes/bulk_issue_probe.cu) -- 8 MMAs (512 tensor cycles)
+// per stage leave the producer ample slack.
+// TMEM (512 columns, both CTAs): D[2] = columns [0, 256) (two 128-token fp32 accumulators, so the
+// epilogue of one tile overlaps the main loop of the next), A ring = [256, 512) (4 slots x 64 columns:
+// a 128-k stage of f16 d*t, two k per 32-bit column).
+constexpr int kStK = 128;                       // k per stage
+constexpr int kWRec = 4096 + 256 + 128;         // weight record: codes [2 halves][128 rows][16 B] | f16 scales | int8 zps
+constexpr int kPairNL = 4;                      // load ring (bulk copies)
+constexpr int kPairNA = 4;                      // A ring in TMEM
+constexpr int kPairStage = 132;  // fp32 words per staged output row (128 + 4 pad: conflict-free v4 stores)
+struct PairSmem {
+    uint8_t b[kPairNL][128 * 2 * 128];  // B half tile: 2 x (128 token rows x 64 k f16, SW128 K-major), 1024-aligned
+    uint8_t w[kPairNL][kWRec];          // weight record of the stage (this CTA's 128 rows)
+    float stage[kMmqBM][kPairStage];    // epilogue staging for the bulk row stores
+    uint64_t full[kPairNL];    // this CTA's weight record + B half landed (TMA)
+    uint64_t lempty[kPairNL];  // the pair's MMAs consumed load slot s (multicast commit, both CTAs)
+    uint64_t aempty[kPairNA];  // the pair's MMAs consumed A slot s (multicast commit, both CTAs)
+    uint64_t ready[kPairNA];   // leader only: A slot s expanded and its B landed in both CTAs (8 warp arrivals)
+    uint64_t dfull;            // accumulator complete (multicast commit)
+    uint64_t dempty;           // leader only: both CTAs' epilogues drained the accumulator (8 warp arrivals)
+    uint32_t tmem_base;
+};
+
+// Work item = (split, token tile, pair row tile); every role walks the same sequence.
+struct PairWork {
+    int tiles_r, tiles_n, ks, NS;  // NS = stages along K
+    __device__ void decode(int it, int& tr, int& tn, int& s0, int& s1) const {
+        const int per = tiles_r * tiles_n;
+        const int sp = it / per, rem = it % per;
+        tn = rem / tiles_r;
+        tr = rem % tiles_r;
+        s0 = (int)((int64_t)sp * NS / ks);
+        s1 = (int)((int64_t)(sp + 1) * NS / ks);
+    }
+};
+
+template <typename TY>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
+    mmq_pair_kernel(const uint8_t* __restrict__ wrec, int asym, PairWork wk, const uint8_t* __restrict__ act,
+                    int64_t rows, int64_t M, TY* __restrict__ y, int64_t stride_r, int64_t stride_m, int64_t slab) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // 1024-byte alignment for the swizzled tiles
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    MmqSmem<BN, NL, NA>& sm = *reinterpret_cast<MmqSmem<BN, NL, NA>*>(base);
+    PairSmem& sm = *reinterpret_cast<PairSmem*>(base);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int rt = blockIdx.x, nt = blockIdx.y;
-    // split-K: this CTA reduces K-chunks [kc0, kc1); partial outputs go to slab blockIdx.z
-    const int kc0 = (int)((int64_t)blockIdx.z * NC / gridDim.z), kc1 = (int)((int64_t)(blockIdx.z + 1) * NC / gridDim.z);
-    y += (int64_t)blockIdx.z * slab;
+    const uint32_t rank = cta_rank_in_cluster();
+    const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+    const int items = wk.tiles_r * wk.tiles_n * wk.ks;
+    constexpr uint32_t kColA = 256;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NL; ++s) {
+        for (int s = 0; s < kPairNL; ++s) {
             mbar_init_(&sm.full[s], 1);
             mbar_init_(&sm.lempty[s], 1);
         }
-        for (int s = 0; s < NA; ++s) {
-            mbar_init_(&sm.aready[s], 32 * kMmqExpWarps);
+        for (int s = 0; s < kPairNA; ++s) {
             mbar_init_(&sm.aempty[s], 1);
+            mbar_init_(&sm.ready[s], 8);
         }
-        mbar_init_(&sm.accum, 1);
+        mbar_init_(&sm.dfull, 1);
+        mbar_init_(&sm.dempty, 8);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 1) {  // TMEM allocation (whole warp), BN fp32 columns x 128 lanes
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&sm.tmem_base)),
-                     "r"(BN < 32 ? 32 : BN));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (warp == 1) {  // the whole TMEM of both SMs of the pair
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(&sm.tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
+    cluster_sync_all();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = sm.tmem_base;
+    // diagnostics only (tools/mmq_trace.py --flags): 1 = no B loads, 2 = no A stores
+    const unsigned dflags = g_mmq_trace ? (unsigned)g_mmq_trace[4095 * 16] : 0u;
 
     if (warp == 0) {
-        if (lane == 0) {
-            const uint8_t* cbase = codes + (int64_t)rt * kMmqCodeChunk;
-            const uint8_t* bbase = act + (int64_t)nt * NC * BN * 128;
-            for (int kc = kc0; kc < kc1; ++kc) {
-                const int s = (kc - kc0) % NL;
-                const unsigned ph = (unsigned)((kc - kc0) / NL) & 1u;
-                mbar_wait_(&sm.lempty[s], ph ^ 1u);
-                const int64_t soff = (int64_t)(kc >> 2) * rows_pad + (int64_t)rt * kMmqBM;
-                mbar_expect_tx_(&sm.full[s], kMmqCodeChunk + BN * 128 + kMmqBM * 2 + (zps ? kMmqBM : 0));
-                bulk_g2s_(sm.codes[s], cbase + (int64_t)kc * rows_pad * 16, kMmqCodeChunk, &sm.full[s]);
-                bulk_g2s_(sm.b[s], bbase + (int64_t)kc * BN * 128, BN * 128, &sm.full[s]);
-                bulk_g2s_(sm.scl[s], scales + soff, kMmqBM * 2, &sm.full[s]);
-                if (zps) bulk_g2s_(sm.zp[s], zps + soff, kMmqBM, &sm.full[s]);
+        if (lane == 0) {  // producer: this CTA's weight record and 64-token half of B, one copy each per stage
+            uint32_t g = 0;
+            long long tw = 0, t_issue = 0;
+            const long long tk0 = clock64();
+            for (int it = cluster; it < items; it += nclusters) {
+                int tr, tn, s0, s1;
+                wk.decode(it, tr, tn, s0, s1);
+                const uint8_t* wsrc = wrec + ((int64_t)(2 * tr + rank) * wk.NS) * kWRec;
+                const uint8_t* bsrc = act + ((int64_t)(2 * tn + rank) * wk.NS) * (2 * 16384);
+                for (int st = s0; st < s1; ++st, ++g) {
+                    const int s = g % kPairNL;
+                    {
+                        MMQ_T0();
+                        mbar_wait_(&sm.lempty[s], ((g / kPairNL) & 1u) ^ 1u);
+                        MMQ_ACC(0, tw);
+                    }
+                    const long long ti0 = clock64();
+                    mbar_expect_tx_(&sm.full[s], kWRec + ((dflags & 1) ? 0 : 2 * 16384));
+                    bulk_g2s_(sm.w[s], wsrc + (int64_t)st * kWRec, kWRec, &sm.full[s]);
+                    if (!(dflags & 1)) bulk_g2s_(sm.b[s], bsrc + (int64_t)st * (2 * 16384), 2 * 16384, &sm.full[s]);
+                    t_issue += clock64() - ti0;
+                }
+            }
+            if (unsigned long long* trc = g_mmq_trace) {
+                trc[blockIdx.x * 16 + 10] = t_issue;
+                trc[blockIdx.x * 16 + 0] = tw;
+                trc[blockIdx.x * 16 + 7] = clock64() - tk0;
+                trc[blockIdx.x * 16 + 8] = g;
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            const uint32_t idesc = umma_idesc_f16<BN>();
-            for (int kc = kc0; kc < kc1; ++kc) {
-                const int s = (kc - kc0) % NL, sa = (kc - kc0) % NA;
-                mbar_wait_(&sm.aready[sa], (unsigned)((kc - kc0) / NA) & 1u);
-                mbar_wait_(&sm.full[s], (unsigned)((kc - kc0) / NL) & 1u);
+        if (rank == 0 && lane == 0) {  // MMA issuer of the pair: M = 256 (128 rows per SM), N = 256, K = 16
+            const uint32_t idesc = (1u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+            uint32_t g = 0, t = 0;
+            long long tw_ready = 0, tw_d = 0;
+            const long long tm0 = clock64();
+            for (int it = cluster; it < items; it += nclusters, ++t) {
+                int tr, tn, s0, s1;
+                wk.decode(it, tr, tn, s0, s1);
+                {
+                    MMQ_T0();
+                    mbar_wait_(&sm.dempty, (t & 1u) ^ 1u);
+                    MMQ_ACC(4, tw_d);
+                }
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t a0 = smem_addr(sm.a[sa]), b0 = smem_addr(sm.b[s]);
+                const uint32_t td = tmem;
+                for (int st = s0; st < s1; ++st, ++g) {
+                    const int s = g % kPairNL, sa = g % kPairNA;
+                    {
+                        MMQ_T0();
+                        mbar_wait_(&sm.ready[sa], (g / kPairNA) & 1u);
+                        MMQ_ACC(3, tw_ready);
+                    }
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t ta = tmem + kColA + 64u * sa, b0 = smem_addr(sm.b[s]);
 #pragma unroll
-                for (int k = 0; k < kMmqBK / 16; ++k) {
-                    const uint64_t ad = umma_desc_sw128(a0 + 32 * k), bd = umma_desc_sw128(b0 + 32 * k);
-                    const uint32_t acc = ((kc - kc0) | k) != 0;
+                    for (int k = 0; k < kStK / 16; ++k) {
+                        const uint64_t bd = umma_desc_sw128(b0 + (k >> 2) * 16384 + 32 * (k & 3));
+                        const uint32_t accum = (st != s0) || (k != 0);
+                        asm volatile(
+                            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                            " tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(td),
+                            "r"(ta + 8u * k), "l"(bd), "r"(idesc), "r"(accum));
+                    }
+                    umma_commit_pair(&sm.aempty[sa]);
+                    umma_commit_pair(&sm.lempty[s]);
+                }
+                umma_commit_pair(&sm.dfull);
+            }
+            if (unsigned long long* trc = g_mmq_trace) {
+                trc[blockIdx.x * 16 + 3] = tw_ready;
+                trc[blockIdx.x * 16 + 4] = tw_d;
+                trc[blockIdx.x * 16 + 9] = clock64() - tm0;
+            }
+        }
+    } else if (warp < kMmqEpiWarp) {
+        // ---- expanders: row r = TMEM lane; 2-bit codes -> f16 d*t, two tcgen05.st of 32 columns per stage.
+        // kMmqExpGroups quads take alternate stages so one quad's tcgen05.st latency overlaps the other's decode.
+        const int q = warp & 3, r = 32 * q + lane, eg = (warp - 2) >> 2;
+        const uint32_t ta_row = tmem + ((uint32_t)(32 * q) << 16) + kColA;
+        uint32_t g = 0;
+        long long tw_full = 0, t_work = 0, tw_aempty = 0;
+        for (int it = cluster; it < items; it += nclusters) {
+            int tr, tn, s0, s1;
+            wk.decode(it, tr, tn, s0, s1);
+            for (int st = s0; st < s1; ++st, ++g) {
+                if ((int)(g % kMmqExpGroups) != eg) continue;
+                const int s = g % kPairNL, sa = g % kPairNA;
+                {
+                    MMQ_T0();
+                    mbar_wait_(&sm.full[s], (g / kPairNL) & 1u);
+                    MMQ_ACC(1, tw_full);
+                    const long long ta0 = clock64();
+                    mbar_wait_(&sm.aempty[sa], ((g / kPairNA) & 1u) ^ 1u);
+                    tw_aempty += clock64() - ta0;
+                }
+                const long long tw0 = clock64();
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t wa = smem_addr(sm.w[s]);
+                const uint16_t dh = lds16(wa + 4096 + 2 * r);
+                const int z = asym ? lds_s8(wa + 4352 + r) : 0;
+                const __half d = __ushort_as_half(dh);
+                const __half ndz = __hmul(d, __int2half_rn(-1 - z));  // exact: -(1 + z) in {0,-1,-2}
+                const uint32_t d2 = (uint32_t)dh | ((uint32_t)dh << 16);
+                const uint32_t ndz2 = (uint32_t)__half_as_ushort(ndz) * 0x10001u;
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {  // 64-k half j of the stage: A columns 32 j .. 32 j + 31
+                    const uint4 w4 = lds128(wa + 2048 * j + 16 * r);
+                    const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+                    uint32_t a[32];
+#pragma unroll
+                    for (int wi = 0; wi < 4; ++wi)
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) {  // column 8 wi + m = k pair (16 wi + 2 m, +1)
+                            const uint32_t v = ((wv[wi] >> (2 * m)) & 0x00030003u) | 0x64006400u;  // f16x2 1024 + c
+                            __half2 hv =
+                                __hsub2(*reinterpret_cast<const __half2*>(&v), __floats2half2_rn(1024.f, 1024.f));
+                            hv = __hfma2(hv, *reinterpret_cast<const __half2*>(&d2),
+                                         *reinterpret_cast<const __half2*>(&ndz2));
+                            a[8 * wi + m] = *reinterpret_cast<uint32_t*>(&hv);
+                        }
+                    if (!(dflags & 2))
                     asm volatile(
-                        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-                        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+                        "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
+                            ta_row + 64u * sa + 32u * j),
+                        "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]),
+                        "r"(a[8]), "r"(a[9]), "r"(a[10]), "r"(a[11]), "r"(a[12]), "r"(a[13]), "r"(a[14]), "r"(a[15]),
+                        "r"(a[16]), "r"(a[17]), "r"(a[18]), "r"(a[19]), "r"(a[20]), "r"(a[21]), "r"(a[22]), "r"(a[23]),
+                        "r"(a[24]), "r"(a[25]), "r"(a[26]), "r"(a[27]), "r"(a[28]), "r"(a[29]), "r"(a[30]), "r"(a[31])
+                        : "memory");
                 }
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                 smem_addr(&sm.aempty[sa]))
-                             : "memory");
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                 smem_addr(&sm.lempty[s]))
-                             : "memory");
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote(&sm.ready[sa], 0);
+                t_work += clock64() - tw0;
             }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             smem_addr(&sm.accum))
-                         : "memory");
         }
+        if (warp == 2 && lane == 0)
+            if (unsigned long long* trc = g_mmq_trace) {
+                trc[blockIdx.x * 16 + 1] = tw_full;
+                trc[blockIdx.x * 16 + 11] = tw_aempty;
+                trc[blockIdx.x * 16 + 2] = t_work;
+            }
     } else {
-        // ---- expanders: 2 threads per row r (TMEM lane quarter of the warp), half h of the chunk ----
-        const int quarter = warp & 3;
-        const int h = (warp - 2) >> 2;  // warps 2-5: h = 0, warps 6-9: h = 1
-        const int r = quarter * 32 + lane;
-        const int64_t grow = (int64_t)rt * kMmqBM + r;
-        for (int kc = kc0; kc < kc1; ++kc) {
-            const int s = (kc - kc0) % NL, sa = (kc - kc0) % NA;
-            // the A slot is free once the MMA that read it committed; codes/scales landed
-            mbar_wait_(&sm.aempty[sa], ((unsigned)((kc - kc0) / NA) & 1u) ^ 1u);
-            mbar_wait_(&sm.full[s], (unsigned)((kc - kc0) / NL) & 1u);
-            const uint16_t dh = sm.scl[s][r];
-            const int z = zps ? (int)sm.zp[s][r] : 0;
-            const __half d = __ushort_as_half(dh);
-            const __half ndz = __hmul(d, __int2half_rn(-1 - z));  // exact: -(1 + z) in {0,-1,-2}
-            const uint32_t d2 = (uint32_t)dh | ((uint32_t)dh << 16);
-            const uint32_t ndz2 = (uint32_t)__half_as_ushort(ndz) * 0x10001u;
-            const uint2 w2 = reinterpret_cast<const uint2*>(sm.codes[s])[r * 2 + h];
-            const uint32_t wv[2] = {w2.x, w2.y};
-            uint8_t* atile = sm.a[sa];
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {  // 16-byte chunk j = 4h + jj: k in [8j, 8j+8)
-                const int j = 4 * h + jj;
-                const uint32_t w = wv[jj >> 1];
-                uint32_t out[4];
-#pragma unroll
-                for (int p = 0; p < 4; ++p) {
-                    const int m = 4 * (jj & 1) + p;  // pair (k, k+1) = (16*(j/2) + 2m, +1)
-                    const uint32_t v = ((w >> (2 * m)) & 0x00030003u) | 0x64006400u;  // f16x2 1024 + c
-                    __half2 hv = __hsub2(*reinterpret_cast<const __half2*>(&v), __floats2half2_rn(1024.f, 1024.f));
-                    // d * c - d * (1 + z) = d * t: the exact result is an f16, so the FMA returns it
-                    hv = __hfma2(hv, *reinterpret_cast<const __half2*>(&d2), *reinterpret_cast<const __half2*>(&ndz2));
-                    out[p] = *reinterpret_cast<uint32_t*>(&hv);
-                }
-                *reinterpret_cast<uint4*>(atile + sw128_off(r, j)) = make_uint4(out[0], out[1], out[2], out[3]);
+        // ---- epilogue: TMEM lane r = output row; 256 tokens in two 128-token halves: registers -> staging
+        // row -> one bulk store per half (plain stores for ragged or strided outputs)
+        const int q = warp & 3, r = 32 * q + lane;
+        const uint32_t td_row = tmem + ((uint32_t)(32 * q) << 16);
+        const bool bulk_ok = stride_m == 1 && ((stride_r * (int64_t)sizeof(TY)) & 15) == 0 &&
+                             (reinterpret_cast<uintptr_t>(y) & 15) == 0;
+        uint32_t t = 0;
+        long long tw_dfull = 0;
+        const long long te0 = clock64();
+        for (int it = cluster; it < items; it += nclusters, ++t) {
+            int tr, tn, s0, s1;
+            wk.decode(it, tr, tn, s0, s1);
+            {
+                MMQ_T0();
+                mbar_wait_(&sm.dfull, t & 1u);
+                MMQ_ACC(5, tw_dfull);
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
-            mbar_arrive_(&sm.aready[sa]);
-        }
-        // ---- epilogue: TMEM lane r, this warp's half of the token columns ----
-        mbar_wait_(&sm.accum, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        constexpr int HALF = BN / 2;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int64_t grow = (int64_t)tr * 256 + rank * kMmqBM + r;
+            TY* yt = y + (int64_t)(it / (wk.tiles_r * wk.tiles_n)) * slab;
+            const bool live = grow < rows;
+            const uint32_t sa = smem_addr(sm.stage[r]);
 #pragma unroll 1
-        for (int c0 = h * HALF; c0 < (h + 1) * HALF; c0 += 32) {
-            uint32_t v[32];
-            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0;
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                  "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                  "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                  "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (grow < rows) {
+            for (int h = 0; h < 2; ++h) {
+                const int64_t m0 = (int64_t)tn * 256 + 128 * h;
+                const bool bulk = live && bulk_ok && m0 + 128 <= M;
+                // the previous bulk store has finished reading the staging row
+                if (bulk) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int64_t m = (int64_t)nt * BN + c0 + i;
-                    if (m < M) y[grow * stride_r + m * stride_m] = (TY)__uint_as_float(v[i]);
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t v[32];
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+                          "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+                          "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                        : "r"(td_row + 128u * h + 32u * c));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (h == 1 && c == 3) {  // accumulator free for the next tile
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_remote(&sm.dempty, 0);
+                    }
+                    if (bulk) {
+                        if constexpr (sizeof(TY) == 4) {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4)
+                                sts128(sa + 4u * (32 * c + j), make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 8) {
+                                uint32_t p[4];
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    __nv_bfloat162 hh = __floats2bfloat162_rn(__uint_as_float(v[j + 2 * e]),
+                                                                              __uint_as_float(v[j + 2 * e + 1]));
+                                    p[e] = *reinterpret_cast<uint32_t*>(&hh);
+                                }
+                                sts128(sa + 2u * (32 * c + j), make_uint4(p[0], p[1], p[2], p[3]));
+                            }
+                        }
+                    } else if (live) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const int64_t m = m0 + 32 * c + j;
+                            if (m < M) yt[grow * stride_r + m * stride_m] = (TY)__uint_as_float(v[j]);
+                        }
+                    }
+                }
+                if (bulk) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                                     yt + grow * stride_r + m0),
+                                 "r"(sa), "r"((uint32_t)(128 * sizeof(TY)))
+                                 : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
             }
         }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        if (warp == kMmqEpiWarp && lane == 0)
+            if (unsigned long long* trc = g_mmq_trace) {
+                trc[blockIdx.x * 16 + 5] = tw_dfull;
+                trc[blockIdx.x * 16 + 6] = clock64() - te0 - tw_dfull;
+            }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
+    cluster_sync_all();
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
     }
 }
 
 // ------------------------------------------------------------------------------------------
-// Repack: container payload (block_n 256, variant s, cols % 256 == 0) -> MMQ layout
-//   codes  [NC = cols/64][rows_pad][4 x u32]  (word w of a row's 64-chunk holds k = 16w..16w+15:
-//          bits 2m..2m+1 = code of k = 16w + 2m, bits 16+2m.. = k = 16w + 2m + 1)
-//   scales [NB][rows_pad] f16,  zps [NB][rows_pad] int8 (asymmetric only)
+// Repack: container payload (block_n 256, variant s, cols % 256 == 0) -> MMQ weight records
+//   [rows_pad / 128 row tiles][cols / 128 stages][kWRec]: codes [half j][row][4 x u32] (word w of a
+//   row's 64-k half holds k = 16w..16w+15: bits 2m..2m+1 = code of k = 16w + 2m, bits 16+2m.. =
+//   k = 16w + 2m + 1) | f16 scales [row] of the stage's 256-block | int8 zero-points [row].
 // ------------------------------------------------------------------------------------------
-__global__ void repack_mmq_kernel(const uint8_t* __restrict__ payload, int64_t rows, int rows_pad, int NB, int asym,
+__global__ void repack_mmq_kernel(const uint8_t* __restrict__ payload, int64_t rows, int64_t rows_pad, int NB, int asym,
                                   uint8_t* __restrict__ out) {
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (row, 64-chunk)
-    const int NC = NB * 4;
-    if (idx >= (int64_t)rows_pad * NC) return;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (row, 64-chunk kc)
+    const int NC = NB * 4, NS = NB * 2;
+    if (idx >= rows_pad * NC) return;
     const int64_t row = idx / NC;
     const int kc = (int)(idx % NC);
-    uint32_t* codes = reinterpret_cast<uint32_t*>(out);
-    uint16_t* scales = reinterpret_cast<uint16_t*>(out + (int64_t)NC * rows_pad * 16);
-    int8_t* zps = reinterpret_cast<int8_t*>(out + (int64_t)NC * rows_pad * 16 + (int64_t)NB * rows_pad * 2);
+    const int st = kc >> 1, j = kc & 1, b = kc >> 2;
+    uint8_t* rec = out + ((row >> 7) * NS + st) * (int64_t)kWRec;
+    const int r = (int)(row & 127);
     uint32_t w[4] = {0, 0, 0, 0};
-    const int b = kc >> 2;
+    uint16_t sb = 0;
+    int8_t z = 0;
     if (row < rows) {
         const uint8_t* blk = payload + (row * NB + b) * 100;
         const int kbase = (kc & 3) * 64;
@@ -277,60 +497,90 @@ __global__ void repack_mmq_kernel(const uint8_t* __restrict__ payload, int64_t r
             const int bit = (wk & 1) ? 16 + 2 * (wk >> 1) : 2 * (wk >> 1);
             w[wi] |= c << bit;
         }
-        if ((kc & 3) == 0) {
-            scales[(int64_t)b * rows_pad + row] = *reinterpret_cast<const uint16_t*>(blk + 96);
-            if (asym) zps[(int64_t)b * rows_pad + row] = (int8_t)(int)f16_bits_to_f64(*reinterpret_cast<const uint16_t*>(blk + 98));
-        }
-    } else if ((kc & 3) == 0) {
-        scales[(int64_t)b * rows_pad + row] = 0;
-        if (asym) zps[(int64_t)b * rows_pad + row] = 0;
+        sb = *reinterpret_cast<const uint16_t*>(blk + 96);
+        if (asym) z = (int8_t)(int)f16_bits_to_f64(*reinterpret_cast<const uint16_t*>(blk + 98));
     }
-    reinterpret_cast<uint4*>(codes)[(int64_t)kc * rows_pad + row] = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4*>(rec + 2048 * j + 16 * r) = make_uint4(w[0], w[1], w[2], w[3]);
+    if (j == 0) {
+        *reinterpret_cast<uint16_t*>(rec + 4096 + 2 * r) = sb;
+        reinterpret_cast<int8_t*>(rec + 4352)[r] = z;
+    }
 }
 
 // ------------------------------------------------------------------------------------------
 // Activation rotation for MMQ: x'' = (H_256 x_b) / 16 in f16, written pre-swizzled as
-// [token tile][64-chunk][BN rows x 128 B] (SW128 K-major canonical layout); padding = 0.
-// One warp per (256-block, token); butterfly in fp32.
+// [256-token tile][CTA half h][64-k chunk kc][128 token rows x 128 B] (SW128 K-major canonical
+// layout), so each CTA's B half of a 128-k stage is ONE contiguous 32 KB copy; padding = 0.
+// One CTA per (256-block, 32 tokens): coalesced loads along whichever of k / token is contiguous
+// into a padded smem tile, one warp per 4 tokens for the butterfly (fp32: shuffles for the lane
+// bits, registers for the rest), then 16-byte stores of 8 consecutive k of one token.
 // ------------------------------------------------------------------------------------------
 template <typename TX>
-__global__ void rotate_act_f16_kernel(const TX* __restrict__ x, int64_t NB, int64_t M, int64_t M_pad,
-                                      int64_t stride_k, int64_t stride_m, int BN, uint8_t* __restrict__ out) {
-    const int lane = threadIdx.x & 31;
-    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (wid >= NB * M_pad) return;
-    const int64_t b = wid % NB, m = wid / NB;
-    float v[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = m < M ? (float)x[(b * 256 + lane + 32 * e) * stride_k + m * stride_m] : 0.f;
-#pragma unroll
-    for (int h = 1; h < 32; h <<= 1) {
-        const bool high = (lane & h) != 0;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const float p = __shfl_xor_sync(FULL, v[e], h);
-            v[e] = high ? p - v[e] : v[e] + p;
+__global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restrict__ x, int64_t M, int64_t stride_k,
+                                                             int64_t stride_m, int64_t NC, uint8_t* __restrict__ out) {
+    __shared__ float tile[32][257];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t b = blockIdx.x, m0 = (int64_t)blockIdx.y * 32;
+    const TX* xb = x + b * 256 * stride_k;
+    if (stride_k == 1 && stride_m != 1) {  // token-major input: threads along k
+#pragma unroll 4
+        for (int j = 0; j < 32; ++j) {
+            const int64_t m = m0 + j;
+            tile[j][tid] = m < M ? (float)xb[tid + m * stride_m] : 0.f;
+        }
+    } else {  // k-major input: lanes along tokens
+#pragma unroll 4
+        for (int i = 0; i < 32; ++i) {
+            const int k = warp + 8 * i;
+            const int64_t m = m0 + lane;
+            tile[lane][k] = m < M ? (float)xb[k * stride_k + m * stride_m] : 0.f;
         }
     }
+    __syncthreads();
+#pragma unroll 1
+    for (int jj = 0; jj < 4; ++jj) {
+        const int j = 4 * warp + jj;
+        float v[8];
 #pragma unroll
-    for (int hh = 1; hh < 8; hh <<= 1)
+        for (int e = 0; e < 8; ++e) v[e] = tile[j][lane + 32 * e];
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-            if ((e & hh) == 0) {
-                const float lo = v[e], hi = v[e + hh];
-                v[e] = lo + hi;
-                v[e + hh] = lo - hi;
+        for (int h = 1; h < 32; h <<= 1) {
+            const bool high = (lane & h) != 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const float p = __shfl_xor_sync(FULL, v[e], h);
+                v[e] = high ? p - v[e] : v[e] + p;
             }
-    const int64_t NC = NB * 4;
-    const int64_t tile = m / BN;
-    const int r = (int)(m % BN);
+        }
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-        const int k = 256 * (int)b + lane + 32 * e;  // global k
+        for (int hh = 1; hh < 8; hh <<= 1)
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if ((e & hh) == 0) {
+                    const float lo = v[e], hi = v[e + hh];
+                    v[e] = lo + hi;
+                    v[e + hh] = lo - hi;
+                }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) tile[j][lane + 32 * e] = v[e] * 0.0625f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int idx = tid + 256 * i, j = idx >> 5, c8 = idx & 31;  // token j, k = 8 c8 .. 8 c8 + 7
+        uint32_t p[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const __half2 h = __floats2half2_rn(tile[j][8 * c8 + 2 * e], tile[j][8 * c8 + 2 * e + 1]);
+            p[e] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        const int64_t m = m0 + j;
+        const int64_t k = b * 256 + 8 * c8;
         const int64_t kc = k >> 6;
-        const int kk = k & 63;
-        uint8_t* t = out + ((tile * NC + kc) * BN) * 128;
-        *reinterpret_cast<__half*>(t + sw128_off(r, kk >> 3) + (kk & 7) * 2) = __float2half_rn(v[e] * 0.0625f);
+        const int kk = (int)(k & 63);
+        const int64_t half = (m >> 7);  // = 2 * tile + h
+        uint8_t* t = out + (half * NC + kc) * 16384;
+        *reinterpret_cast<uint4*>(t + sw128_off((int)(m & 127), kk >> 3)) = make_uint4(p[0], p[1], p[2], p[3]);
     }
 }
 
@@ -349,11 +599,11 @@ __global__ void mmq_splitk_reduce(const float* __restrict__ ws, int ks, int64_t 
 
 using namespace itq3;
 
-static int mmq_rows_pad(int64_t rows) { return (int)((rows + kMmqBM - 1) / kMmqBM * kMmqBM); }
+static int mmq_rows_pad(int64_t rows) { return (int)((rows + 255) / 256 * 256); }  // whole CTA-pair tiles
 
 extern "C" int64_t itq3_mmq_nbytes(int64_t rows, int64_t cols, int asymmetric) {
-    const int64_t rp = mmq_rows_pad(rows), NB = cols / 256;
-    return NB * 4 * rp * 16 + NB * rp * 2 + (asymmetric ? NB * rp : 0);
+    (void)asymmetric;  // the zero-point bytes are part of every record
+    return (int64_t)(mmq_rows_pad(rows) / 128) * (cols / kStK) * kWRec;
 }
 
 extern "C" int itq3_repack_mmq(const uint8_t* payload, int64_t rows, int64_t cols, int asymmetric, uint8_t* out,
@@ -362,15 +612,15 @@ extern "C" int itq3_repack_mmq(const uint8_t* payload, int64_t rows, int64_t col
         set_error("itq3_repack_mmq: needs cols %% 256 == 0 (got %lld x %lld)", (long long)rows, (long long)cols);
         return ITQ3_E_UNSUPPORTED;
     }
-    const int rp = mmq_rows_pad(rows);
+    const int64_t rp = mmq_rows_pad(rows);
     const int NB = (int)(cols / 256);
-    const int64_t n = (int64_t)rp * NB * 4;
+    const int64_t n = rp * NB * 4;
     repack_mmq_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(payload, rows, rp, NB, asymmetric,
                                                                                      out);
     return check_launch("itq3_repack_mmq");
 }
 
-extern "C" int itq3_mmq_block_n(int64_t m) { return m <= 64 ? 64 : (m <= 128 ? 128 : 256); }
+extern "C" int itq3_mmq_block_n(int64_t m) { return (void)m, 256; }  // tokens per CTA-pair tile
 
 extern "C" int64_t itq3_mmq_act_nbytes(int64_t cols, int64_t m) {
     const int BN = itq3_mmq_block_n(m);
@@ -386,24 +636,21 @@ extern "C" int itq3_rotate_act_f16(const void* x, int x_dtype, int64_t cols, int
     }
     const int BN = itq3_mmq_block_n(m);
     const int64_t NB = cols / 256, M_pad = (m + BN - 1) / BN * BN;
-    const int64_t threads = NB * M_pad * 32;
-    const unsigned grid = (unsigned)((threads + 255) / 256);
+    const dim3 grid((unsigned)NB, (unsigned)(M_pad / 32));
     cudaStream_t s = (cudaStream_t)stream;
     switch (x_dtype) {
         case ITQ3_F32:
-            rotate_act_f16_kernel<float><<<grid, 256, 0, s>>>((const float*)x, NB, m, M_pad, stride_k, stride_m, BN, out);
+            rotate_act_f16_kernel<float><<<grid, 256, 0, s>>>((const float*)x, m, stride_k, stride_m, NB * 4, out);
             break;
         case ITQ3_F64:
-            rotate_act_f16_kernel<double><<<grid, 256, 0, s>>>((const double*)x, NB, m, M_pad, stride_k, stride_m, BN,
-                                                               out);
+            rotate_act_f16_kernel<double><<<grid, 256, 0, s>>>((const double*)x, m, stride_k, stride_m, NB * 4, out);
             break;
         case ITQ3_BF16:
-            rotate_act_f16_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, NB, m, M_pad, stride_k,
-                                                                      stride_m, BN, out);
+            rotate_act_f16_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, m, stride_k, stride_m,
+                                                                      NB * 4, out);
             break;
         case ITQ3_F16:
-            rotate_act_f16_kernel<__half><<<grid, 256, 0, s>>>((const __half*)x, NB, m, M_pad, stride_k, stride_m, BN,
-                                                               out);
+            rotate_act_f16_kernel<__half><<<grid, 256, 0, s>>>((const __half*)x, m, stride_k, stride_m, NB * 4, out);
             break;
         default:
             set_error("itq3_rotate_act_f16: unsupported dtype %d", x_dtype);
@@ -412,55 +659,84 @@ extern "C" int itq3_rotate_act_f16(const void* x, int x_dtype, int64_t cols, int
     return check_launch("itq3_rotate_act_f16");
 }
 
+static int mmq_max_clusters() {
+    // co-resident CTA pairs of the persistent kernel (74 on a full B200)
+    static int n = 0;
+    if (n == 0) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(2, 1, 1);
+        cfg.blockDim = dim3(kMmqThreads, 1, 1);
+        cfg.dynamicSmemBytes = sizeof(PairSmem) + 1024;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int c = 0;
+        if (cudaOccupancyMaxActiveClusters(&c, mmq_pair_kernel<float>, &cfg) != cudaSuccess || c < 1) {
+            cudaGetLastError();
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+            c = sms / 2;
+        }
+        n = c;
+    }
+    return n;
+}
+
 static int mmq_splits(int64_t rows, int64_t cols, int64_t m) {
-    // split K only when the output tiles fill less than half of the 148 SMs (one wave), so the
-    // fp32 partial traffic never costs more than the idle SMs it recovers; >= 8 K-chunks per split
-    const int64_t tiles = (int64_t)(mmq_rows_pad(rows) / kMmqBM) * ((m + itq3_mmq_block_n(m) - 1) / itq3_mmq_block_n(m));
-    if (tiles > 74) return 1;
-    const int64_t NC = cols / 64;
-    int64_t ks = 148 / tiles;
-    ks = ks < NC / 8 ? ks : NC / 8;
+    // split K only when the output tiles leave more than half of the CTA pairs idle, so the fp32
+    // partial traffic never costs more than the idle SMs it recovers; >= 4 stages (512 k) per split
+    const int64_t tiles = (int64_t)(mmq_rows_pad(rows) / 256) * ((m + 255) / 256);
+    const int64_t pairs = mmq_max_clusters();
+    if (tiles * 2 > pairs) return 1;
+    const int64_t NS = cols / kStK;
+    int64_t ks = pairs / tiles;
+    ks = ks < NS / 4 ? ks : NS / 4;
     return (int)(ks < 1 ? 1 : ks);
 }
 
-template <int BN, typename TY>
+template <typename TY>
 static int launch_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym, const uint8_t* act, int64_t m, TY* y,
                       int64_t sr, int64_t sm_, float* ws, cudaStream_t s) {
-    constexpr int NL = BN == 256 ? 4 : (BN == 128 ? 8 : 12);  // load slots: ~150 KB of bulk copies in flight
-    constexpr int NA = BN == 256 ? 2 : 3;
-    const int smem = (int)sizeof(MmqSmem<BN, NL, NA>) + 1024;
-    static bool attr = false;
+    const int smem = (int)sizeof(PairSmem) + 1024;
+    static bool attr = false, attr32 = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(mmq_kernel<BN, NL, NA, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-            cudaSuccess)
+        if (cudaFuncSetAttribute(mmq_pair_kernel<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
             return check_launch("itq3_mmq: smem attribute");
         attr = true;
     }
-    const int rp = mmq_rows_pad(rows);
-    const int NB = (int)(cols / 256), NC = NB * 4;
-    const uint8_t* codes = mmq;
-    const uint16_t* scales = reinterpret_cast<const uint16_t*>(mmq + (int64_t)NC * rp * 16);
-    const int8_t* zps = asym ? reinterpret_cast<const int8_t*>(mmq + (int64_t)NC * rp * 16 + (int64_t)NB * rp * 2) : nullptr;
-    const int ks = ws ? mmq_splits(rows, cols, m) : 1;
-    const dim3 grid((unsigned)(rp / kMmqBM), (unsigned)((m + BN - 1) / BN), (unsigned)ks);
-    if (ks == 1) {
-        mmq_kernel<BN, NL, NA, TY><<<grid, kMmqThreads, smem, s>>>(codes, scales, zps, rp, NC, act, rows, m, y, sr, sm_, 0);
-        return check_launch("itq3_mmq");
-    }
-    static bool attr32 = false;
     if (!attr32) {
-        if (cudaFuncSetAttribute(mmq_kernel<BN, NL, NA, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        if (cudaFuncSetAttribute(mmq_pair_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
             cudaSuccess)
             return check_launch("itq3_mmq: smem attribute");
         attr32 = true;
     }
-    mmq_kernel<BN, NL, NA, float><<<grid, kMmqThreads, smem, s>>>(codes, scales, zps, rp, NC, act, rows, m, ws, m, 1,
-                                                                  rows * m);
+    PairWork wk;
+    wk.tiles_r = mmq_rows_pad(rows) / 256;
+    wk.tiles_n = (int)((m + 255) / 256);
+    wk.ks = ws ? mmq_splits(rows, cols, m) : 1;
+    wk.NS = (int)(cols / kStK);
+    const int64_t items = (int64_t)wk.tiles_r * wk.tiles_n * wk.ks;
+    const int64_t clusters = items < mmq_max_clusters() ? items : mmq_max_clusters();
+    const dim3 grid((unsigned)(2 * clusters));
+    if (wk.ks == 1) {
+        mmq_pair_kernel<TY><<<grid, kMmqThreads, smem, s>>>(mmq, asym, wk, act, rows, m, y, sr, sm_, 0);
+        return check_launch("itq3_mmq");
+    }
+    mmq_pair_kernel<float><<<grid, kMmqThreads, smem, s>>>(mmq, asym, wk, act, rows, m, ws, m, 1, rows * m);
     int rc = check_launch("itq3_mmq (split-K)");
     if (rc) return rc;
     const int64_t n = rows * m;
-    mmq_splitk_reduce<TY><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ws, ks, rows, m, y, sr, sm_);
+    mmq_splitk_reduce<TY><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ws, wk.ks, rows, m, y, sr, sm_);
     return check_launch("itq3_mmq (split-K reduce)");
+}
+
+extern "C" int itq3_mmq_set_trace(void* buf) {
+    unsigned long long* p = (unsigned long long*)buf;
+    return cudaMemcpyToSymbol(g_mmq_trace, &p, sizeof(p)) == cudaSuccess ? 0 : check_launch("itq3_mmq_set_trace");
 }
 
 extern "C" int64_t itq3_mmq_ws_nbytes(int64_t rows, int64_t cols, int64_t m) {
@@ -475,19 +751,10 @@ extern "C" int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym
         return ITQ3_E_SHAPE;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    const int BN = itq3_mmq_block_n(m);
     float* ws = (float*)workspace;
-    if (y_dtype == ITQ3_F32) {
-        if (BN == 64) return launch_mmq<64>(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, ws, s);
-        if (BN == 128) return launch_mmq<128>(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, ws, s);
-        return launch_mmq<256>(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, ws, s);
-    }
-    if (y_dtype == ITQ3_BF16) {
-        if (BN == 64) return launch_mmq<64>(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s);
-        if (BN == 128)
-            return launch_mmq<128>(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s);
-        return launch_mmq<256>(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s);
-    }
+    if (y_dtype == ITQ3_F32) return launch_mmq(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, ws, s);
+    if (y_dtype == ITQ3_BF16)
+        return launch_mmq(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s);
     set_error("itq3_mmq: output dtype must be float32 or bfloat16");
     return ITQ3_E_DOMAIN;
 }

@@ -70,3 +70,27 @@ def test_mmq_dtypes_and_strides():
     # token-major activations (M x K transposed view) -> identical result
     Y2 = P.fused_matmul(q, X.t().contiguous().t())
     torch.testing.assert_close(Y, Y2, rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("rows,cols,m", [(8192, 1024, 640), (4352, 512, 257), (2304, 768, 1030)])
+def test_mmq_persistent_pairs(rows, cols, m):
+    """More (256-row x 128-token) pair tiles than co-resident CTA pairs: every pair walks several
+    tiles and alternates its two TMEM accumulators; ragged token tails take the plain-store path
+    (m = 257: rows not 16-byte aligned, so no bulk row stores at all)."""
+    rng = np.random.default_rng(rows + m)
+    w = rng.standard_normal((rows, cols)) * 0.05
+    q = P.quantize_tensor(torch.from_numpy(w.astype(np.float32)).cuda())
+    X = rng.standard_normal((cols, m)).astype(np.float32)
+    Y = P.fused_matmul(q, torch.from_numpy(X).cuda()).cpu().numpy().astype(np.float64)
+    exact, bound = mmq_bound(q.payload().cpu().numpy(), rows, cols, X)
+    assert np.all(np.abs(Y - exact) <= bound), np.max(np.abs(Y - exact) / bound)
+
+
+def test_mmq_bf16_output_matches_fp32():
+    rng = np.random.default_rng(9)
+    q = P.quantize_tensor(torch.from_numpy((rng.standard_normal((1536, 1024)) * 0.05).astype(np.float32)).cuda())
+    X = torch.from_numpy(rng.standard_normal((1024, 384)).astype(np.float32)).cuda()
+    y32 = P.compute._matmul_device(q, X, torch.float32, P.compute.perf_limbs(384))
+    y16 = P.compute._matmul_device(q, X, torch.bfloat16, P.compute.perf_limbs(384))
+    assert y16.dtype == torch.bfloat16
+    torch.testing.assert_close(y16, y32.to(torch.bfloat16), rtol=0, atol=0)
