@@ -35,11 +35,9 @@
 namespace itq3 {
 
 constexpr int kMmqBM = 128;
-constexpr int kMmqBK = 64;  // one 128-byte swizzle atom of f16 per row
 constexpr int kMmqExpGroups = 2;  // expander warp quads; group e decodes the chunks g with g % 2 == e
 constexpr int kMmqEpiWarp = 2 + 4 * kMmqExpGroups;
 constexpr int kMmqThreads = 32 * (kMmqEpiWarp + 4);  // producer, MMA, expander quads, 4 epilogue warps
-constexpr int kMmqCodeChunk = kMmqBM * 16;  // 2 KB: 128 rows x 64 codes x 2 bits
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -515,10 +513,33 @@ __global__ void repack_mmq_kernel(const uint8_t* __restrict__ payload, int64_t r
 // into a padded smem tile, one warp per 4 tokens for the butterfly (fp32: shuffles for the lane
 // bits, registers for the rest), then 16-byte stores of 8 consecutive k of one token.
 // ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void load4(const float* p, float (&f)[4]) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    f[0] = v.x, f[1] = v.y, f[2] = v.z, f[3] = v.w;
+}
+__device__ __forceinline__ void load4(const double* p, float (&f)[4]) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    f[0] = (float)a.x, f[1] = (float)a.y, f[2] = (float)b.x, f[3] = (float)b.y;
+}
+__device__ __forceinline__ void load4(const __half* p, float (&f)[4]) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&v.x)), b = __half22float2(*reinterpret_cast<const __half2*>(&v.y));
+    f[0] = a.x, f[1] = a.y, f[2] = b.x, f[3] = b.y;
+}
+__device__ __forceinline__ void load4(const __nv_bfloat16* p, float (&f)[4]) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x)),
+                 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
+    f[0] = a.x, f[1] = a.y, f[2] = b.x, f[3] = b.y;
+}
+
 template <typename TX>
 __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restrict__ x, int64_t M, int64_t stride_k,
                                                              int64_t stride_m, int64_t NC, uint8_t* __restrict__ out) {
-    __shared__ float tile[32][257];
+    // fp32 inputs, token-major (257: conflict-free transposes); after the butterflies the same bytes hold
+    // the rotated f16 outputs as [32][264] (528-byte rows: 16-byte aligned, 4 wavefronts per 16-B warp load)
+    __shared__ __align__(16) float tile[32][257];
+    __half(&th)[32][264] = *reinterpret_cast<__half(*)[32][264]>(&tile[0][0]);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t b = blockIdx.x, m0 = (int64_t)blockIdx.y * 32;
     const TX* xb = x + b * 256 * stride_k;
@@ -528,6 +549,17 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
             const int64_t m = m0 + j;
             tile[j][tid] = m < M ? (float)xb[tid + m * stride_m] : 0.f;
         }
+    } else if (stride_m == 1 && (stride_k & 3) == 0 && m0 + 32 <= M &&
+               (reinterpret_cast<uintptr_t>(x) & (4 * sizeof(TX) - 1)) == 0) {
+        // k-major, 4-token vectors: thread (k_lo = tid / 8, tokens 4 (tid % 8) ..) loads 8 vectors in flight
+        const int kl = tid >> 3, mq = tid & 7;
+        float f[8][4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) load4(xb + (int64_t)(kl + 32 * i) * stride_k + m0 + 4 * mq, f[i]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) tile[4 * mq + e][kl + 32 * i] = f[i][e];  // conflict-free: 257 = 1 mod 32
     } else {  // k-major input: lanes along tokens
 #pragma unroll 4
         for (int i = 0; i < 32; ++i) {
@@ -537,19 +569,21 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
         }
     }
     __syncthreads();
-#pragma unroll 1
-    for (int jj = 0; jj < 4; ++jj) {
-        const int j = 4 * warp + jj;
-        float v[8];
+    float v[4][8];  // the warp's 4 tokens: lane holds k = lane + 32 e
 #pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] = tile[j][lane + 32 * e];
+    for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[jj][e] = tile[4 * warp + jj][lane + 32 * e];
+    __syncthreads();  // the f16 outputs overwrite the fp32 tile
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
 #pragma unroll
         for (int h = 1; h < 32; h <<= 1) {
             const bool high = (lane & h) != 0;
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                const float p = __shfl_xor_sync(FULL, v[e], h);
-                v[e] = high ? p - v[e] : v[e] + p;
+                const float p = __shfl_xor_sync(FULL, v[jj][e], h);
+                v[jj][e] = high ? p - v[jj][e] : v[jj][e] + p;
             }
         }
 #pragma unroll
@@ -557,23 +591,19 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
 #pragma unroll
             for (int e = 0; e < 8; ++e)
                 if ((e & hh) == 0) {
-                    const float lo = v[e], hi = v[e + hh];
-                    v[e] = lo + hi;
-                    v[e + hh] = lo - hi;
+                    const float lo = v[jj][e], hi = v[jj][e + hh];
+                    v[jj][e] = lo + hi;
+                    v[jj][e + hh] = lo - hi;
                 }
 #pragma unroll
-        for (int e = 0; e < 8; ++e) tile[j][lane + 32 * e] = v[e] * 0.0625f;
+        for (int e = 0; e < 8; ++e) th[4 * warp + jj][lane + 32 * e] = __float2half_rn(v[jj][e] * 0.0625f);
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int idx = tid + 256 * i, j = idx >> 5, c8 = idx & 31;  // token j, k = 8 c8 .. 8 c8 + 7
-        uint32_t p[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const __half2 h = __floats2half2_rn(tile[j][8 * c8 + 2 * e], tile[j][8 * c8 + 2 * e + 1]);
-            p[e] = *reinterpret_cast<const uint32_t*>(&h);
-        }
+        const uint4 pv = *reinterpret_cast<const uint4*>(&th[j][8 * c8]);  // 528-byte rows: 4 wavefronts per warp
+        const uint32_t p[4] = {pv.x, pv.y, pv.z, pv.w};
         const int64_t m = m0 + j;
         const int64_t k = b * 256 + 8 * c8;
         const int64_t kc = k >> 6;

@@ -69,33 +69,48 @@ def main():
             copies.append((q.mmq_layout(), q.mmq8_layout()))
         for M in MS:
             X = torch.randn((K, M), generator=g, device=dev)
-            small = M_SMALL(M)
-            act = torch.empty(lib.itq3_mmq8_act_nbytes(K, M) if small else lib.itq3_mmq_act_nbytes(K, M),
-                              dtype=torch.uint8, device=dev)
-            Y = torch.empty((rows, M), dtype=torch.float32, device=dev)
-            wsn = lib.itq3_mmq8_ws_nbytes(rows, K, M) if small else lib.itq3_mmq_ws_nbytes(rows, K, M)
-            ws = torch.empty(max(wsn, 1), dtype=torch.uint8, device=dev)
+            kinds = (["i8"] if M_SMALL(M) else []) + (["f16"] if M >= 32 else [])
+            for kind in kinds:
+                small = kind == "i8"
+                act = torch.empty(lib.itq3_mmq8_act_nbytes(K, M) if small else lib.itq3_mmq_act_nbytes(K, M),
+                                  dtype=torch.uint8, device=dev)
+                Y = torch.empty((rows, M), dtype=torch.float32, device=dev)
+                wsn = lib.itq3_mmq8_ws_nbytes(rows, K, M) if small else lib.itq3_mmq_ws_nbytes(rows, K, M)
+                ws = torch.empty(max(wsn, 1), dtype=torch.uint8, device=dev)
 
-            def run(i):
-                s = _lib.stream_ptr(dev)
-                if small:  # K5b, kind::i8 (compute.py routes 16 <= M <= 64 here)
-                    _lib.call("itq3_rotate_act_i8", _lib.ptr(X), _lib.F32, K, M, X.stride(0), X.stride(1),
-                              _lib.ptr(act), s)
-                    _lib.call("itq3_mmq8", _lib.ptr(copies[i % len(copies)][1]), rows, K, _lib.ptr(act), M,
-                              _lib.ptr(Y), _lib.F32, Y.stride(0), Y.stride(1), _lib.ptr(ws) if wsn else None, s)
-                    return
-                _lib.call("itq3_rotate_act_f16", _lib.ptr(X), _lib.F32, K, M, X.stride(0), X.stride(1),
-                          _lib.ptr(act), s)
-                _lib.call("itq3_mmq", _lib.ptr(copies[i % len(copies)][0]), rows, K, 0, _lib.ptr(act), M, _lib.ptr(Y),
-                          _lib.F32, Y.stride(0), Y.stride(1), _lib.ptr(ws) if wsn else None, s)
+                def rot(i):
+                    s = _lib.stream_ptr(dev)
+                    if small:
+                        _lib.call("itq3_rotate_act_i8", _lib.ptr(X), _lib.F32, K, M, X.stride(0), X.stride(1),
+                                  _lib.ptr(act), s)
+                    else:
+                        _lib.call("itq3_rotate_act_f16", _lib.ptr(X), _lib.F32, K, M, X.stride(0), X.stride(1),
+                                  _lib.ptr(act), s)
 
-            ms = graph_time(run, args.reps)
-            tf = 2.0 * rows * K * M / (ms * 1e-3) / 1e12
-            wbytes = rows * K * 66 / 256
-            r = {"rows": rows, "K": K, "M": M, "kernel": "K5b kind::i8" if small else "K5 kind::f16", "us": ms * 1e3, "tflops": tf, "frac_of_bf16_peak": tf / peak,
-                 "weight_gbps": wbytes / (ms * 1e-3) / 1e9}
-            res.append(r)
-            print(json.dumps(r), flush=True)
+                def mm(i):
+                    s = _lib.stream_ptr(dev)
+                    if small:  # K5b, kind::i8
+                        _lib.call("itq3_mmq8", _lib.ptr(copies[i % len(copies)][1]), rows, K, _lib.ptr(act), M,
+                                  _lib.ptr(Y), _lib.F32, Y.stride(0), Y.stride(1), _lib.ptr(ws) if wsn else None, s)
+                    else:  # K5, kind::f16 CTA pairs
+                        _lib.call("itq3_mmq", _lib.ptr(copies[i % len(copies)][0]), rows, K, 0, _lib.ptr(act), M,
+                                  _lib.ptr(Y), _lib.F32, Y.stride(0), Y.stride(1), _lib.ptr(ws) if wsn else None, s)
+
+                def run(i):
+                    rot(i)
+                    mm(i)
+
+                ms = graph_time(run, args.reps)
+                ms_k = graph_time(mm, args.reps)
+                tf = 2.0 * rows * K * M / (ms * 1e-3) / 1e12
+                tf_k = 2.0 * rows * K * M / (ms_k * 1e-3) / 1e12
+                wbytes = rows * K * 66 / 256
+                r = {"rows": rows, "K": K, "M": M, "kernel": "K5b kind::i8" if small else "K5 kind::f16 pair",
+                     "us": ms * 1e3, "tflops": tf, "frac_of_bf16_peak": tf / peak, "kernel_us": ms_k * 1e3,
+                     "kernel_tflops": tf_k, "kernel_frac_of_bf16_peak": tf_k / peak,
+                     "weight_gbps": wbytes / (ms * 1e-3) / 1e9}
+                res.append(r)
+                print(json.dumps(r), flush=True)
     if args.out:
         json.dump({"peak_bf16_tflops": peak, "results": res}, open(args.out, "w"), indent=1)
 
