@@ -228,7 +228,17 @@ __device__ __forceinline__ float2 chain_tile(const uint8_t* ring, int warp, int 
     return make_float2(d0 * (fcx * v0 - zf0 * corr), d1 * (fcx * v1 - zf1 * corr));
 }
 
+constexpr int kSmemStages = 150;  // stage descriptors + this CTA's split cached in smem (global beyond)
+
+// Work split of stage st for CTA cta: K-chunk ch (CTAs c with c % nch == ch), and the row
+// tiles rt = rt0, rt0 + Gc, ... (Gc CTAs per chunk); active = 0 if the CTA is idle.
+struct StageSplit {
+    int nch, ch, rt0, Gc, active, pad[3];
+};
+
 struct ChainSmem {
+    ChainStage desc[kSmemStages];
+    StageSplit split[kSmemStages];
     uint8_t ring[kNumSlots][kSlotBytes];
     uint8_t rot[kChainConsumerWarps][kActSmemBlock];   // per-warp rotation scratch (own block only)
     float part[kNumSlots][kChainConsumerWarps][16];    // per-warp row partials of a unit
@@ -252,19 +262,28 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-// Work split of stage st for CTA cta: K-chunk ch (CTAs c with c % nch == ch), and the row
-// tiles rt = rt0, rt0 + Gc, ... (Gc CTAs per chunk).  Returns false if the CTA is idle.
-struct StageSplit {
-    int nch, ch, rt0, Gc;
-};
-__device__ __forceinline__ bool stage_split(const ChainStage& st, int cta, int G, int s, StageSplit& sp) {
+__device__ __forceinline__ bool compute_split(const ChainStage& st, int cta, int G, int s, StageSplit& sp) {
     sp.nch = (st.NB + kUnitBlocks - 1) / kUnitBlocks;
     sp.Gc = G / sp.nch;
     sp.ch = cta % sp.nch;
     const int idx = cta / sp.nch;
+    sp.active = 0;
     if (idx >= sp.Gc) return false;
     sp.rt0 = (idx + 7 * s) % sp.Gc;
-    return sp.rt0 < st.RT;
+    sp.active = sp.rt0 < st.RT;
+    return sp.active;
+}
+// Stage s's descriptor and this CTA's split: from the smem cache (filled at kernel start, so the
+// per-stage critical path has no dependent global loads or integer divisions) or computed.
+__device__ __forceinline__ bool stage_get(const ChainSmem& sm, const ChainStage* stages, int cta, int G, int s,
+                                          ChainStage& st, StageSplit& sp) {
+    if (s < kSmemStages) {
+        st = sm.desc[s];
+        sp = sm.split[s];
+        return sp.active;
+    }
+    st = stages[s];
+    return compute_split(st, cta, G, s, sp);
 }
 
 // trace (optional): per (cta, stage) globaltimer stamps
@@ -285,6 +304,11 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     const unsigned epoch = *reinterpret_cast<volatile unsigned*>(epoch_ptr) + 1u;
     if (threadIdx.x == 0) atomicAdd(epoch_ptr + 1, 1u);
 
+    for (int s = tid; s < min(S, kSmemStages); s += kChainThreads) {
+        const ChainStage st = stages[s];
+        sm.desc[s] = st;
+        compute_split(st, cta, G, s, sm.split[s]);
+    }
     if (tid == 0) {
         for (int i = 0; i < kNumSlots; ++i) {
             mbar_init(&sm.full[i], 1);
@@ -303,9 +327,9 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         // never wait on each other.
         int seq = 0;
         for (int s = 0; s < S; ++s) {
-            const ChainStage st = stages[s];
+            ChainStage st;
             StageSplit sp;
-            if (!stage_split(st, cta, G, s, sp)) continue;
+            if (!stage_get(sm, stages, cta, G, s, st, sp)) continue;
             const int n_units = (st.RT - 1 - sp.rt0) / sp.Gc + 1;
             unsigned long long* yout = st.y + (int64_t)sp.ch * st.rows;
             const unsigned long long tag = (unsigned long long)epoch << 32;
@@ -336,9 +360,9 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             int slot = 0;
             unsigned phase = 0;
             for (int s = 0; s < S; ++s) {
-                const ChainStage st = stages[s];
+                ChainStage st;
                 StageSplit sp;
-                if (!stage_split(st, cta, G, s, sp)) continue;
+                if (!stage_get(sm, stages, cta, G, s, st, sp)) continue;
                 const uint8_t* scales = st.tiled + (int64_t)st.RT * st.NB * 1024;
                 const uint8_t* zps = scales + (int64_t)st.RT * st.NB * 32;
                 const int b0 = sp.ch * kUnitBlocks;
@@ -371,11 +395,11 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     int seq = 0;  // CTA-wide unit sequence number (ring slot = seq % kNumSlots)
     uint8_t* rot = sm.rot[warp];
     const bool prof = trace != nullptr && cta == 0;
-    long long c_wait = 0, c_tile = 0, c_rot = 0, c_start = clock64();
+    long long c_wait = 0, c_tile = 0, c_rot = 0, c_in = 0, c_start = clock64();
     for (int s = 0; s < S; ++s) {
-        const ChainStage st = stages[s];
+        ChainStage st;
         StageSplit sp;
-        if (!stage_split(st, cta, G, s, sp)) continue;
+        if (!stage_get(sm, stages, cta, G, s, st, sp)) continue;
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 0] = globaltimer();
         const int b0 = sp.ch * kUnitBlocks;
         const int nb = min(kUnitBlocks, st.NB - b0);
@@ -390,11 +414,12 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 #pragma unroll
                 for (int e = 0; e < 8; ++e) f[e] = __ldg(xs + 256 * (b0 + warp) + lane + 32 * e);
             } else {
-                const ChainStage pv = stages[s - 1];
+                const ChainStage pv = s - 1 < kSmemStages ? sm.desc[s - 1] : stages[s - 1];
                 const int pn = (pv.NB + kUnitBlocks - 1) / kUnitBlocks;
                 load_tagged_block(pv.y + 256 * (b0 + warp), pn, pv.rows, epoch, lane, f);
             }
             if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 1] = globaltimer();
+            if (prof) c_in += clock64() - c0;
             chain_rotate_to_smem(f, L, rot, lane);
             __syncwarp();
             // fragments for lane (g, t): columns g < 4 hold limbs, columns >= 4 are zero
@@ -470,6 +495,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         pt[1] = c_tile;
         pt[2] = c_rot;
         pt[3] = clock64() - c_start;
+        pt[64 - 3 * warp] = c_in;  // per-warp input-wait cycles: trace word [.. + 64 + warp]
     }
     // fold the last stage's K-chunk partials into `out` (fixed order), waiting on the tags
     const ChainStage last = stages[S - 1];

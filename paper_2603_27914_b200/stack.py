@@ -75,7 +75,7 @@ class LinearStack:
         """Per-(CTA, stage) globaltimer stamps: entered, input ready, input rotated, last tile done."""
         sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
         S = len(self.qs)
-        self.trace = torch.zeros(sms * S * 4 + S * 16 * 4 + 16 * 4, dtype=torch.int64, device=self.dev)
+        self.trace = torch.zeros(sms * S * 4 + S * 16 * 4 + 16 * 8, dtype=torch.int64, device=self.dev)
         self.graph = None
         return self.trace
 

@@ -33,14 +33,18 @@ def main():
         st.forward(x)
     raw = tr.cpu().numpy().astype(np.float64)
     S = len(st.qs)
-    G = (raw.size - S * 64 - 64) // (S * 4)
+    G = (raw.size - S * 64 - 128) // (S * 4)
     t = raw[: G * S * 4].reshape(G, S, 4)
     wt = raw[G * S * 4: G * S * 4 + S * 64].reshape(S, 16, 4)
-    cyc = raw[G * S * 4 + S * 64:].reshape(16, 4)
+    cyc = raw[G * S * 4 + S * 64:G * S * 4 + S * 64 + 64].reshape(16, 4)
+    c_in = raw[G * S * 4 + S * 64 + 64:G * S * 4 + S * 64 + 80]
     tot = cyc[:, 3].mean()
     print("CTA0 compute-warp cycle split (mean over warps): wait_full %.1f%%  tiles %.1f%%  rotate+input %.1f%%  "
           "(total %.0f cycles)" % (100 * cyc[:, 0].mean() / tot, 100 * cyc[:, 1].mean() / tot,
                                    100 * cyc[:, 2].mean() / tot, tot))
+    print("  of which input wait+load %.1f%%, rotation proper %.1f%%; per stage: input %.0f, rotation %.0f cycles"
+          % (100 * c_in.mean() / tot, 100 * (cyc[:, 2].mean() - c_in.mean()) / tot, c_in.mean() / S,
+             (cyc[:, 2].mean() - c_in.mean()) / S))
     t0 = t[:, 0, 0].min()
     t = (t - t0) / 1000.0  # us
     wt = np.where(wt > 0, (wt - t0) / 1000.0, np.nan)
