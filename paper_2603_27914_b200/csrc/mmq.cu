@@ -17,8 +17,9 @@
 // MMA issuer and of the expanders, which share the SM sub-partitions' issue slots (N = 128 tiles ran
 // at ~55% of the tensor rate for that reason; tools/mmq_trace.py).
 // Warp roles (14 warps per CTA):
-//   warp 0     producer: the two bulk copies per stage into a 4-deep ring (full/lempty mbarriers;
-//              lempty is signalled by the pair's multicast tcgen05.commit);
+//   warp 0     producer: the two bulk copies per stage into a 4-deep ring (full/empty mbarriers;
+//              empty is signalled by ONE multicast tcgen05.commit per stage, which also frees the
+//              stage's A slot: each commit costs the tensor pipe ~100-170 cycles);
 //   warp 1     TMEM allocation (cta_group::2, all 512 columns: D = [0, 256), A ring = 4 x 64 columns);
 //              in the leader CTA lane 0 issues the 8 MMAs of a stage once both CTAs' expanders
 //              arrived on the leader's `ready` (relaxed remote mbarrier arrivals: no MEMBAR.GPU);
@@ -81,6 +82,13 @@ __device__ __forceinline__ uint32_t umma_idesc_f16() {
 // swizzled byte offset of (row r, 16-byte chunk j) inside a K-major SW128 tile
 __device__ __forceinline__ uint32_t sw128_off(int r, int j) {
     return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((j ^ (r & 7)) << 4));
+}
+
+// one lane of a converged warp (the MMA issuer): lets the descriptors stay in uniform registers
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n selp.b32 %0, 1, 0, P;\n}\n" : "=r"(pred));
+    return pred != 0;
 }
 
 // ---- cluster / pair helpers ----
@@ -152,17 +160,16 @@ __device__ unsigned long long* g_mmq_trace = nullptr;
 // a 128-k stage of f16 d*t, two k per 32-bit column).
 constexpr int kStK = 128;                       // k per stage
 constexpr int kWRec = 4096 + 256 + 128;         // weight record: codes [2 halves][128 rows][16 B] | f16 scales | int8 zps
-constexpr int kPairNL = 4;                      // load ring (bulk copies)
-constexpr int kPairNA = 4;                      // A ring in TMEM
+constexpr int kPairNS = 4;  // stages in flight: load slot s and A slot s are freed by ONE commit (a
+                             // tcgen05.commit costs the tensor pipe ~100-170 cycles; tc_f16_pair_probe)
 constexpr int kPairStage = 132;  // fp32 words per staged output row (128 + 4 pad: conflict-free v4 stores)
 struct PairSmem {
-    uint8_t b[kPairNL][128 * 2 * 128];  // B half tile: 2 x (128 token rows x 64 k f16, SW128 K-major), 1024-aligned
-    uint8_t w[kPairNL][kWRec];          // weight record of the stage (this CTA's 128 rows)
+    uint8_t b[kPairNS][128 * 2 * 128];  // B half tile: 2 x (128 token rows x 64 k f16, SW128 K-major), 1024-aligned
+    uint8_t w[kPairNS][kWRec];          // weight record of the stage (this CTA's 128 rows)
     float stage[kMmqBM][kPairStage];    // epilogue staging for the bulk row stores
-    uint64_t full[kPairNL];    // this CTA's weight record + B half landed (TMA)
-    uint64_t lempty[kPairNL];  // the pair's MMAs consumed load slot s (multicast commit, both CTAs)
-    uint64_t aempty[kPairNA];  // the pair's MMAs consumed A slot s (multicast commit, both CTAs)
-    uint64_t ready[kPairNA];   // leader only: A slot s expanded and its B landed in both CTAs (8 warp arrivals)
+    uint64_t full[kPairNS];    // this CTA's weight record + B half landed (TMA)
+    uint64_t empty[kPairNS];   // the pair's MMAs consumed stage slot s: smem slot + A slot (multicast commit)
+    uint64_t ready[kPairNS];   // leader only: A slot s expanded and its B landed in both CTAs (8 warp arrivals)
     uint64_t dfull;            // accumulator complete (multicast commit)
     uint64_t dempty;           // leader only: both CTAs' epilogues drained the accumulator (8 warp arrivals)
     uint32_t tmem_base;
@@ -195,12 +202,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
     constexpr uint32_t kColA = 256;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kPairNL; ++s) {
+        for (int s = 0; s < kPairNS; ++s) {
             mbar_init_(&sm.full[s], 1);
-            mbar_init_(&sm.lempty[s], 1);
-        }
-        for (int s = 0; s < kPairNA; ++s) {
-            mbar_init_(&sm.aempty[s], 1);
+            mbar_init_(&sm.empty[s], 1);
             mbar_init_(&sm.ready[s], 8);
         }
         mbar_init_(&sm.dfull, 1);
@@ -229,10 +233,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
                 const uint8_t* wsrc = wrec + ((int64_t)(2 * tr + rank) * wk.NS) * kWRec;
                 const uint8_t* bsrc = act + ((int64_t)(2 * tn + rank) * wk.NS) * (2 * 16384);
                 for (int st = s0; st < s1; ++st, ++g) {
-                    const int s = g % kPairNL;
+                    const int s = g % kPairNS;
                     {
                         MMQ_T0();
-                        mbar_wait_(&sm.lempty[s], ((g / kPairNL) & 1u) ^ 1u);
+                        mbar_wait_(&sm.empty[s], ((g / kPairNS) & 1u) ^ 1u);
                         MMQ_ACC(0, tw);
                     }
                     const long long ti0 = clock64();
@@ -250,7 +254,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (rank == 0 && lane == 0) {  // MMA issuer of the pair: M = 256 (128 rows per SM), N = 256, K = 16
+        if (rank == 0) {  // MMA issuer of the pair (the whole warp runs the loop, one elected lane issues):
+                          // M = 256 (128 rows per SM), N = 256, K = 16
             const uint32_t idesc = (1u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
             uint32_t g = 0, t = 0;
             long long tw_ready = 0, tw_d = 0;
@@ -266,29 +271,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t td = tmem;
                 for (int st = s0; st < s1; ++st, ++g) {
-                    const int s = g % kPairNL, sa = g % kPairNA;
+                    const int s = g % kPairNS, sa = s;
                     {
                         MMQ_T0();
-                        mbar_wait_(&sm.ready[sa], (g / kPairNA) & 1u);
+                        mbar_wait_(&sm.ready[sa], (g / kPairNS) & 1u);
                         MMQ_ACC(3, tw_ready);
                     }
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const uint32_t ta = tmem + kColA + 64u * sa, b0 = smem_addr(sm.b[s]);
+                    if (elect_one()) {
 #pragma unroll
-                    for (int k = 0; k < kStK / 16; ++k) {
-                        const uint64_t bd = umma_desc_sw128(b0 + (k >> 2) * 16384 + 32 * (k & 3));
-                        const uint32_t accum = (st != s0) || (k != 0);
-                        asm volatile(
-                            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                            " tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(td),
-                            "r"(ta + 8u * k), "l"(bd), "r"(idesc), "r"(accum));
+                        for (int k = 0; k < kStK / 16; ++k) {
+                            const uint64_t bd = umma_desc_sw128(b0 + (k >> 2) * 16384 + 32 * (k & 3));
+                            const uint32_t accum = (st != s0) || (k != 0);
+                            asm volatile(
+                                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                                " tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(td),
+                                "r"(ta + 8u * k), "l"(bd), "r"(idesc), "r"(accum));
+                        }
+                        umma_commit_pair(&sm.empty[s]);
                     }
-                    umma_commit_pair(&sm.aempty[sa]);
-                    umma_commit_pair(&sm.lempty[s]);
+                    __syncwarp();
                 }
-                umma_commit_pair(&sm.dfull);
+                if (elect_one()) umma_commit_pair(&sm.dfull);
+                __syncwarp();
             }
-            if (unsigned long long* trc = g_mmq_trace) {
+            if (unsigned long long* trc = g_mmq_trace; trc && lane == 0) {
                 trc[blockIdx.x * 16 + 3] = tw_ready;
                 trc[blockIdx.x * 16 + 4] = tw_d;
                 trc[blockIdx.x * 16 + 9] = clock64() - tm0;
@@ -306,14 +314,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
             wk.decode(it, tr, tn, s0, s1);
             for (int st = s0; st < s1; ++st, ++g) {
                 if ((int)(g % kMmqExpGroups) != eg) continue;
-                const int s = g % kPairNL, sa = g % kPairNA;
+                const int s = g % kPairNS, sa = s;
                 {
+                    // slot s landed, so the producer saw `empty` for its previous use: the MMAs that
+                    // read A slot s last have completed as well (one commit frees both)
                     MMQ_T0();
-                    mbar_wait_(&sm.full[s], (g / kPairNL) & 1u);
+                    mbar_wait_(&sm.full[s], (g / kPairNS) & 1u);
                     MMQ_ACC(1, tw_full);
-                    const long long ta0 = clock64();
-                    mbar_wait_(&sm.aempty[sa], ((g / kPairNA) & 1u) ^ 1u);
-                    tw_aempty += clock64() - ta0;
                 }
                 const long long tw0 = clock64();
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -807,8 +814,10 @@ extern "C" int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym
 namespace itq3 {
 
 constexpr int kQ8Rec = 8192 + 256 + 128;  // codes [c][row][16 B] | f16 scales [row] | int8 zps [row]
-constexpr int kQ8Threads = 32 * 14;
-constexpr int kQ8NA = 2, kQ8ND = 2;
+constexpr int kQ8ExpGroups = 2;              // expander quads on alternate blocks
+constexpr int kQ8EpiWarp = 2 + 4 * kQ8ExpGroups;
+constexpr int kQ8Threads = 32 * (kQ8EpiWarp + 8);
+constexpr int kQ8NA = 4, kQ8ND = 2;          // TMEM: A ring 4 x 64 columns | D ring 2 x N columns (N <= 128)
 
 __host__ __device__ constexpr int q8_act_bytes(int BN) { return 512 * BN + 8 * BN; }  // B tile + (f, corr)/token
 __host__ __device__ constexpr int q8_slot_bytes(int BN) { return (q8_act_bytes(BN) + kQ8Rec + 1023) / 1024 * 1024; }
@@ -820,8 +829,9 @@ struct Q8Smem {
     uint8_t slot[q8_slots<BN>()][q8_slot_bytes(BN)];  // [B tile (1024-aligned) | meta | weight record]
     uint64_t full[q8_slots<BN>()];
     uint64_t empty[q8_slots<BN>()];
-    uint64_t aready[kQ8NA], aempty[kQ8NA];
-    uint64_t dfull[kQ8ND], dempty[kQ8ND];
+    uint64_t aready[kQ8NA];
+    uint64_t done[kQ8NA];  // block i's MMAs completed (ONE commit): A slot i % 4 free, D slot i % 2 full
+    uint64_t dempty[kQ8ND];
     uint32_t tmem_base;
 };
 
@@ -831,7 +841,8 @@ __global__ void __launch_bounds__(kQ8Threads, 1)
                 TY* __restrict__ y, int64_t stride_r, int64_t stride_m, int64_t slab) {
     constexpr int NS = q8_slots<BN>();
     constexpr int N = 2 * BN;
-    constexpr uint32_t kCols = 2 * 64 + 2 * N <= 256 ? 256 : 512;
+    constexpr uint32_t kCols = 512;
+    constexpr uint32_t kColD = 64 * kQ8NA;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     Q8Smem<BN>& sm = *reinterpret_cast<Q8Smem<BN>*>(base);
@@ -846,12 +857,9 @@ __global__ void __launch_bounds__(kQ8Threads, 1)
         }
         for (int s = 0; s < kQ8NA; ++s) {
             mbar_init_(&sm.aready[s], 4);
-            mbar_init_(&sm.aempty[s], 1);
+            mbar_init_(&sm.done[s], 1);
         }
-        for (int s = 0; s < kQ8ND; ++s) {
-            mbar_init_(&sm.dfull[s], 1);
-            mbar_init_(&sm.dempty[s], 8);
-        }
+        for (int s = 0; s < kQ8ND; ++s) mbar_init_(&sm.dempty[s], 8);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -864,12 +872,14 @@ __global__ void __launch_bounds__(kQ8Threads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = sm.tmem_base;
     const int nblk = b1 - b0;
+    long long c[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // cycle accounting (g_mmq_trace)
+    const long long tk0 = clock64();
 
     if (warp == 0) {
         if (lane == 0) {
             for (int i = 0; i < nblk; ++i) {
                 const int s = i % NS;
-                mbar_wait_(&sm.empty[s], ((unsigned)(i / NS) & 1u) ^ 1u);
+                { MMQ_T0(); mbar_wait_(&sm.empty[s], ((unsigned)(i / NS) & 1u) ^ 1u); MMQ_ACC(0, c[0]); }
                 mbar_expect_tx_(&sm.full[s], q8_act_bytes(BN) + kQ8Rec);
                 const int b = b0 + i;
                 bulk_g2s_(sm.slot[s], act + ((int64_t)tt * NB + b) * q8_act_bytes(BN), q8_act_bytes(BN), &sm.full[s]);
@@ -877,118 +887,123 @@ __global__ void __launch_bounds__(kQ8Threads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {  // the whole warp runs the loop, one elected lane issues (descriptors in uniform registers)
             // D s32, A u8, B s8, K-major, N = 2 BN, M = 128
             const uint32_t idesc = (2u << 4) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
             for (int i = 0; i < nblk; ++i) {
                 const int s = i % NS, sa = i % kQ8NA, sd = i % kQ8ND;
-                mbar_wait_(&sm.aready[sa], (unsigned)(i / kQ8NA) & 1u);
-                mbar_wait_(&sm.full[s], (unsigned)(i / NS) & 1u);
-                mbar_wait_(&sm.dempty[sd], ((unsigned)(i / kQ8ND) & 1u) ^ 1u);
+                { MMQ_T0(); mbar_wait_(&sm.aready[sa], (unsigned)(i / kQ8NA) & 1u); MMQ_ACC(0, c[1]); }
+                { MMQ_T0(); mbar_wait_(&sm.full[s], (unsigned)(i / NS) & 1u); MMQ_ACC(0, c[2]); }
+                { MMQ_T0(); mbar_wait_(&sm.dempty[sd], ((unsigned)(i / kQ8ND) & 1u) ^ 1u); MMQ_ACC(0, c[3]); }
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t bt = smem_addr(sm.slot[s]);
-                const uint32_t ta = tmem + 64u * sa, td = tmem + 128u + (uint32_t)N * sd;
+                const uint32_t ta = tmem + 64u * sa, td = tmem + kColD + (uint32_t)N * sd;
+                if (elect_one()) {
 #pragma unroll
-                for (int m = 0; m < 8; ++m) {
-                    const uint64_t bd = umma_desc_sw128(bt + (m >> 2) * (N * 128) + 32 * (m & 3));
-                    const uint32_t acc = m > 0;
-                    asm volatile(
-                        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                        " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(td),
-                        "r"(ta + 8u * m), "l"(bd), "r"(idesc), "r"(acc));
+                    for (int m = 0; m < 8; ++m) {
+                        const uint64_t bd = umma_desc_sw128(bt + (m >> 2) * (N * 128) + 32 * (m & 3));
+                        const uint32_t acc = m > 0;
+                        asm volatile(
+                            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                            " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(td),
+                            "r"(ta + 8u * m), "l"(bd), "r"(idesc), "r"(acc));
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     smem_addr(&sm.done[sa]))
+                                 : "memory");
                 }
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                 smem_addr(&sm.aempty[sa]))
-                             : "memory");
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                 smem_addr(&sm.dfull[sd]))
-                             : "memory");
+                __syncwarp();
             }
         }
-    } else if (warp < 6) {
-        // ---- expanders: row r = TMEM lane; A column 8 m + c = code word (8 (m & 1) + c) >> 2 (m >> 1) & 3s
-        const int q = warp & 3, r = 32 * q + lane;
+    } else if (warp < kQ8EpiWarp) {
+        // ---- expanders: row r = TMEM lane; A column 8 m + c = code word (8 (m & 1) + c) >> 2 (m >> 1) & 3s.
+        // Two quads take alternate blocks so one quad's decode overlaps the other's tcgen05.st latency.
+        const int q = warp & 3, r = 32 * q + lane, eg = (warp - 2) >> 2;
         const uint32_t ta_row = tmem + ((uint32_t)(32 * q) << 16);
-        for (int i = 0; i < nblk; ++i) {
+        for (int i = eg; i < nblk; i += kQ8ExpGroups) {
             const int s = i % NS, sa = i % kQ8NA;
-            mbar_wait_(&sm.full[s], (unsigned)(i / NS) & 1u);
-            const uint8_t* rec = sm.slot[s] + q8_act_bytes(BN);
+            { MMQ_T0(); mbar_wait_(&sm.full[s], (unsigned)(i / NS) & 1u); MMQ_ACC(0, c[5]); }
+            const uint32_t rec = smem_addr(sm.slot[s]) + q8_act_bytes(BN);
             uint32_t w[16];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const uint4 v = reinterpret_cast<const uint4*>(rec + c * 2048)[r];
-                w[4 * c] = v.x;
-                w[4 * c + 1] = v.y;
-                w[4 * c + 2] = v.z;
-                w[4 * c + 3] = v.w;
+            for (int cc = 0; cc < 4; ++cc) {
+                const uint4 v = lds128(rec + cc * 2048 + 16 * r);
+                w[4 * cc] = v.x;
+                w[4 * cc + 1] = v.y;
+                w[4 * cc + 2] = v.z;
+                w[4 * cc + 3] = v.w;
             }
-            mbar_wait_(&sm.aempty[sa], ((unsigned)(i / kQ8NA) & 1u) ^ 1u);
+            // A slot sa was last read by block i - 4: wait for its completion (phase of block i - 4)
+            if (i >= kQ8NA) { MMQ_T0(); mbar_wait_(&sm.done[sa], (unsigned)((i - kQ8NA) / kQ8NA) & 1u); MMQ_ACC(0, c[6]); }
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            uint32_t a[64];
 #pragma unroll
-            for (int m = 0; m < 8; ++m)
+            for (int hh = 0; hh < 2; ++hh) {  // columns 32 hh .. 32 hh + 31 (m = 4 hh .. 4 hh + 3)
+                uint32_t a[32];
 #pragma unroll
-                for (int c = 0; c < 8; ++c) a[8 * m + c] = (w[8 * (m & 1) + c] >> (2 * (m >> 1))) & 0x03030303u;
-            asm volatile(
-                "tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-                "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,"
-                "%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,"
-                "%61,%62,%63,%64};" ::"r"(ta_row + 64u * sa),
-                "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]),
-                "r"(a[8]), "r"(a[9]), "r"(a[10]), "r"(a[11]), "r"(a[12]), "r"(a[13]), "r"(a[14]), "r"(a[15]),
-                "r"(a[16]), "r"(a[17]), "r"(a[18]), "r"(a[19]), "r"(a[20]), "r"(a[21]), "r"(a[22]), "r"(a[23]),
-                "r"(a[24]), "r"(a[25]), "r"(a[26]), "r"(a[27]), "r"(a[28]), "r"(a[29]), "r"(a[30]), "r"(a[31]),
-                "r"(a[32]), "r"(a[33]), "r"(a[34]), "r"(a[35]), "r"(a[36]), "r"(a[37]), "r"(a[38]), "r"(a[39]),
-                "r"(a[40]), "r"(a[41]), "r"(a[42]), "r"(a[43]), "r"(a[44]), "r"(a[45]), "r"(a[46]), "r"(a[47]),
-                "r"(a[48]), "r"(a[49]), "r"(a[50]), "r"(a[51]), "r"(a[52]), "r"(a[53]), "r"(a[54]), "r"(a[55]),
-                "r"(a[56]), "r"(a[57]), "r"(a[58]), "r"(a[59]), "r"(a[60]), "r"(a[61]), "r"(a[62]), "r"(a[63])
-                : "memory");
+                for (int mm = 0; mm < 4; ++mm)
+#pragma unroll
+                    for (int cc = 0; cc < 8; ++cc) {
+                        const int m = 4 * hh + mm;
+                        a[8 * mm + cc] = (w[8 * (m & 1) + cc] >> (2 * (m >> 1))) & 0x03030303u;
+                    }
+                asm volatile(
+                    "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+                    "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
+                        ta_row + 64u * sa + 32u * hh),
+                    "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]),
+                    "r"(a[8]), "r"(a[9]), "r"(a[10]), "r"(a[11]), "r"(a[12]), "r"(a[13]), "r"(a[14]), "r"(a[15]),
+                    "r"(a[16]), "r"(a[17]), "r"(a[18]), "r"(a[19]), "r"(a[20]), "r"(a[21]), "r"(a[22]), "r"(a[23]),
+                    "r"(a[24]), "r"(a[25]), "r"(a[26]), "r"(a[27]), "r"(a[28]), "r"(a[29]), "r"(a[30]), "r"(a[31])
+                    : "memory");
+            }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive_(&sm.aready[sa]);
         }
     } else {
-        // ---- epilogue: rows 32 q + lane, tokens [hh BN/2, (hh + 1) BN/2) ----
+        // ---- epilogue: rows 32 q + lane, tokens [hh BN/2, (hh + 1) BN/2), drained 8 tokens at a time ----
         constexpr int H = BN / 2;
-        const int q = warp & 3, hh = (warp - 6) >> 2;  // TMEM lane quarter = warp % 4
+        const int q = warp & 3, hh = (warp - kQ8EpiWarp) >> 2;  // TMEM lane quarter = warp % 4
         const int r = 32 * q + lane;
         const int64_t grow = (int64_t)rt * 128 + r;
-        const uint32_t td_row = tmem + ((uint32_t)(32 * q) << 16) + 128u;
+        const uint32_t td_row = tmem + ((uint32_t)(32 * q) << 16) + kColD;
         float acc[H];
 #pragma unroll
         for (int j = 0; j < H; ++j) acc[j] = 0.f;
         for (int i = 0; i < nblk; ++i) {
             const int s = i % NS, sd = i % kQ8ND;
-            mbar_wait_(&sm.dfull[sd], (unsigned)(i / kQ8ND) & 1u);
+            { MMQ_T0(); mbar_wait_(&sm.done[i % kQ8NA], (unsigned)(i / kQ8NA) & 1u); MMQ_ACC(0, c[8]); }
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            uint32_t c0[H], c1[H];
+            const uint8_t* slot = sm.slot[s];
+            const uint32_t rec = smem_addr(slot) + q8_act_bytes(BN);
+            const float d = __half2float(__ushort_as_half(lds16(rec + 8192 + 2 * r)));
+            const float zf = (float)(1 + lds_s8(rec + 8192 + 256 + r));
+            const float2* meta = reinterpret_cast<const float2*>(slot + 512 * BN) + hh * H;
             const uint32_t t0 = td_row + (uint32_t)N * sd + (uint32_t)(hh * H);
 #pragma unroll
-            for (int j = 0; j < H; j += 8) {
+            for (int j0 = 0; j0 < H; j0 += 8) {
+                uint32_t c0[8], c1[8];
                 asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                             : "=r"(c0[j]), "=r"(c0[j + 1]), "=r"(c0[j + 2]), "=r"(c0[j + 3]), "=r"(c0[j + 4]),
-                               "=r"(c0[j + 5]), "=r"(c0[j + 6]), "=r"(c0[j + 7])
-                             : "r"(t0 + j));
+                             : "=r"(c0[0]), "=r"(c0[1]), "=r"(c0[2]), "=r"(c0[3]), "=r"(c0[4]), "=r"(c0[5]),
+                               "=r"(c0[6]), "=r"(c0[7])
+                             : "r"(t0 + j0));
                 asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                             : "=r"(c1[j]), "=r"(c1[j + 1]), "=r"(c1[j + 2]), "=r"(c1[j + 3]), "=r"(c1[j + 4]),
-                               "=r"(c1[j + 5]), "=r"(c1[j + 6]), "=r"(c1[j + 7])
-                             : "r"(t0 + BN + j));
-            }
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive_(&sm.dempty[sd]);
-            const uint8_t* slot = sm.slot[s];
-            const uint8_t* rec = slot + q8_act_bytes(BN);
-            const float d = __half2float(__ushort_as_half(reinterpret_cast<const uint16_t*>(rec + 8192)[r]));
-            const float zf = (float)(1 + (int)reinterpret_cast<const int8_t*>(rec + 8192 + 256)[r]);
-            const float2* meta = reinterpret_cast<const float2*>(slot + 512 * BN) + hh * H;
+                             : "=r"(c1[0]), "=r"(c1[1]), "=r"(c1[2]), "=r"(c1[3]), "=r"(c1[4]), "=r"(c1[5]),
+                               "=r"(c1[6]), "=r"(c1[7])
+                             : "r"(t0 + BN + j0));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (j0 + 8 >= H) {  // last chunk read: accumulator slot free
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_(&sm.dempty[sd]);
+                }
 #pragma unroll
-            for (int j = 0; j < H; ++j) {
-                const float2 fc = meta[j];  // (2^(ex-4), Q 2^(ex-4)) of token hh H + j
-                const float v = (float)((int)c0[j] + 256 * (int)c1[j]);
-                acc[j] += d * (fc.x * v - zf * fc.y);
+                for (int j = 0; j < 8; ++j) {
+                    const float2 fc = meta[j0 + j];  // (2^(ex-4), Q 2^(ex-4)) of token hh H + j0 + j
+                    const float v = (float)((int)c0[j] + 256 * (int)c1[j]);
+                    acc[j0 + j] += d * (fc.x * v - zf * fc.y);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive_(&sm.empty[s]);
@@ -1000,6 +1015,14 @@ __global__ void __launch_bounds__(kQ8Threads, 1)
                 if (m < M) y[grow * stride_r + m * stride_m] = (TY)acc[j];
             }
         }
+    }
+    if (unsigned long long* trc = g_mmq_trace) {
+        const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+        const long long tot = clock64() - tk0;
+        if (threadIdx.x == 0) { trc[cta * 16 + 0] = c[0]; trc[cta * 16 + 10] = nblk; trc[cta * 16 + 11] = tot; }
+        if (threadIdx.x == 32) { trc[cta * 16 + 1] = c[1]; trc[cta * 16 + 2] = c[2]; trc[cta * 16 + 3] = c[3]; trc[cta * 16 + 4] = tot; }
+        if (threadIdx.x == 64) { trc[cta * 16 + 5] = c[5]; trc[cta * 16 + 6] = c[6]; trc[cta * 16 + 7] = tot; }
+        if (threadIdx.x == 32 * kQ8EpiWarp) { trc[cta * 16 + 8] = c[8]; trc[cta * 16 + 9] = tot; }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();

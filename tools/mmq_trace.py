@@ -49,6 +49,17 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     _lib.call("itq3_mmq_set_trace", None)
+    if P.compute.MMQ_MIN_TOKENS <= a.m <= P.compute.MMQ8_MAX_TOKENS:  # K5b: its own counter layout
+        _lib.call("itq3_mmq_set_trace", None)
+        t = tr.view(-1, 16).cpu().numpy()
+        t = t[t[:, 10] > 0]
+        names8 = ["prod_wait_empty", "mma_wait_aready", "mma_wait_full", "mma_wait_dempty", "mma_total",
+                  "exp_wait_full", "exp_wait_aempty", "exp_total", "epi_wait_dfull", "epi_total", "blocks", "cta_total"]
+        print(f"K5b {a.rows}x{a.cols} M={a.m}: {e0.elapsed_time(e1) * 1e3:.1f} us (rotate + mmq8), {len(t)} CTAs")
+        for i, n in enumerate(names8):
+            print(f"  {n:18s} median {np.median(t[:, i]):10.0f}  max {t[:, i].max():10.0f}")
+        print(f"  cycles per block: {np.median(t[:, 11]) / np.median(t[:, 10]):.0f}")
+        return
     # separate timings (no trace): rotation and the MMQ kernel, 10 calls each
     lib = _lib.load()
     act = torch.empty(lib.itq3_mmq_act_nbytes(a.cols, a.m), dtype=torch.uint8, device=dev)

@@ -14,7 +14,7 @@ __device__ __forceinline__ void csync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int CG, int N, bool ATMEM, int COMMIT = 0, bool ST = false>
+template <int CG, int N, bool ATMEM, int COMMIT = 0, bool ST = false, bool LD = false, bool I8 = false>
 __global__ void __cluster_dims__(2, 1, 1) rate(int R, long long* out) {
     extern __shared__ __align__(1024) uint8_t dyn[];
     uint8_t* bt = dyn;              // 32 KB: B tile (N/CG rows x 128 B per k-atom, reused)
@@ -46,7 +46,8 @@ __global__ void __cluster_dims__(2, 1, 1) rate(int R, long long* out) {
     const uint32_t tm = tbase;
     const bool issuer = threadIdx.x == 0 && (CG == 1 || rank == 0);
     if (issuer) {
-        const uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)((128 * CG) >> 4) << 24);
+        const uint32_t idesc = I8 ? ((2u << 4) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)((128 * CG) >> 4) << 24))
+                                  : ((1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)((128 * CG) >> 4) << 24));
         const long long t0 = clock64();
         for (int k = 0; k < R; ++k) {
             const uint64_t bd = desc_sw128(saddr(bt) + 32 * (k & 3));
@@ -55,6 +56,10 @@ __global__ void __cluster_dims__(2, 1, 1) rate(int R, long long* out) {
                 if (CG == 2)
                     asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
                                  " tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tm),
+                                 "r"(tm + 256 + 8 * (k & 31)), "l"(bd), "r"(idesc), "r"(acc));
+                else if (I8)
+                    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                                 " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tm),
                                  "r"(tm + 256 + 8 * (k & 31)), "l"(bd), "r"(idesc), "r"(acc));
                 else
                     asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -93,6 +98,19 @@ __global__ void __cluster_dims__(2, 1, 1) rate(int R, long long* out) {
         const long long t1 = clock64();
         if (blockIdx.x == 0) out[0] = t1 - t0;
     }
+    if (LD && warp >= 4) {  // concurrent D traffic: tcgen05.ld.32x32b.x32 + wait in a loop (epilogue-like)
+        const uint32_t td = tm + ((uint32_t)((warp & 3) * 32) << 16) + 128;
+        uint32_t sink = 0;
+        for (int k = 0; k < R / 4; ++k) {
+            uint32_t v[8];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                         : "r"(td + 8 * (k & 7)));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            sink += v[0] ^ v[7];
+        }
+        if (sink == 0x12345) out[7] = sink;
+    }
     if (ST && warp >= 4) {  // concurrent A traffic: one tcgen05.st.32x32b.x32 + wait per 4 MMAs
         uint32_t a[32];
         for (int i = 0; i < 32; ++i) a[i] = 0x3c003c00u;
@@ -122,13 +140,13 @@ __global__ void __cluster_dims__(2, 1, 1) rate(int R, long long* out) {
     }
 }
 
-template <int CG, int N, bool AT, int COMMIT = 0, bool ST = false>
+template <int CG, int N, bool AT, int COMMIT = 0, bool ST = false, bool LD = false, bool I8 = false>
 void go(long long* d) {
     const int R = 8192;
     const int smem = 48 * 1024 + 1024;
-    cudaFuncSetAttribute(rate<CG, N, AT, COMMIT, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    rate<CG, N, AT, COMMIT, ST><<<148, 256, smem>>>(R, d);
-    rate<CG, N, AT, COMMIT, ST><<<148, 256, smem>>>(R, d);
+    cudaFuncSetAttribute(rate<CG, N, AT, COMMIT, ST, LD, I8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    rate<CG, N, AT, COMMIT, ST, LD, I8><<<148, 256, smem>>>(R, d);
+    rate<CG, N, AT, COMMIT, ST, LD, I8><<<148, 256, smem>>>(R, d);
     cudaError_t e = cudaDeviceSynchronize();
     long long h[1];
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
@@ -137,26 +155,22 @@ void go(long long* d) {
         return;
     }
     const double macs_per_sm = 128.0 * N * 16 * R / h[0];  // per SM (the pair splits M = 256)
-    printf("cta_group::%d M=%3d N=%3d A=%s commit/%d st=%d: %.1f cycles/MMA, %.0f MACs/clk/SM\n", CG, 128 * CG, N,
-           AT ? "tmem" : "smem", COMMIT, (int)ST, (double)h[0] / R, macs_per_sm);
+    printf("cta_group::%d %s M=%3d N=%3d A=%s commit/%d st=%d ld=%d: %.1f cycles/MMA, %.0f MACs/clk/SM\n", CG,
+           I8 ? "i8 " : "f16", 128 * CG, N, AT ? "tmem" : "smem", COMMIT, (int)ST, (int)LD, (double)h[0] / R,
+           macs_per_sm * (I8 ? 2 : 1));
 }
 
 int main() {
     long long* d;
     cudaMalloc(&d, 64);
-    go<1, 128, false>(d);
-    go<1, 256, false>(d);
-    go<1, 128, true>(d);
-    go<1, 256, true>(d);
-    go<2, 64, false>(d);
-    go<2, 128, false>(d);
-    go<2, 256, false>(d);
-    go<2, 64, true>(d);
     go<2, 128, true>(d);
     go<2, 256, true>(d);
-    go<2, 128, true, 4>(d);
-    go<2, 128, true, 0, true>(d);
-    go<2, 128, true, 4, true>(d);
-    go<1, 256, true, 4, true>(d);
+    go<2, 256, true, 8, true, true>(d);
+    go<1, 32, true, 0, false, false, true>(d);
+    go<1, 32, true, 8, false, false, true>(d);
+    go<1, 32, true, 8, true, false, true>(d);
+    go<1, 32, true, 8, false, true, true>(d);
+    go<1, 32, true, 8, true, true, true>(d);
+    go<1, 128, true, 8, true, true, true>(d);
     return 0;
 }
