@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
     __shared__ __align__(16) float tile[32][257];
     __half(&th)[32][264] = *reinterpret_cast<__half(*)[32][264]>(&tile[0][0]);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t b = blockIdx.x, m0 = (int64_t)blockIdx.y * 32;
+    const int64_t b = blockIdx.y, m0 = (int64_t)blockIdx.x * 32;  // adjacent CTAs: adjacent token groups (DRAM locality)
     const TX* xb = x + b * 256 * stride_k;
     if (stride_k == 1 && stride_m != 1) {  // token-major input: threads along k
 #pragma unroll 4
@@ -673,7 +673,7 @@ extern "C" int itq3_rotate_act_f16(const void* x, int x_dtype, int64_t cols, int
     }
     const int BN = itq3_mmq_block_n(m);
     const int64_t NB = cols / 256, M_pad = (m + BN - 1) / BN * BN;
-    const dim3 grid((unsigned)NB, (unsigned)(M_pad / 32));
+    const dim3 grid((unsigned)(M_pad / 32), (unsigned)NB);
     cudaStream_t s = (cudaStream_t)stream;
     switch (x_dtype) {
         case ITQ3_F32:
