@@ -197,6 +197,58 @@ __global__ void validate_kernel(const uint8_t* __restrict__ payload, int64_t n_b
     if (lane == 0 && key != ~0ull) atomicMin(first_bad, key);
 }
 
+// K7 fast path (block_n 256, variant s): one THREAD per 100-byte block.  The warp stages its 32
+// consecutive blocks (3200 contiguous bytes) with 16-byte coalesced loads into shared memory, each
+// thread checks its own block from there (25 words, stride 25: conflict-free), and only offenders
+// touch the atomic -- no shuffles, so the pass runs at HBM speed.
+__global__ void __launch_bounds__(256) validate256_kernel(const uint8_t* __restrict__ payload, int64_t n_blocks,
+                                                          uint32_t mask, unsigned long long* first_bad) {
+    __shared__ uint32_t stage[8][32 * 25];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t blk0 = ((int64_t)blockIdx.x * 8 + w) * 32;
+    if (blk0 >= n_blocks) return;
+    const int nb = (int)(n_blocks - blk0 < 32 ? n_blocks - blk0 : 32);
+    const uint8_t* src = payload + blk0 * 100;
+    uint32_t* st = stage[w];
+    if (nb == 32 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+#pragma unroll
+        for (int i = 0; i < 7; ++i) {
+            const int c = lane + 32 * i;  // 16-byte chunk of the warp's 3200 bytes
+            if (c < 200) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + c);
+                st[4 * c] = v.x, st[4 * c + 1] = v.y, st[4 * c + 2] = v.z, st[4 * c + 3] = v.w;
+            }
+        }
+    } else {
+        for (int c = lane; c < nb * 25; c += 32) st[c] = __ldg(reinterpret_cast<const uint32_t*>(src) + c);
+    }
+    __syncwarp();
+    if (lane >= nb) return;
+    const uint32_t* b = st + 25 * lane;
+    const int64_t blk = blk0 + lane;
+    unsigned long long key = ~0ull;
+    if (mask & ITQ3_CHECK_PLANES) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t bad = b[16 + i] | (b[i] & b[8 + i]);
+            if (bad) {
+                key = ((unsigned long long)blk << 16) | (unsigned long long)(32 * i + __ffs(bad) - 1);
+                break;
+            }
+        }
+    }
+    const uint16_t sb = (uint16_t)(b[24] & 0xffffu), zb = (uint16_t)(b[24] >> 16);
+    unsigned long long k2 = ~0ull;
+    if ((mask & ITQ3_CHECK_SCALE_NAN) && (sb & 0x7fff) > 0x7c00) k2 = 1;
+    else if ((mask & ITQ3_CHECK_ZP) && !(zb == 0 || zb == 0x8000 || zb == 0x3C00 || zb == 0xBC00)) k2 = 2;
+    else if ((mask & ITQ3_CHECK_ZP_FINITE) && (zb & 0x7c00) == 0x7c00) k2 = 4;
+    if (k2 != ~0ull) {
+        const unsigned long long kk = ((unsigned long long)blk << 16) | (k2 << 10);
+        key = kk < key ? kk : key;
+    }
+    if (key != ~0ull) atomicMin(first_bad, key);
+}
+
 // ------------------------------------------------------------------------------------------
 // K2 (generic): decode_block (codec.py:152-161) in binary64 with the reference's data flow.
 // One warp per block; bit-exact for every block size and variant.
@@ -321,6 +373,11 @@ extern "C" int itq3_validate(const uint8_t* payload, int64_t n_blocks, int block
     }
     if (n_blocks <= 0) return ITQ3_OK;
     const int64_t threads = n_blocks * 32;
+    if (block_n == 256 && !sub_scales) {
+        validate256_kernel<<<(unsigned)((n_blocks + 255) / 256), 256, 0, (cudaStream_t)stream>>>(payload, n_blocks,
+                                                                                               check_mask, d_first_bad);
+        return check_launch("itq3_validate");
+    }
     validate_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         payload, n_blocks, block_n, sub_scales, check_mask, d_first_bad);
     return check_launch("itq3_validate");

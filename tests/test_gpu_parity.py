@@ -274,3 +274,25 @@ def test_block_codec_single_block():
     assert z.scale == 0.0
     np.testing.assert_array_equal(P.decode_block(z), np.zeros(32))
     assert math.isclose(P.argmin_scale_coeff(), 0.878, abs_tol=1e-12)
+
+
+@pytest.mark.parametrize("nblocks", [1, 31, 33, 70001])
+def test_validate_fast_path_first_offender(nblocks):
+    """K7 fast path (block_n 256, variant s, one thread per block): same first offender and message as
+    the per-block reference checks, for block counts that leave ragged warps."""
+    from paper_2603_27914_b200 import codec as C
+
+    rng = np.random.default_rng(nblocks)
+    w = rng.standard_normal((nblocks, 256)).astype(np.float32)
+    q = P.quantize_tensor(torch.from_numpy(w).cuda())
+    pay = q.payload().clone()
+    C.validate_payload(pay, 256, False, True, True)  # clean: no error
+    late, early = nblocks - 1, nblocks // 2
+    bad = pay.clone()
+    bad[late, 64 + 5] |= 0x10      # plane 2 bit -> stored code > 2 at index 8*5+4 = 44
+    with pytest.raises(P.CorruptionError, match=f"block {late}:.*index 44"):
+        C.validate_payload(bad, 256, False, True, True)
+    if early < late:  # an earlier offender wins
+        bad[early, 96:98] = torch.tensor([0x01, 0x7E], dtype=torch.uint8)  # scale NaN (0x7E01)
+        with pytest.raises(P.CorruptionError, match=f"block {early}: deserialize_block: scale is NaN"):
+            C.validate_payload(bad, 256, False, True, True)
