@@ -74,6 +74,9 @@ int itq3_validate(const uint8_t* payload, int64_t n_blocks, int block_n, int sub
  * out: numel values (F64 = bit-exact with the reference, F32 = exact value cast). */
 int itq3_dequant(const uint8_t* payload, int64_t n_blocks, int block_n, int sub_scales, int64_t numel, void* out,
                  int out_dtype, void* stream);
+/* diagnostics: device buffer of 16 u64 counters per CTA (cycle accounting of the tensor-core
+ * dequantiser used for block_n 256 / variant s; tools/dequant_trace.py), or NULL to switch it off. */
+int itq3_dequant_set_trace(void* buf);
 
 /* ---- transform: fwht_forward / fwht_inverse (transform.py:61-96) on n_vec
  * contiguous vectors of length n (2..512, power of two), dtype F32 or F64,

@@ -383,10 +383,69 @@ extern "C" int itq3_validate(const uint8_t* payload, int64_t n_blocks, int block
     return check_launch("itq3_validate");
 }
 
+// The exact pass behind the tensor-core dequantiser (dequant.cu): a warp screens 32 blocks at a
+// time (one lane each) and decodes, with the reference's float64 data flow, only the blocks that
+// path leaves out (scale zero, negative, inf or NaN; zero-point other than +-0 / +-1) -- normally none.
+template <typename TOut>
+__global__ void __launch_bounds__(256) dequant_fixup_kernel(const uint8_t* __restrict__ payload, int64_t n_blocks,
+                                                            int64_t numel, TOut* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t b0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; b0 < n_blocks; b0 += nwarps * 32) {
+        const int64_t bl = b0 + lane;
+        bool unsafe = false;
+        if (bl < n_blocks) {
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(payload + bl * 100 + 96);
+            const uint16_t sb = (uint16_t)(w & 0xffffu), zb = (uint16_t)(w >> 16);
+            unsafe = !(sb != 0 && !(sb & 0x8000) && (sb & 0x7c00) != 0x7c00 &&
+                       (zb == 0 || zb == 0x8000 || zb == 0x3C00 || zb == 0xBC00));
+        }
+        uint32_t m = __ballot_sync(FULL, unsafe);
+        while (m) {
+            const int64_t blk = b0 + __ffs(m) - 1;
+            m &= m - 1;
+            const uint8_t* p = payload + blk * 100;
+            const uint16_t sb = *reinterpret_cast<const uint16_t*>(p + 96);
+            const uint16_t zb = *reinterpret_cast<const uint16_t*>(p + 98);
+            const double z = trunc(f16_bits_to_f64(zb));
+            const double scale = f16_bits_to_f64(sb);
+            double v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const uint32_t p0 = *reinterpret_cast<const uint32_t*>(p + 4 * e);
+                const uint32_t p1 = *reinterpret_cast<const uint32_t*>(p + 32 + 4 * e);
+                const uint32_t p2 = *reinterpret_cast<const uint32_t*>(p + 64 + 4 * e);
+                const int c = (int)((p0 >> lane) & 1u) + 2 * (int)((p1 >> lane) & 1u) + 4 * (int)((p2 >> lane) & 1u);
+                v[e] = __dmul_rn(scale, __dsub_rn((double)(c - 1), z));
+            }
+            warp_butterfly<8>(v, lane);
+            const double norm = __ddiv_rn(1.0, __dsqrt_rn(256.0));
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int64_t gi = blk * 256 + lane + 32 * e;
+                if (gi < numel) out[gi] = (TOut)__dmul_rn(v[e], norm);
+            }
+        }
+    }
+}
+
+template <typename TOut>
+int itq3_dequant_tc(const uint8_t* payload, int64_t n_blocks, int64_t numel, TOut* out, cudaStream_t s);
+
 template <typename TOut>
 static int launch_dequant(const uint8_t* payload, int64_t nb, int n, int ss, int64_t numel, TOut* out,
                           cudaStream_t s) {
     const unsigned grid = (unsigned)((nb * 32 + 255) / 256);
+    if (n == 256 && !ss) {  // tensor-core IFWHT (dequant.cu) + exact pass for the blocks it leaves out
+        const int rc = itq3_dequant_tc<TOut>(payload, nb, numel, out, s);
+        if (rc) return rc;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        const int64_t want = (nb + 255) / 256;
+        const unsigned fgrid = (unsigned)(want < 8 * sms ? (want > 0 ? want : 1) : 8 * sms);
+        dequant_fixup_kernel<TOut><<<fgrid, 256, 0, s>>>(payload, nb, numel, out);
+        return check_launch("itq3_dequant (exact pass)");
+    }
     switch (n) {
         case 32: dequant_kernel<32, TOut><<<grid, 256, 0, s>>>(payload, nb, ss, numel, out); break;
         case 64: dequant_kernel<64, TOut><<<grid, 256, 0, s>>>(payload, nb, ss, numel, out); break;
