@@ -296,3 +296,35 @@ def test_validate_fast_path_first_offender(nblocks):
         bad[early, 96:98] = torch.tensor([0x01, 0x7E], dtype=torch.uint8)  # scale NaN (0x7E01)
         with pytest.raises(P.CorruptionError, match=f"block {early}: deserialize_block: scale is NaN"):
             C.validate_payload(bad, 256, False, True, True)
+
+
+@pytest.mark.parametrize("nblocks,tail", [(1, 0), (129, 0), (300, 77), (1000, 255)])
+@pytest.mark.filterwarnings("ignore::RuntimeWarning")
+def test_dequant_tensor_core_path_bit_exact(nblocks, tail):
+    """K2t (tensor-core IFWHT, block_n 256 / variant s) plus its exact float64 pass: bit-identical
+    (incl. signed zeros) to the oracle's decode, for ragged element counts and for blocks the tensor-core
+    path hands to the exact pass (scale +0, negative, inf; zero-point 2.0)."""
+    rng = np.random.default_rng(nblocks + tail)
+    numel = nblocks * 256 - tail
+    w = (rng.standard_normal(numel) * 0.1).astype(np.float32)
+    ref_pay, _ = O.quantize_payload(w[None, :])
+    pay = ref_pay.copy()
+    nb = pay.shape[0]
+    specials = {0: 0x0000, 1: 0xBC00, 2: 0x7C00}  # scale +0, -1.0, +inf
+    for b, sb in specials.items():
+        if b < nb:
+            pay[b, 96:98] = np.frombuffer(np.uint16(sb).tobytes(), np.uint8)
+    if nb > 3:
+        pay[3, 98:100] = np.frombuffer(np.uint16(0x4000).tobytes(), np.uint8)  # zero-point 2.0
+    want = O.dequantize(pay, 1, numel, 256, False).reshape(-1)
+    dev = torch.device("cuda", 0)
+    p = torch.from_numpy(pay).to(dev)
+    for dt in (torch.float64, torch.float32):
+        out = torch.empty(numel, dtype=dt, device=dev)
+        P._lib.call("itq3_dequant", P._lib.ptr(p), nb, 256, 0, numel, P._lib.ptr(out), P._lib.TORCH_DTYPE_CODE[dt],
+                    P._lib.stream_ptr(dev))
+        got = out.cpu().numpy().astype(np.float64)
+        exp = want.astype(np.float32).astype(np.float64) if dt == torch.float32 else want
+        assert np.array_equal(got.view(np.uint64), exp.view(np.uint64)) or \
+            np.array_equal(np.isnan(got), np.isnan(exp)) and np.array_equal(
+                np.where(np.isnan(got), 0, got).view(np.uint64), np.where(np.isnan(exp), 0, exp).view(np.uint64)), dt
