@@ -188,7 +188,7 @@ struct PairWork {
     }
 };
 
-template <typename TY>
+template <int BN, typename TY>  // BN = tokens per pair tile (256, or 128 for M <= 128)
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
     mmq_pair_kernel(const uint8_t* __restrict__ wrec, int asym, PairWork wk, const uint8_t* __restrict__ act,
                     int64_t rows, int64_t M, TY* __restrict__ y, int64_t stride_r, int64_t stride_m, int64_t slab) {
@@ -231,7 +231,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
                 int tr, tn, s0, s1;
                 wk.decode(it, tr, tn, s0, s1);
                 const uint8_t* wsrc = wrec + ((int64_t)(2 * tr + rank) * wk.NS) * kWRec;
-                const uint8_t* bsrc = act + ((int64_t)(2 * tn + rank) * wk.NS) * (2 * 16384);
+                const uint8_t* bsrc = act + ((int64_t)(2 * tn + rank) * wk.NS) * (BN * 128);
                 for (int st = s0; st < s1; ++st, ++g) {
                     const int s = g % kPairNS;
                     {
@@ -240,9 +240,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
                         MMQ_ACC(0, tw);
                     }
                     const long long ti0 = clock64();
-                    mbar_expect_tx_(&sm.full[s], kWRec + ((dflags & 1) ? 0 : 2 * 16384));
+                    mbar_expect_tx_(&sm.full[s], kWRec + ((dflags & 1) ? 0 : BN * 128));
                     bulk_g2s_(sm.w[s], wsrc + (int64_t)st * kWRec, kWRec, &sm.full[s]);
-                    if (!(dflags & 1)) bulk_g2s_(sm.b[s], bsrc + (int64_t)st * (2 * 16384), 2 * 16384, &sm.full[s]);
+                    if (!(dflags & 1)) bulk_g2s_(sm.b[s], bsrc + (int64_t)st * (BN * 128), BN * 128, &sm.full[s]);
                     t_issue += clock64() - ti0;
                 }
             }
@@ -256,7 +256,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
     } else if (warp == 1) {
         if (rank == 0) {  // MMA issuer of the pair (the whole warp runs the loop, one elected lane issues):
                           // M = 256 (128 rows per SM), N = 256, K = 16
-            const uint32_t idesc = (1u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+            const uint32_t idesc = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
             uint32_t g = 0, t = 0;
             long long tw_ready = 0, tw_d = 0;
             const long long tm0 = clock64();
@@ -282,7 +282,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
                     if (elect_one()) {
 #pragma unroll
                         for (int k = 0; k < kStK / 16; ++k) {
-                            const uint64_t bd = umma_desc_sw128(b0 + (k >> 2) * 16384 + 32 * (k & 3));
+                            const uint64_t bd = umma_desc_sw128(b0 + (k >> 2) * (BN * 64) + 32 * (k & 3));
                             const uint32_t accum = (st != s0) || (k != 0);
                             asm volatile(
                                 "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -395,8 +395,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
             const bool live = grow < rows;
             const uint32_t sa = smem_addr(sm.stage[r]);
 #pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
-                const int64_t m0 = (int64_t)tn * 256 + 128 * h;
+            for (int h = 0; h < BN / 128; ++h) {
+                const int64_t m0 = (int64_t)tn * BN + 128 * h;
                 const bool bulk = live && bulk_ok && m0 + 128 <= M;
                 // the previous bulk store has finished reading the staging row
                 if (bulk) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -413,7 +413,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
                           "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
                         : "r"(td_row + 128u * h + 32u * c));
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (h == 1 && c == 3) {  // accumulator free for the next tile
+                    if (h == BN / 128 - 1 && c == 3) {  // accumulator free for the next tile
                         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                         __syncwarp();
                         if (lane == 0) mbar_arrive_remote(&sm.dempty, 0);
@@ -514,8 +514,8 @@ __global__ void repack_mmq_kernel(const uint8_t* __restrict__ payload, int64_t r
 
 // ------------------------------------------------------------------------------------------
 // Activation rotation for MMQ: x'' = (H_256 x_b) / 16 in f16, written pre-swizzled as
-// [256-token tile][CTA half h][64-k chunk kc][128 token rows x 128 B] (SW128 K-major canonical
-// layout), so each CTA's B half of a 128-k stage is ONE contiguous 32 KB copy; padding = 0.
+// [BN-token tile][CTA half h][64-k chunk kc][BN/2 token rows x 128 B] (SW128 K-major canonical
+// layout), so each CTA's B half of a 128-k stage is ONE contiguous copy (BN x 128 B); padding = 0.
 // One CTA per (256-block, 32 tokens): coalesced loads along whichever of k / token is contiguous
 // into a padded smem tile, one warp per 4 tokens for the butterfly (fp32: shuffles for the lane
 // bits, registers for the rest), then 16-byte stores of 8 consecutive k of one token.
@@ -542,7 +542,8 @@ __device__ __forceinline__ void load4(const __nv_bfloat16* p, float (&f)[4]) {
 
 template <typename TX>
 __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restrict__ x, int64_t M, int64_t stride_k,
-                                                             int64_t stride_m, int64_t NC, uint8_t* __restrict__ out) {
+                                                             int64_t stride_m, int64_t NC, int BN,
+                                                             uint8_t* __restrict__ out) {
     // fp32 inputs, token-major (257: conflict-free transposes); after the butterflies the same bytes hold
     // the rotated f16 outputs as [32][264] (528-byte rows: 16-byte aligned, 4 wavefronts per 16-B warp load)
     __shared__ __align__(16) float tile[32][257];
@@ -615,9 +616,10 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
         const int64_t k = b * 256 + 8 * c8;
         const int64_t kc = k >> 6;
         const int kk = (int)(k & 63);
-        const int64_t half = (m >> 7);  // = 2 * tile + h
-        uint8_t* t = out + (half * NC + kc) * 16384;
-        *reinterpret_cast<uint4*>(t + sw128_off((int)(m & 127), kk >> 3)) = make_uint4(p[0], p[1], p[2], p[3]);
+        const int hb = BN / 2;                 // tokens per CTA half of a tile
+        const int64_t half = m / hb;           // = 2 * tile + h
+        uint8_t* t = out + (half * NC + kc) * (int64_t)(hb * 128);
+        *reinterpret_cast<uint4*>(t + sw128_off((int)(m % hb), kk >> 3)) = make_uint4(p[0], p[1], p[2], p[3]);
     }
 }
 
@@ -657,7 +659,7 @@ extern "C" int itq3_repack_mmq(const uint8_t* payload, int64_t rows, int64_t col
     return check_launch("itq3_repack_mmq");
 }
 
-extern "C" int itq3_mmq_block_n(int64_t m) { return (void)m, 256; }  // tokens per CTA-pair tile
+extern "C" int itq3_mmq_block_n(int64_t m) { return m <= 128 ? 128 : 256; }  // tokens per CTA-pair tile
 
 extern "C" int64_t itq3_mmq_act_nbytes(int64_t cols, int64_t m) {
     const int BN = itq3_mmq_block_n(m);
@@ -677,17 +679,17 @@ extern "C" int itq3_rotate_act_f16(const void* x, int x_dtype, int64_t cols, int
     cudaStream_t s = (cudaStream_t)stream;
     switch (x_dtype) {
         case ITQ3_F32:
-            rotate_act_f16_kernel<float><<<grid, 256, 0, s>>>((const float*)x, m, stride_k, stride_m, NB * 4, out);
+            rotate_act_f16_kernel<float><<<grid, 256, 0, s>>>((const float*)x, m, stride_k, stride_m, NB * 4, BN, out);
             break;
         case ITQ3_F64:
-            rotate_act_f16_kernel<double><<<grid, 256, 0, s>>>((const double*)x, m, stride_k, stride_m, NB * 4, out);
+            rotate_act_f16_kernel<double><<<grid, 256, 0, s>>>((const double*)x, m, stride_k, stride_m, NB * 4, BN, out);
             break;
         case ITQ3_BF16:
             rotate_act_f16_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, m, stride_k, stride_m,
-                                                                      NB * 4, out);
+                                                                      NB * 4, BN, out);
             break;
         case ITQ3_F16:
-            rotate_act_f16_kernel<__half><<<grid, 256, 0, s>>>((const __half*)x, m, stride_k, stride_m, NB * 4, out);
+            rotate_act_f16_kernel<__half><<<grid, 256, 0, s>>>((const __half*)x, m, stride_k, stride_m, NB * 4, BN, out);
             break;
         default:
             set_error("itq3_rotate_act_f16: unsupported dtype %d", x_dtype);
@@ -712,7 +714,7 @@ static int mmq_max_clusters() {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         int c = 0;
-        if (cudaOccupancyMaxActiveClusters(&c, mmq_pair_kernel<float>, &cfg) != cudaSuccess || c < 1) {
+        if (cudaOccupancyMaxActiveClusters(&c, mmq_pair_kernel<256, float>, &cfg) != cudaSuccess || c < 1) {
             cudaGetLastError();
             int sms = 148;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -726,7 +728,8 @@ static int mmq_max_clusters() {
 static int mmq_splits(int64_t rows, int64_t cols, int64_t m) {
     // split K only when the output tiles leave more than half of the CTA pairs idle, so the fp32
     // partial traffic never costs more than the idle SMs it recovers; >= 4 stages (512 k) per split
-    const int64_t tiles = (int64_t)(mmq_rows_pad(rows) / 256) * ((m + 255) / 256);
+    const int BN = itq3_mmq_block_n(m);
+    const int64_t tiles = (int64_t)(mmq_rows_pad(rows) / 256) * ((m + BN - 1) / BN);
     const int64_t pairs = mmq_max_clusters();
     if (tiles * 2 > pairs) return 1;
     const int64_t NS = cols / kStK;
@@ -735,35 +738,35 @@ static int mmq_splits(int64_t rows, int64_t cols, int64_t m) {
     return (int)(ks < 1 ? 1 : ks);
 }
 
-template <typename TY>
+template <int BN, typename TY>
 static int launch_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym, const uint8_t* act, int64_t m, TY* y,
                       int64_t sr, int64_t sm_, float* ws, cudaStream_t s) {
     const int smem = (int)sizeof(PairSmem) + 1024;
     static bool attr = false, attr32 = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(mmq_pair_kernel<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        if (cudaFuncSetAttribute(mmq_pair_kernel<BN, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
             return check_launch("itq3_mmq: smem attribute");
         attr = true;
     }
     if (!attr32) {
-        if (cudaFuncSetAttribute(mmq_pair_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        if (cudaFuncSetAttribute(mmq_pair_kernel<BN, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
             cudaSuccess)
             return check_launch("itq3_mmq: smem attribute");
         attr32 = true;
     }
     PairWork wk;
     wk.tiles_r = mmq_rows_pad(rows) / 256;
-    wk.tiles_n = (int)((m + 255) / 256);
+    wk.tiles_n = (int)((m + BN - 1) / BN);
     wk.ks = ws ? mmq_splits(rows, cols, m) : 1;
     wk.NS = (int)(cols / kStK);
     const int64_t items = (int64_t)wk.tiles_r * wk.tiles_n * wk.ks;
     const int64_t clusters = items < mmq_max_clusters() ? items : mmq_max_clusters();
     const dim3 grid((unsigned)(2 * clusters));
     if (wk.ks == 1) {
-        mmq_pair_kernel<TY><<<grid, kMmqThreads, smem, s>>>(mmq, asym, wk, act, rows, m, y, sr, sm_, 0);
+        mmq_pair_kernel<BN, TY><<<grid, kMmqThreads, smem, s>>>(mmq, asym, wk, act, rows, m, y, sr, sm_, 0);
         return check_launch("itq3_mmq");
     }
-    mmq_pair_kernel<float><<<grid, kMmqThreads, smem, s>>>(mmq, asym, wk, act, rows, m, ws, m, 1, rows * m);
+    mmq_pair_kernel<BN, float><<<grid, kMmqThreads, smem, s>>>(mmq, asym, wk, act, rows, m, ws, m, 1, rows * m);
     int rc = check_launch("itq3_mmq (split-K)");
     if (rc) return rc;
     const int64_t n = rows * m;
@@ -789,9 +792,13 @@ extern "C" int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym
     }
     cudaStream_t s = (cudaStream_t)stream;
     float* ws = (float*)workspace;
-    if (y_dtype == ITQ3_F32) return launch_mmq(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, ws, s);
+    const bool n128 = itq3_mmq_block_n(m) == 128;
+    if (y_dtype == ITQ3_F32)
+        return n128 ? launch_mmq<128>(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, ws, s)
+                    : launch_mmq<256>(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, ws, s);
     if (y_dtype == ITQ3_BF16)
-        return launch_mmq(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s);
+        return n128 ? launch_mmq<128>(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s)
+                    : launch_mmq<256>(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s);
     set_error("itq3_mmq: output dtype must be float32 or bfloat16");
     return ITQ3_E_DOMAIN;
 }
