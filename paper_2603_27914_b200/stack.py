@@ -144,17 +144,37 @@ class LinearStack:
             self.capture()
         self.graph.replay()
 
+    def capture_host_step(self) -> None:
+        """One CUDA graph for a whole host-to-host step: H2D of the pinned input, the chain (or the
+        kernel sequence), D2H of the last stage into pinned memory -- a single launch per token."""
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(side):
+            self.x.copy_(self.host_in, non_blocking=True)
+            self.launch_all()  # warm-up outside capture
+            self.host_out.copy_(self.output(), non_blocking=True)
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.x.copy_(self.host_in, non_blocking=True)
+            self.launch_all()
+            self.host_out.copy_(self.output(), non_blocking=True)
+        self.host_graph = g
+
     def forward(self, x) -> np.ndarray:
-        """Host in -> host out: H2D of x, the graphed chain, D2H of the last stage's output."""
+        """Host in -> host out: H2D of x, the chain, D2H of the last stage's output, as ONE graph launch."""
         xt = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x, dtype=np.float32))
         if xt.numel() != self.x.numel():
             raise ShapeError(f"LinearStack.forward: expected {self.x.numel()} inputs, got {xt.numel()}")
         if xt.is_cuda:
             self.x.copy_(xt.reshape(-1))
+            self.replay()
+            self.host_out.copy_(self.output(), non_blocking=True)
         else:
+            if getattr(self, "host_graph", None) is None or self.graph is None:
+                self.replay()  # first use: capture the device-only graph too (stage outputs, epochs)
+                self.capture_host_step()
             self.host_in.copy_(xt.reshape(-1))
-            self.x.copy_(self.host_in, non_blocking=True)
-        self.replay()
-        self.host_out.copy_(self.output(), non_blocking=True)
+            self.host_graph.replay()
         torch.cuda.current_stream(self.dev).synchronize()
         return self.host_out.numpy()
