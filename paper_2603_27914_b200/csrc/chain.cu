@@ -392,7 +392,8 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     // fragments in registers for every unit; each unit's 16 per-warp partials are summed by the
     // last warp to finish it, in warp order (deterministic).
     const int g = lane >> 2, t = lane & 3;
-    int seq = 0;  // CTA-wide unit sequence number (ring slot = seq % kNumSlots)
+    int cs = 0;        // ring slot of the CTA's next unit
+    unsigned cp = 0;   // and its full-barrier phase parity
     uint8_t* rot = sm.rot[warp];
     const bool prof = trace != nullptr && cta == 0;
     long long c_wait = 0, c_tile = 0, c_rot = 0, c_in = 0, c_start = clock64();
@@ -442,11 +443,16 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             // warp's in-order issue stream (software pipelining across ring slots)
             for (int j = u0; j < u1; j += 2) {
                 const bool two = j + 1 < u1;
-                const int useq0 = seq + j, useq1 = seq + j + 1;
-                const int slot0 = useq0 % kNumSlots, slot1 = useq1 % kNumSlots;
+                // ring position of the two units, advanced incrementally (no division by the ring size)
+                const int slot0 = cs;
+                const unsigned ph0 = cp;
+                if (++cs == kNumSlots) cs = 0, cp ^= 1u;
+                const int slot1 = cs;
+                const unsigned ph1 = cp;
+                if (two && ++cs == kNumSlots) cs = 0, cp ^= 1u;
                 long long c1 = prof ? clock64() : 0;
-                mbar_wait(&sm.full[slot0], (unsigned)(useq0 / kNumSlots) & 1u);
-                if (two) mbar_wait(&sm.full[slot1], (unsigned)(useq1 / kNumSlots) & 1u);
+                mbar_wait(&sm.full[slot0], ph0);
+                if (two) mbar_wait(&sm.full[slot1], ph1);
                 if (prof) {
                     const long long c2 = clock64();
                     c_wait += c2 - c1;
@@ -466,13 +472,12 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                     rb.x += __shfl_xor_sync(FULL, rb.x, 2);
                     rb.y += __shfl_xor_sync(FULL, rb.y, 2);
                 }
-                if (t == 0) {
-                    sm.part[slot0][warp][g] = ra.x;
-                    sm.part[slot0][warp][g + 8] = ra.y;
-                    if (two) {
-                        sm.part[slot1][warp][g] = rb.x;
-                        sm.part[slot1][warp][g + 8] = rb.y;
-                    }
+                // every lane of a quad holds the quad's sums: all four store the same value (no branch)
+                sm.part[slot0][warp][g] = ra.x;
+                sm.part[slot0][warp][g + 8] = ra.y;
+                if (two) {
+                    sm.part[slot1][warp][g] = rb.x;
+                    sm.part[slot1][warp][g + 8] = rb.y;
                 }
                 __syncwarp();
                 if (prof) c_tile += clock64() - c1;
@@ -486,7 +491,6 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                 }
             }
         }
-        seq += n_units;
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 3] = globaltimer();
     }
     if (prof && lane == 0) {
