@@ -35,6 +35,27 @@
 
 namespace itq3 {
 
+// Programmatic dependent launch: the MMQ kernels are launched so that their prologue (TMEM
+// allocation, barrier init, weight-record fetch set-up) overlaps the activation rotation that
+// precedes them on the stream; the rotation kernels release their dependents at entry and the MMQ
+// producer waits (griddepcontrol.wait) before its first activation copy.
+template <typename Kern, typename... Args>
+static cudaError_t launch_pdl(Kern kernel, dim3 grid, dim3 block, int smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 constexpr int kMmqBM = 128;
 constexpr int kMmqExpGroups = 2;  // expander warp quads; group e decodes the chunks g with g % 2 == e
 constexpr int kMmqEpiWarp = 2 + 4 * kMmqExpGroups;
@@ -224,6 +245,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // producer: this CTA's weight record and 64-token half of B, one copy each per stage
+            pdl_wait();   // the activation rotation that precedes this launch has completed
             uint32_t g = 0;
             long long tw = 0, t_issue = 0;
             const long long tk0 = clock64();
@@ -546,6 +568,7 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
                                                              uint8_t* __restrict__ out) {
     // fp32 inputs, token-major (257: conflict-free transposes); after the butterflies the same bytes hold
     // the rotated f16 outputs as [32][264] (528-byte rows: 16-byte aligned, 4 wavefronts per 16-B warp load)
+    pdl_release();
     __shared__ __align__(16) float tile[32][257];
     __half(&th)[32][264] = *reinterpret_cast<__half(*)[32][264]>(&tile[0][0]);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -763,10 +786,12 @@ static int launch_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym, 
     const int64_t clusters = items < mmq_max_clusters() ? items : mmq_max_clusters();
     const dim3 grid((unsigned)(2 * clusters));
     if (wk.ks == 1) {
-        mmq_pair_kernel<BN, TY><<<grid, kMmqThreads, smem, s>>>(mmq, asym, wk, act, rows, m, y, sr, sm_, 0);
+        launch_pdl(mmq_pair_kernel<BN, TY>, grid, dim3(kMmqThreads), smem, s, mmq, asym, wk, act, rows, m, y, sr, sm_,
+                   (int64_t)0);
         return check_launch("itq3_mmq");
     }
-    mmq_pair_kernel<BN, float><<<grid, kMmqThreads, smem, s>>>(mmq, asym, wk, act, rows, m, ws, m, 1, rows * m);
+    launch_pdl(mmq_pair_kernel<BN, float>, grid, dim3(kMmqThreads), smem, s, mmq, asym, wk, act, rows, m, ws, m,
+               (int64_t)1, rows * m);
     int rc = check_launch("itq3_mmq (split-K)");
     if (rc) return rc;
     const int64_t n = rows * m;
@@ -884,6 +909,7 @@ __global__ void __launch_bounds__(kQ8Threads, 1)
 
     if (warp == 0) {
         if (lane == 0) {
+            pdl_wait();  // the activation rotation that precedes this launch has completed
             for (int i = 0; i < nblk; ++i) {
                 const int s = i % NS;
                 { MMQ_T0(); mbar_wait_(&sm.empty[s], ((unsigned)(i / NS) & 1u) ^ 1u); MMQ_ACC(0, c[0]); }
@@ -1077,6 +1103,7 @@ __global__ void repack_mmq8_kernel(const uint8_t* __restrict__ payload, int64_t 
 template <typename TX>
 __global__ void rotate_act_i8_kernel(const TX* __restrict__ x, int64_t NB, int64_t M, int64_t M_pad,
                                      int64_t stride_k, int64_t stride_m, int BN, uint8_t* __restrict__ out) {
+    pdl_release();
     const int lane = threadIdx.x & 31;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (wid >= NB * M_pad) return;
@@ -1236,7 +1263,7 @@ static int launch_mmq8(const uint8_t* w, int64_t rows, int64_t cols, const uint8
     const int ks = ws ? mmq8_splits(rows, cols, m) : 1;
     const dim3 grid((unsigned)((rows + 127) / 128), (unsigned)((m + BN - 1) / BN), (unsigned)ks);
     if (ks == 1) {
-        mmq8_kernel<BN, TY><<<grid, kQ8Threads, smem, s>>>(w, NB, act, rows, m, y, sr, sm_, 0);
+        launch_pdl(mmq8_kernel<BN, TY>, grid, dim3(kQ8Threads), smem, s, w, NB, act, rows, m, y, sr, sm_, (int64_t)0);
         return check_launch("itq3_mmq8");
     }
     if (!attr32) {
@@ -1245,7 +1272,8 @@ static int launch_mmq8(const uint8_t* w, int64_t rows, int64_t cols, const uint8
             return check_launch("itq3_mmq8: smem attribute");
         attr32 = true;
     }
-    mmq8_kernel<BN, float><<<grid, kQ8Threads, smem, s>>>(w, NB, act, rows, m, ws, m, 1, rows * m);
+    launch_pdl(mmq8_kernel<BN, float>, grid, dim3(kQ8Threads), smem, s, w, NB, act, rows, m, ws, m, (int64_t)1,
+               rows * m);
     int rc = check_launch("itq3_mmq8 (split-K)");
     if (rc) return rc;
     const int64_t n = rows * m;
