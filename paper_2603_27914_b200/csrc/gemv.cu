@@ -108,6 +108,7 @@ template <typename TX>
 __global__ void __launch_bounds__(256) rotate_act_kernel(const TX* __restrict__ x, int64_t NB, int64_t M,
                                                          int64_t stride_k, int64_t stride_m, int L, int tpp,
                                                          uint8_t* __restrict__ act, int64_t n_pass) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // let the GEMV launch (PDL)
     __shared__ __align__(16) uint8_t img[kActFragBytes];
     __shared__ double meta[8][2];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -227,6 +228,7 @@ __global__ void __launch_bounds__(32 * kGemvWarps) gemv_kernel(const uint8_t* __
     TiledPtrs P = tiled_ptrs(const_cast<uint8_t*>(tiled), RT, NB);
     const uint2* frag = reinterpret_cast<const uint2*>(act);
     const ACC* meta = MetaT<ACC>::base(act, n_pass, NB);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the rotation launched before this GEMV is done
 
     ACC acc[2][2] = {{ACC(0), ACC(0)}, {ACC(0), ACC(0)}};
     for (int64_t b = w; b < NB; b += kGemvWarps) {
@@ -466,16 +468,25 @@ extern "C" int itq3_gemv(const uint8_t* tiled, int64_t rows, int64_t cols, int a
     const int64_t n_pass = (m + tpp - 1) / tpp;
     const dim3 grid((unsigned)RT, (unsigned)n_pass), block(32 * kGemvWarps);
     cudaStream_t s = (cudaStream_t)stream;
+    // programmatic dependent launch: the GEMV's launch and prologue overlap the preceding rotation
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
     if (y_dtype == ITQ3_F32)
-        gemv_kernel<float, float><<<grid, block, 0, s>>>(tiled, rows, NB, RT, asymmetric, act, m, limbs, tpp,
-                                                         n_pass, (float*)y, stride_r, stride_m);
+        cudaLaunchKernelEx(&cfg, gemv_kernel<float, float>, tiled, rows, NB, RT, asymmetric, act, m, limbs, tpp, n_pass,
+                           (float*)y, stride_r, stride_m);
     else if (y_dtype == ITQ3_F64)
-        gemv_kernel<double, double><<<grid, block, 0, s>>>(tiled, rows, NB, RT, asymmetric, act, m, limbs, tpp,
-                                                           n_pass, (double*)y, stride_r, stride_m);
+        cudaLaunchKernelEx(&cfg, gemv_kernel<double, double>, tiled, rows, NB, RT, asymmetric, act, m, limbs, tpp,
+                           n_pass, (double*)y, stride_r, stride_m);
     else if (y_dtype == ITQ3_BF16)
-        gemv_kernel<float, __nv_bfloat16><<<grid, block, 0, s>>>(tiled, rows, NB, RT, asymmetric, act, m, limbs,
-                                                                 tpp, n_pass, (__nv_bfloat16*)y, stride_r,
-                                                                 stride_m);
+        cudaLaunchKernelEx(&cfg, gemv_kernel<float, __nv_bfloat16>, tiled, rows, NB, RT, asymmetric, act, m, limbs,
+                           tpp, n_pass, (__nv_bfloat16*)y, stride_r, stride_m);
     else {
         set_error("itq3_gemv: output dtype must be float32, float64 or bfloat16");
         return ITQ3_E_DOMAIN;
