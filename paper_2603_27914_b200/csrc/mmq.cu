@@ -197,29 +197,47 @@ struct PairSmem {
 };
 
 // Work item = (split, token tile, pair row tile); every role walks the same sequence.
+// Tail split: items [F, F + R * kt) are the last R tiles (the final partial round of the persistent
+// grid) split kt ways along K; they write fp32 partials to the workspace, summed by mmq_tail_reduce.
 struct PairWork {
     int tiles_r, tiles_n, ks, NS;  // NS = stages along K
-    __device__ void decode(int it, int& tr, int& tn, int& s0, int& s1) const {
-        const int per = tiles_r * tiles_n;
-        const int sp = it / per, rem = it % per;
-        tn = rem / tiles_r;
-        tr = rem % tiles_r;
-        s0 = (int)((int64_t)sp * NS / ks);
-        s1 = (int)((int64_t)(sp + 1) * NS / ks);
+    int F, R, kt;                  // tail split (kt = 1: none)
+    __device__ int items() const { return F + R * kt; }
+    // split = -1 for an item written straight to Y
+    __device__ void decode(int it, int& tr, int& tn, int& s0, int& s1, int& split) const {
+        int T, sp, n;
+        if (it < F) {
+            const int per = tiles_r * tiles_n;
+            sp = it / per;
+            T = it % per;
+            n = ks;
+            split = ks > 1 ? sp : -1;
+        } else {
+            const int j = it - F;
+            T = F + j / kt;
+            sp = j % kt;
+            n = kt;
+            split = sp;
+        }
+        tn = T / tiles_r;
+        tr = T % tiles_r;
+        s0 = (int)((int64_t)sp * NS / n);
+        s1 = (int)((int64_t)(sp + 1) * NS / n);
     }
 };
 
 template <int BN, typename TY>  // BN = tokens per pair tile (256, or 128 for M <= 128)
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
     mmq_pair_kernel(const uint8_t* __restrict__ wrec, int asym, PairWork wk, const uint8_t* __restrict__ act,
-                    int64_t rows, int64_t M, TY* __restrict__ y, int64_t stride_r, int64_t stride_m, int64_t slab) {
+                    int64_t rows, int64_t M, TY* __restrict__ y, int64_t stride_r, int64_t stride_m, int64_t slab,
+                    float* __restrict__ tailws) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     PairSmem& sm = *reinterpret_cast<PairSmem*>(base);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cta_rank_in_cluster();
     const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
-    const int items = wk.tiles_r * wk.tiles_n * wk.ks;
+    const int items = wk.items();
     constexpr uint32_t kColA = 256;
 
     if (threadIdx.x == 0) {
@@ -250,8 +268,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
             long long tw = 0, t_issue = 0;
             const long long tk0 = clock64();
             for (int it = cluster; it < items; it += nclusters) {
-                int tr, tn, s0, s1;
-                wk.decode(it, tr, tn, s0, s1);
+                int tr, tn, s0, s1, split;
+                wk.decode(it, tr, tn, s0, s1, split);
                 const uint8_t* wsrc = wrec + ((int64_t)(2 * tr + rank) * wk.NS) * kWRec;
                 const uint8_t* bsrc = act + ((int64_t)(2 * tn + rank) * wk.NS) * (BN * 128);
                 for (int st = s0; st < s1; ++st, ++g) {
@@ -283,8 +301,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
             long long tw_ready = 0, tw_d = 0;
             const long long tm0 = clock64();
             for (int it = cluster; it < items; it += nclusters, ++t) {
-                int tr, tn, s0, s1;
-                wk.decode(it, tr, tn, s0, s1);
+                int tr, tn, s0, s1, split;
+                wk.decode(it, tr, tn, s0, s1, split);
                 {
                     MMQ_T0();
                     mbar_wait_(&sm.dempty, (t & 1u) ^ 1u);
@@ -332,8 +350,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
         uint32_t g = 0;
         long long tw_full = 0, t_work = 0, tw_aempty = 0;
         for (int it = cluster; it < items; it += nclusters) {
-            int tr, tn, s0, s1;
-            wk.decode(it, tr, tn, s0, s1);
+            int tr, tn, s0, s1, split;
+            wk.decode(it, tr, tn, s0, s1, split);
             for (int st = s0; st < s1; ++st, ++g) {
                 if ((int)(g % kMmqExpGroups) != eg) continue;
                 const int s = g % kPairNS, sa = s;
@@ -404,8 +422,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
         long long tw_dfull = 0;
         const long long te0 = clock64();
         for (int it = cluster; it < items; it += nclusters, ++t) {
-            int tr, tn, s0, s1;
-            wk.decode(it, tr, tn, s0, s1);
+            int tr, tn, s0, s1, split;
+            wk.decode(it, tr, tn, s0, s1, split);
             {
                 MMQ_T0();
                 mbar_wait_(&sm.dfull, t & 1u);
@@ -414,12 +432,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const int64_t grow = (int64_t)tr * 256 + rank * kMmqBM + r;
             TY* yt = y + (int64_t)(it / (wk.tiles_r * wk.tiles_n)) * slab;
-            const bool live = grow < rows;
+            const bool tail = it >= wk.F;  // tail-split partial: fp32 tile in the workspace
+            const bool live = tail || grow < rows;
             const uint32_t sa = smem_addr(sm.stage[r]);
 #pragma unroll 1
             for (int h = 0; h < BN / 128; ++h) {
                 const int64_t m0 = (int64_t)tn * BN + 128 * h;
-                const bool bulk = live && bulk_ok && m0 + 128 <= M;
+                const bool bulk = live && !tail && bulk_ok && m0 + 128 <= M;
                 // the previous bulk store has finished reading the staging row
                 if (bulk) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 #pragma unroll
@@ -458,6 +477,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
                                 sts128(sa + 2u * (32 * c + j), make_uint4(p[0], p[1], p[2], p[3]));
                             }
                         }
+                    } else if (tail) {
+                        float* pt = tailws + ((int64_t)(split * wk.R + (tr + tn * wk.tiles_r - wk.F)) * 256 +
+                                              rank * kMmqBM + r) * BN + 128 * h + 32 * c;
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4)
+                            *reinterpret_cast<uint4*>(pt + j) = make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                     } else if (live) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
@@ -646,6 +671,23 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
     }
 }
 
+// Sum the kt fp32 partials of the R tail tiles (fixed split order) into Y.
+template <typename TY>
+__global__ void mmq_tail_reduce(const float* __restrict__ tws, int F, int R, int kt, int tiles_r, int BN, int64_t rows,
+                                int64_t M, TY* __restrict__ y, int64_t stride_r, int64_t stride_m) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per = (int64_t)256 * BN;
+    if (i >= (int64_t)R * per) return;
+    const int tl = (int)(i / per);
+    const int lr = (int)((i % per) / BN), lc = (int)(i % BN);
+    const int T = F + tl;
+    const int64_t row = (int64_t)(T % tiles_r) * 256 + lr, m = (int64_t)(T / tiles_r) * BN + lc;
+    if (row >= rows || m >= M) return;
+    float v = tws[((int64_t)tl * 256 + lr) * BN + lc];
+    for (int sp = 1; sp < kt; ++sp) v += tws[(((int64_t)sp * R + tl) * 256 + lr) * BN + lc];
+    y[row * stride_r + m * stride_m] = (TY)v;
+}
+
 template <typename TY>
 __global__ void mmq_splitk_reduce(const float* __restrict__ ws, int ks, int64_t rows, int64_t M, TY* __restrict__ y,
                                   int64_t stride_r, int64_t stride_m) {
@@ -761,6 +803,23 @@ static int mmq_splits(int64_t rows, int64_t cols, int64_t m) {
     return (int)(ks < 1 ? 1 : ks);
 }
 
+// The last partial round of R tiles (R <= P / 2) is split kt = min(P / R, NS / 4) ways along K so the
+// final wave keeps the pairs busy; F = tiles - R are processed whole.
+static void mmq_tail_plan(int64_t tiles, int NS, int P, bool allowed, int& F, int& R, int& kt) {
+    F = (int)tiles;
+    R = 0;
+    kt = 1;
+    if (!allowed || tiles <= P) return;
+    const int r = (int)(tiles % P);
+    if (r == 0 || 2 * r > P) return;
+    int k = P / r;
+    if (k > NS / 4) k = NS / 4;
+    if (k < 2) return;
+    F = (int)(tiles - r);
+    R = r;
+    kt = k;
+}
+
 template <int BN, typename TY>
 static int launch_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym, const uint8_t* act, int64_t m, TY* y,
                       int64_t sr, int64_t sm_, float* ws, cudaStream_t s) {
@@ -782,20 +841,34 @@ static int launch_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym, 
     wk.tiles_n = (int)((m + BN - 1) / BN);
     wk.ks = ws ? mmq_splits(rows, cols, m) : 1;
     wk.NS = (int)(cols / kStK);
-    const int64_t items = (int64_t)wk.tiles_r * wk.tiles_n * wk.ks;
-    const int64_t clusters = items < mmq_max_clusters() ? items : mmq_max_clusters();
+    const int64_t tiles = (int64_t)wk.tiles_r * wk.tiles_n;
+    const int P = mmq_max_clusters();
+    mmq_tail_plan(tiles, wk.NS, P, ws != nullptr && wk.ks == 1, wk.F, wk.R, wk.kt);
+    if (wk.ks > 1) {  // underfilled grid: every tile split ks ways (slabs [ks][rows][M])
+        wk.F = (int)(tiles * wk.ks);
+        wk.R = 0;
+        wk.kt = 1;
+    }
+    const int64_t items = (int64_t)wk.F + (int64_t)wk.R * wk.kt;
+    const int64_t clusters = items < P ? items : P;
     const dim3 grid((unsigned)(2 * clusters));
+    float* tws = reinterpret_cast<float*>(ws);
     if (wk.ks == 1) {
         launch_pdl(mmq_pair_kernel<BN, TY>, grid, dim3(kMmqThreads), smem, s, mmq, asym, wk, act, rows, m, y, sr, sm_,
-                   (int64_t)0);
-        return check_launch("itq3_mmq");
+                   (int64_t)0, tws);
+        int rc = check_launch("itq3_mmq");
+        if (rc || wk.R == 0) return rc;
+        const int64_t n = (int64_t)wk.R * 256 * BN;
+        mmq_tail_reduce<TY><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(tws, wk.F, wk.R, wk.kt, wk.tiles_r, BN, rows, m,
+                                                                      y, sr, sm_);
+        return check_launch("itq3_mmq (tail reduce)");
     }
-    launch_pdl(mmq_pair_kernel<BN, float>, grid, dim3(kMmqThreads), smem, s, mmq, asym, wk, act, rows, m, ws, m,
-               (int64_t)1, rows * m);
+    launch_pdl(mmq_pair_kernel<BN, float>, grid, dim3(kMmqThreads), smem, s, mmq, asym, wk, act, rows, m, tws, m,
+               (int64_t)1, rows * m, tws);
     int rc = check_launch("itq3_mmq (split-K)");
     if (rc) return rc;
     const int64_t n = rows * m;
-    mmq_splitk_reduce<TY><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ws, wk.ks, rows, m, y, sr, sm_);
+    mmq_splitk_reduce<TY><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(tws, wk.ks, rows, m, y, sr, sm_);
     return check_launch("itq3_mmq (split-K reduce)");
 }
 
@@ -806,7 +879,12 @@ extern "C" int itq3_mmq_set_trace(void* buf) {
 
 extern "C" int64_t itq3_mmq_ws_nbytes(int64_t rows, int64_t cols, int64_t m) {
     const int ks = mmq_splits(rows, cols, m);
-    return ks > 1 ? (int64_t)ks * rows * m * (int64_t)sizeof(float) : 0;
+    if (ks > 1) return (int64_t)ks * rows * m * (int64_t)sizeof(float);
+    const int BN = itq3_mmq_block_n(m);
+    int F, R, kt;
+    mmq_tail_plan((int64_t)(mmq_rows_pad(rows) / 256) * ((m + BN - 1) / BN), (int)(cols / kStK), mmq_max_clusters(), true,
+                  F, R, kt);
+    return R ? (int64_t)R * kt * 256 * BN * (int64_t)sizeof(float) : 0;
 }
 
 extern "C" int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asymmetric, const uint8_t* act, int64_t m,

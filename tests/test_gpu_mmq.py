@@ -72,10 +72,11 @@ def test_mmq_dtypes_and_strides():
     torch.testing.assert_close(Y, Y2, rtol=0, atol=0)
 
 
-@pytest.mark.parametrize("rows,cols,m", [(8192, 1024, 640), (4352, 512, 257), (2304, 768, 1030)])
+@pytest.mark.parametrize("rows,cols,m", [(8192, 1024, 640), (4352, 512, 257), (2304, 768, 1030), (19200, 1024, 200)])
 def test_mmq_persistent_pairs(rows, cols, m):
-    """More (256-row x 128-token) pair tiles than co-resident CTA pairs: every pair walks several
-    tiles and alternates its two TMEM accumulators; ragged token tails take the plain-store path
+    """More pair tiles than co-resident CTA pairs: every pair walks several tiles; the final partial
+    round is split along K into workspace partials (8192 x 1024 x 640: 96 tiles; 19200 x 1024: 75
+    tiles = one full round + 1 tile split 2 ways); ragged token tails take the plain-store path
     (m = 257: rows not 16-byte aligned, so no bulk row stores at all)."""
     rng = np.random.default_rng(rows + m)
     w = rng.standard_normal((rows, cols)) * 0.05
