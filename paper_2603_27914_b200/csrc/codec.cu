@@ -131,12 +131,24 @@ __global__ void __launch_bounds__(32 * kEncWarps) encode_kernel(const TIn* __res
         }
     }
 
-    // ternary_quantize (quantizer.py:156-168) and pack_ternary (packing.py:59-64)
+    // ternary_quantize (quantizer.py:156-168) and pack_ternary (packing.py:59-64).
+    // code = clip(round_half_away(fl(y / d)) + z, -1, 1) only depends on which side of 0.5 and 1.5
+    // |fl(y / d)| falls, so a multiply by fl(1 / d) (within 2^-50 of the quotient for |q| <= 2)
+    // decides every element farther than 2^-40 from those two points; the rest (and the SS
+    // variant, whose scale varies per element) take the correctly rounded division.
     uint32_t c[E];
+    const double inv = ss ? 0.0 : __drcp_rn(deff_e[0]);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-        const double q = __ddiv_rn(v[e], deff_e[e]);
-        const double code = clip1(__dadd_rn(round_half_away(q), z));
+        const double a = fabs(v[e]) * inv;
+        double code;
+        if (!ss && fabs(a - 0.5) > 0x1p-40 && fabs(a - 1.5) > 0x1p-40) {
+            const double rr = a >= 1.5 ? 2.0 : (a >= 0.5 ? 1.0 : 0.0);
+            code = clip1(__dadd_rn(copysign(rr, v[e]), z));
+        } else {
+            const double q = __ddiv_rn(v[e], deff_e[e]);
+            code = clip1(__dadd_rn(round_half_away(q), z));
+        }
         c[e] = (uint32_t)((int)code + 1);
     }
 #pragma unroll

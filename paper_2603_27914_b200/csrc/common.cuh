@@ -148,17 +148,22 @@ __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+// p + sg * v with sg = +-1: the product is exact, so this is v + p (sg = 1) or p - v (sg = -1) with ONE
+// rounding -- bit-identical to add_rn / sub_rn (signed zeros included), one instruction instead of
+// two adds and a select
+__device__ __forceinline__ double pm_rn(double sg, double v, double p) { return __fma_rn(sg, v, p); }
+__device__ __forceinline__ float pm_rn(float sg, float v, float p) { return __fmaf_rn(sg, v, p); }
 
 // Unnormalised butterfly over N = 32*E elements held in stride layout.
 template <int E, typename T>
 __device__ __forceinline__ void warp_butterfly(T (&v)[E], int lane) {
 #pragma unroll
     for (int h = 1; h < 32 && h < 32 * E; h <<= 1) {
-        const bool high = (lane & h) != 0;
+        const T sg = (lane & h) ? T(-1) : T(1);  // high lane: lo - hi = p - v
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const T p = __shfl_xor_sync(FULL, v[e], h);
-            v[e] = high ? sub_rn(p, v[e]) : add_rn(v[e], p);  // high lane: lo - hi
+            v[e] = pm_rn(sg, v[e], p);
         }
     }
 #pragma unroll
