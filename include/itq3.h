@@ -110,8 +110,10 @@ int64_t itq3_mmq_nbytes(int64_t rows, int64_t cols, int asymmetric);
 int itq3_repack_mmq(const uint8_t* payload, int64_t rows, int64_t cols, int asymmetric, uint8_t* out, void* stream);
 int itq3_mmq_block_n(int64_t m);
 int64_t itq3_mmq_act_nbytes(int64_t cols, int64_t m);
+/* nonfinite (nullable device u32): OR-ed with 1 if any input element is not finite -- fused_matmul's
+ * DomainError check without a separate pass over X; the caller zeroes it before and reads it after. */
 int itq3_rotate_act_f16(const void* x, int x_dtype, int64_t cols, int64_t m, int64_t stride_k, int64_t stride_m,
-                        uint8_t* out, void* stream);
+                        uint8_t* out, unsigned* nonfinite, void* stream);
 /* workspace: itq3_mmq_ws_nbytes(rows, cols, m) bytes (may be 0 -> pass NULL); with a workspace,
  * small problems are split along K across CTAs and reduced in fixed order (deterministic). */
 int64_t itq3_mmq_ws_nbytes(int64_t rows, int64_t cols, int64_t m);
@@ -148,7 +150,7 @@ int64_t itq3_mmq8_nbytes(int64_t rows, int64_t cols);
 int itq3_repack_mmq8(const uint8_t* payload, int64_t rows, int64_t cols, int asymmetric, uint8_t* out, void* stream);
 int64_t itq3_mmq8_act_nbytes(int64_t cols, int64_t m);
 int itq3_rotate_act_i8(const void* x, int x_dtype, int64_t cols, int64_t m, int64_t stride_k, int64_t stride_m,
-                       uint8_t* out, void* stream);
+                       uint8_t* out, unsigned* nonfinite, void* stream);
 int64_t itq3_mmq8_ws_nbytes(int64_t rows, int64_t cols, int64_t m);
 int itq3_mmq8(const uint8_t* w, int64_t rows, int64_t cols, const uint8_t* act, int64_t m, void* y, int y_dtype,
               int64_t stride_r, int64_t stride_m, void* workspace, void* stream);

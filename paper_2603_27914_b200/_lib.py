@@ -47,7 +47,7 @@ SIGNATURES = {
     "itq3_repack_mmq": (_i32, [_vp, _i64, _i64, _i32, _vp, _vp]),
     "itq3_mmq_block_n": (_i32, [_i64]),
     "itq3_mmq_act_nbytes": (_i64, [_i64, _i64]),
-    "itq3_rotate_act_f16": (_i32, [_vp, _i32, _i64, _i64, _i64, _i64, _vp, _vp]),
+    "itq3_rotate_act_f16": (_i32, [_vp, _i32, _i64, _i64, _i64, _i64, _vp, _vp, _vp]),
     "itq3_mmq_ws_nbytes": (_i64, [_i64, _i64, _i64]),
     "itq3_mmq_set_trace": (_i32, [_vp]),
     "itq3_dequant_set_trace": (_i32, [_vp]),
@@ -58,7 +58,7 @@ SIGNATURES = {
     "itq3_mmq8_nbytes": (_i64, [_i64, _i64]),
     "itq3_repack_mmq8": (_i32, [_vp, _i64, _i64, _i32, _vp, _vp]),
     "itq3_mmq8_act_nbytes": (_i64, [_i64, _i64]),
-    "itq3_rotate_act_i8": (_i32, [_vp, _i32, _i64, _i64, _i64, _i64, _vp, _vp]),
+    "itq3_rotate_act_i8": (_i32, [_vp, _i32, _i64, _i64, _i64, _i64, _vp, _vp, _vp]),
     "itq3_mmq8_ws_nbytes": (_i64, [_i64, _i64, _i64]),
     "itq3_mmq8": (_i32, [_vp, _i64, _i64, _vp, _i64, _vp, _i32, _i64, _i64, _vp, _vp]),
     "itq3_chain_desc_nbytes": (_i64, []),

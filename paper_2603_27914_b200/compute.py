@@ -27,6 +27,24 @@ MMQ_MIN_TOKENS = 16  # perf mode: k >= 16 columns go to the tcgen05 MMQ kernels 
 MMQ8_MAX_TOKENS = 64  # ... 16 <= k <= 64 to the kind::i8 one (K5b), larger k to the kind::f16 one (K5)
 
 
+_NONFINITE: dict = {}
+
+
+def _nonfinite_flag(dev: torch.device) -> torch.Tensor:
+    """Per-device u32 flag the MMQ activation rotations OR with 1 on a non-finite input (kept zero)."""
+    f = _NONFINITE.get(dev)
+    if f is None:
+        f = torch.zeros(1, dtype=torch.int32, device=dev)
+        _NONFINITE[dev] = f
+    return f
+
+
+def _raise_if_nonfinite(flag: torch.Tensor) -> None:
+    if int(flag.item()):
+        flag.zero_()
+        raise DomainError("fused_matmul: X contains non-finite values")
+
+
 def perf_limbs(m: int) -> int:
     return 3 if m == 1 else 2
 
@@ -85,27 +103,31 @@ def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, 
         lib = _lib.load()
         s = _lib.stream_ptr(dev)
         act = torch.empty(lib.itq3_mmq8_act_nbytes(cols, k), dtype=torch.uint8, device=dev)
+        flag = _nonfinite_flag(dev)
         _lib.call("itq3_rotate_act_i8", _lib.ptr(X), _lib.TORCH_DTYPE_CODE[X.dtype], cols, k, X.stride(0),
-                  X.stride(1), _lib.ptr(act), s)
+                  X.stride(1), _lib.ptr(act), _lib.ptr(flag), s)
         Y = torch.empty((rows, k), dtype=out_dtype, device=dev)
         wsn = lib.itq3_mmq8_ws_nbytes(rows, cols, k)
         ws = torch.empty(wsn, dtype=torch.uint8, device=dev) if wsn else None
         _lib.call("itq3_mmq8", _lib.ptr(q.mmq8_layout()), rows, cols, _lib.ptr(act), k, _lib.ptr(Y),
                   _lib.TORCH_DTYPE_CODE[out_dtype], Y.stride(0), Y.stride(1), _lib.ptr(ws) if ws is not None else None,
                   s)
+        _raise_if_nonfinite(flag)
         return Y
     if q.fast_layout() and out_dtype != torch.float64 and k >= MMQ_MIN_TOKENS:
         mmq = q.mmq_layout()
         s = _lib.stream_ptr(dev)
         act = torch.empty(_lib.load().itq3_mmq_act_nbytes(cols, k), dtype=torch.uint8, device=dev)
+        flag = _nonfinite_flag(dev)
         _lib.call("itq3_rotate_act_f16", _lib.ptr(X), _lib.TORCH_DTYPE_CODE[X.dtype], cols, k, X.stride(0),
-                  X.stride(1), _lib.ptr(act), s)
+                  X.stride(1), _lib.ptr(act), _lib.ptr(flag), s)
         Y = torch.empty((rows, k), dtype=out_dtype, device=dev)
         wsn = _lib.load().itq3_mmq_ws_nbytes(rows, cols, k)
         ws = torch.empty(wsn, dtype=torch.uint8, device=dev) if wsn else None
         _lib.call("itq3_mmq", _lib.ptr(mmq), rows, cols, int(not q.symmetric), _lib.ptr(act), k, _lib.ptr(Y),
                   _lib.TORCH_DTYPE_CODE[out_dtype], Y.stride(0), Y.stride(1), _lib.ptr(ws) if ws is not None else None,
                   s)
+        _raise_if_nonfinite(flag)
         return Y
     if q.fast_layout():
         tiled = q.tiled()
@@ -135,9 +157,11 @@ def fused_matmul(q: QuantizedTensor, x, *, limbs: int | None = None):
             raise ShapeError(f"fused_matmul: X has {x.shape[0]} rows, tensor has {q.cols} columns")
         if x.dtype not in _lib.TORCH_DTYPE_CODE:
             x = x.to(torch.float32)
-        if not bool(torch.isfinite(x).all()):
-            raise DomainError("fused_matmul: X contains non-finite values")
         parity = x.dtype == torch.float64
+        # the MMQ paths (k >= 16, perf mode) check finiteness inside their activation rotation
+        if parity or x.shape[1] < MMQ_MIN_TOKENS or not q.fast_layout():
+            if not bool(torch.isfinite(x).all()):
+                raise DomainError("fused_matmul: X contains non-finite values")
         L = limbs or (PARITY_LIMBS if parity else perf_limbs(x.shape[1]))
         return _matmul_device(q, x, torch.float64 if parity else torch.float32, L)
     a = np.asarray(x, dtype=np.float64)

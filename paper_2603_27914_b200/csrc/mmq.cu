@@ -590,7 +590,7 @@ __device__ __forceinline__ void load4(const __nv_bfloat16* p, float (&f)[4]) {
 template <typename TX>
 __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restrict__ x, int64_t M, int64_t stride_k,
                                                              int64_t stride_m, int64_t NC, int BN,
-                                                             uint8_t* __restrict__ out) {
+                                                             uint8_t* __restrict__ out, unsigned* __restrict__ nonfinite) {
     // fp32 inputs, token-major (257: conflict-free transposes); after the butterflies the same bytes hold
     // the rotated f16 outputs as [32][264] (528-byte rows: 16-byte aligned, 4 wavefronts per 16-B warp load)
     pdl_release();
@@ -626,10 +626,16 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
     }
     __syncthreads();
     float v[4][8];  // the warp's 4 tokens: lane holds k = lane + 32 e
+    bool bad = false;
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) v[jj][e] = tile[4 * warp + jj][lane + 32 * e];
+        for (int e = 0; e < 8; ++e) {
+            v[jj][e] = tile[4 * warp + jj][lane + 32 * e];
+            bad |= !isfinite(v[jj][e]);
+        }
+    // fused_matmul's DomainError check (compute.py): one flag word, set if any input is not finite
+    if (nonfinite && __any_sync(FULL, bad) && lane == 0) atomicOr(nonfinite, 1u);
     __syncthreads();  // the f16 outputs overwrite the fp32 tile
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj) {
@@ -733,7 +739,7 @@ extern "C" int64_t itq3_mmq_act_nbytes(int64_t cols, int64_t m) {
 }
 
 extern "C" int itq3_rotate_act_f16(const void* x, int x_dtype, int64_t cols, int64_t m, int64_t stride_k,
-                                   int64_t stride_m, uint8_t* out, void* stream) {
+                                   int64_t stride_m, uint8_t* out, unsigned* nonfinite, void* stream) {
     if (cols <= 0 || cols % 256 || m <= 0) {
         set_error("itq3_rotate_act_f16: need cols %% 256 == 0 and m > 0");
         return ITQ3_E_SHAPE;
@@ -744,17 +750,20 @@ extern "C" int itq3_rotate_act_f16(const void* x, int x_dtype, int64_t cols, int
     cudaStream_t s = (cudaStream_t)stream;
     switch (x_dtype) {
         case ITQ3_F32:
-            rotate_act_f16_kernel<float><<<grid, 256, 0, s>>>((const float*)x, m, stride_k, stride_m, NB * 4, BN, out);
+            rotate_act_f16_kernel<float><<<grid, 256, 0, s>>>((const float*)x, m, stride_k, stride_m, NB * 4, BN, out,
+                                                             nonfinite);
             break;
         case ITQ3_F64:
-            rotate_act_f16_kernel<double><<<grid, 256, 0, s>>>((const double*)x, m, stride_k, stride_m, NB * 4, BN, out);
+            rotate_act_f16_kernel<double><<<grid, 256, 0, s>>>((const double*)x, m, stride_k, stride_m, NB * 4, BN, out,
+                                                             nonfinite);
             break;
         case ITQ3_BF16:
             rotate_act_f16_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, m, stride_k, stride_m,
-                                                                      NB * 4, BN, out);
+                                                                      NB * 4, BN, out, nonfinite);
             break;
         case ITQ3_F16:
-            rotate_act_f16_kernel<__half><<<grid, 256, 0, s>>>((const __half*)x, m, stride_k, stride_m, NB * 4, BN, out);
+            rotate_act_f16_kernel<__half><<<grid, 256, 0, s>>>((const __half*)x, m, stride_k, stride_m, NB * 4, BN, out,
+                                                             nonfinite);
             break;
         default:
             set_error("itq3_rotate_act_f16: unsupported dtype %d", x_dtype);
@@ -1180,7 +1189,8 @@ __global__ void repack_mmq8_kernel(const uint8_t* __restrict__ payload, int64_t 
 // per (block, token); the chain kernel's integer rotation with |q| <= 2^14 (two balanced limbs).
 template <typename TX>
 __global__ void rotate_act_i8_kernel(const TX* __restrict__ x, int64_t NB, int64_t M, int64_t M_pad,
-                                     int64_t stride_k, int64_t stride_m, int BN, uint8_t* __restrict__ out) {
+                                     int64_t stride_k, int64_t stride_m, int BN, uint8_t* __restrict__ out,
+                                     unsigned* __restrict__ nonfinite) {
     pdl_release();
     const int lane = threadIdx.x & 31;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1195,6 +1205,10 @@ __global__ void rotate_act_i8_kernel(const TX* __restrict__ x, int64_t NB, int64
         float f[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) f[e] = (float)x[(b * 256 + lane + 32 * e) * stride_k + m * stride_m];
+        bool bad = false;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) bad |= !isfinite(f[e]);
+        if (nonfinite && __any_sync(FULL, bad) && lane == 0) atomicOr(nonfinite, 1u);
         unsigned fb = 0;
 #pragma unroll
         for (int e = 0; e < 8; ++e) fb = max(fb, __float_as_uint(fabsf(f[e])));
@@ -1285,7 +1299,7 @@ extern "C" int64_t itq3_mmq8_act_nbytes(int64_t cols, int64_t m) {
 }
 
 extern "C" int itq3_rotate_act_i8(const void* x, int x_dtype, int64_t cols, int64_t m, int64_t stride_k,
-                                  int64_t stride_m, uint8_t* out, void* stream) {
+                                  int64_t stride_m, uint8_t* out, unsigned* nonfinite, void* stream) {
     if (cols <= 0 || cols % 256 || m <= 0 || m > 64) {
         set_error("itq3_rotate_act_i8: need cols %% 256 == 0 and 0 < m <= 64");
         return ITQ3_E_SHAPE;
@@ -1296,15 +1310,15 @@ extern "C" int itq3_rotate_act_i8(const void* x, int x_dtype, int64_t cols, int6
     cudaStream_t s = (cudaStream_t)stream;
     switch (x_dtype) {
         case ITQ3_F32:
-            rotate_act_i8_kernel<float><<<grid, 256, 0, s>>>((const float*)x, NB, m, M_pad, stride_k, stride_m, BN, out);
+            rotate_act_i8_kernel<float><<<grid, 256, 0, s>>>((const float*)x, NB, m, M_pad, stride_k, stride_m, BN, out, nonfinite);
             break;
         case ITQ3_BF16:
             rotate_act_i8_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, NB, m, M_pad, stride_k,
-                                                                     stride_m, BN, out);
+                                                                     stride_m, BN, out, nonfinite);
             break;
         case ITQ3_F16:
             rotate_act_i8_kernel<__half><<<grid, 256, 0, s>>>((const __half*)x, NB, m, M_pad, stride_k, stride_m, BN,
-                                                              out);
+                                                              out, nonfinite);
             break;
         default:
             set_error("itq3_rotate_act_i8: unsupported dtype %d", x_dtype);

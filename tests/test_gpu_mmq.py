@@ -95,3 +95,19 @@ def test_mmq_bf16_output_matches_fp32():
     y16 = P.compute._matmul_device(q, X, torch.bfloat16, P.compute.perf_limbs(384))
     assert y16.dtype == torch.bfloat16
     torch.testing.assert_close(y16, y32.to(torch.bfloat16), rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("m", [16, 64, 200])
+@pytest.mark.parametrize("bad", [float("nan"), float("inf")])
+def test_mmq_nonfinite_input_raises(m, bad):
+    """The batched paths check X for non-finite values inside their activation rotation (no separate
+    pass): same DomainError as the reference, and the device flag is left clear for the next call."""
+    rng = np.random.default_rng(m)
+    q = P.quantize_tensor(rng.standard_normal((256, 512)) * 0.1)
+    X = torch.from_numpy(rng.standard_normal((512, m)).astype(np.float32)).cuda()
+    X[300, m - 1] = bad
+    with pytest.raises(P.DomainError, match="non-finite"):
+        P.fused_matmul(q, X)
+    X[300, m - 1] = 0.0
+    Y = P.fused_matmul(q, X)  # clean call afterwards
+    assert torch.isfinite(Y).all()

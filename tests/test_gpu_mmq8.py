@@ -26,7 +26,7 @@ def run_mmq8(q, X, out_dtype=torch.float32):
     act = torch.empty(lib.itq3_mmq8_act_nbytes(cols, M), dtype=torch.uint8, device=dev)
     s = _lib.stream_ptr(dev)
     _lib.call("itq3_rotate_act_i8", _lib.ptr(X), _lib.TORCH_DTYPE_CODE[X.dtype], cols, M, X.stride(0), X.stride(1),
-              _lib.ptr(act), s)
+              _lib.ptr(act), None, s)
     Y = torch.empty((rows, M), dtype=out_dtype, device=dev)
     wsn = lib.itq3_mmq8_ws_nbytes(rows, cols, M)
     ws = torch.empty(max(wsn, 1), dtype=torch.uint8, device=dev)

@@ -73,7 +73,7 @@ def main():
             def mmqf(i):
                 s = _lib.stream_ptr(dev)
                 _lib.call("itq3_rotate_act_f16", _lib.ptr(X), _lib.F32, K, M, X.stride(0), X.stride(1),
-                          _lib.ptr(actf), s)
+                          _lib.ptr(actf), None, s)
                 _lib.call("itq3_mmq", _lib.ptr(mmq[i % ncopy]), rows, K, 0, _lib.ptr(actf), M, _lib.ptr(Y), _lib.F32,
                           Y.stride(0), Y.stride(1), _lib.ptr(ws) if wsn else None, s)
 
@@ -83,7 +83,7 @@ def main():
 
             def mmq8f(i):
                 s = _lib.stream_ptr(dev)
-                _lib.call("itq3_rotate_act_i8", _lib.ptr(X), _lib.F32, K, M, X.stride(0), X.stride(1), _lib.ptr(act8), s)
+                _lib.call("itq3_rotate_act_i8", _lib.ptr(X), _lib.F32, K, M, X.stride(0), X.stride(1), _lib.ptr(act8), None, s)
                 _lib.call("itq3_mmq8", _lib.ptr(mmq8[i % ncopy]), rows, K, _lib.ptr(act8), M, _lib.ptr(Y), _lib.F32,
                           Y.stride(0), Y.stride(1), _lib.ptr(ws8) if ws8n else None, s)
 

@@ -11,7 +11,7 @@ q=P.quantize_tensor(w)
 X=torch.randn((cols,M),generator=g,device='cuda')
 BN=16; N=32
 act=torch.empty(lib.itq3_mmq8_act_nbytes(cols,M),dtype=torch.uint8,device='cuda')
-_lib.call("itq3_rotate_act_i8", _lib.ptr(X), _lib.F32, cols, M, X.stride(0), X.stride(1), _lib.ptr(act), _lib.stream_ptr(X.device))
+_lib.call("itq3_rotate_act_i8", _lib.ptr(X), _lib.F32, cols, M, X.stride(0), X.stride(1), _lib.ptr(act), None, _lib.stream_ptr(X.device))
 a=act.cpu().numpy()
 def sw(n,c): return (n>>3)*1024+(n&7)*128+((c^(n&7))<<4)
 Bt=np.zeros((N,256),np.int64)

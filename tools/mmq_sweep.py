@@ -82,10 +82,10 @@ def main():
                     s = _lib.stream_ptr(dev)
                     if small:
                         _lib.call("itq3_rotate_act_i8", _lib.ptr(X), _lib.F32, K, M, X.stride(0), X.stride(1),
-                                  _lib.ptr(act), s)
+                                  _lib.ptr(act), None, s)
                     else:
                         _lib.call("itq3_rotate_act_f16", _lib.ptr(X), _lib.F32, K, M, X.stride(0), X.stride(1),
-                                  _lib.ptr(act), s)
+                                  _lib.ptr(act), None, s)
 
                 def mm(i):
                     s = _lib.stream_ptr(dev)

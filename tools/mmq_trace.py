@@ -68,7 +68,7 @@ def main():
     ws = torch.empty(max(wsn, 1), dtype=torch.uint8, device=dev)
     s = _lib.stream_ptr(dev)
     rot = lambda: _lib.call("itq3_rotate_act_f16", _lib.ptr(X), 0, a.cols, a.m, X.stride(0), X.stride(1),
-                            _lib.ptr(act), s)
+                            _lib.ptr(act), None, s)
     mmq = lambda: _lib.call("itq3_mmq", _lib.ptr(q.mmq_layout()), a.rows, a.cols, 0, _lib.ptr(act), a.m,
                             _lib.ptr(Y), 0, Y.stride(0), Y.stride(1), _lib.ptr(ws) if wsn else None, s)
     for name, fn in (("rotate_act_f16", rot), ("mmq", mmq)):
