@@ -91,7 +91,8 @@ def _matvec_chain(q: QuantizedTensor, x: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, limbs: int) -> torch.Tensor:
+def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, limbs: int,
+                   check_finite: bool = True) -> torch.Tensor:
     """Y (rows x k) = w_hat @ X for a CUDA X (cols x k, any strides)."""
     dev = X.device
     rows, cols = q.rows, q.cols
@@ -103,31 +104,33 @@ def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, 
         lib = _lib.load()
         s = _lib.stream_ptr(dev)
         act = torch.empty(lib.itq3_mmq8_act_nbytes(cols, k), dtype=torch.uint8, device=dev)
-        flag = _nonfinite_flag(dev)
+        flag = _nonfinite_flag(dev) if check_finite else None
         _lib.call("itq3_rotate_act_i8", _lib.ptr(X), _lib.TORCH_DTYPE_CODE[X.dtype], cols, k, X.stride(0),
-                  X.stride(1), _lib.ptr(act), _lib.ptr(flag), s)
+                  X.stride(1), _lib.ptr(act), _lib.ptr(flag) if flag is not None else None, s)
         Y = torch.empty((rows, k), dtype=out_dtype, device=dev)
         wsn = lib.itq3_mmq8_ws_nbytes(rows, cols, k)
         ws = torch.empty(wsn, dtype=torch.uint8, device=dev) if wsn else None
         _lib.call("itq3_mmq8", _lib.ptr(q.mmq8_layout()), rows, cols, _lib.ptr(act), k, _lib.ptr(Y),
                   _lib.TORCH_DTYPE_CODE[out_dtype], Y.stride(0), Y.stride(1), _lib.ptr(ws) if ws is not None else None,
                   s)
-        _raise_if_nonfinite(flag)
+        if flag is not None:
+            _raise_if_nonfinite(flag)
         return Y
     if q.fast_layout() and out_dtype != torch.float64 and k >= MMQ_MIN_TOKENS:
         mmq = q.mmq_layout()
         s = _lib.stream_ptr(dev)
         act = torch.empty(_lib.load().itq3_mmq_act_nbytes(cols, k), dtype=torch.uint8, device=dev)
-        flag = _nonfinite_flag(dev)
+        flag = _nonfinite_flag(dev) if check_finite else None
         _lib.call("itq3_rotate_act_f16", _lib.ptr(X), _lib.TORCH_DTYPE_CODE[X.dtype], cols, k, X.stride(0),
-                  X.stride(1), _lib.ptr(act), _lib.ptr(flag), s)
+                  X.stride(1), _lib.ptr(act), _lib.ptr(flag) if flag is not None else None, s)
         Y = torch.empty((rows, k), dtype=out_dtype, device=dev)
         wsn = _lib.load().itq3_mmq_ws_nbytes(rows, cols, k)
         ws = torch.empty(wsn, dtype=torch.uint8, device=dev) if wsn else None
         _lib.call("itq3_mmq", _lib.ptr(mmq), rows, cols, int(not q.symmetric), _lib.ptr(act), k, _lib.ptr(Y),
                   _lib.TORCH_DTYPE_CODE[out_dtype], Y.stride(0), Y.stride(1), _lib.ptr(ws) if ws is not None else None,
                   s)
-        _raise_if_nonfinite(flag)
+        if flag is not None:
+            _raise_if_nonfinite(flag)
         return Y
     if q.fast_layout():
         tiled = q.tiled()
@@ -148,8 +151,12 @@ def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, 
     return Y if out_dtype == torch.float64 else Y.to(out_dtype)
 
 
-def fused_matmul(q: QuantizedTensor, x, *, limbs: int | None = None):
-    """Multiply the quantized matrix by X (cols x k) without materialising it."""
+def fused_matmul(q: QuantizedTensor, x, *, limbs: int | None = None, check_finite: bool = True):
+    """Multiply the quantized matrix by X (cols x k) without materialising it.
+
+    check_finite (CUDA X only, an addition to the reference signature): False skips the DomainError
+    check on X -- and with it the one host synchronisation the check needs -- so the call stays
+    asynchronous on the stream."""
     if isinstance(x, torch.Tensor) and x.is_cuda:
         if x.ndim != 2:
             raise ShapeError(f"fused_matmul: X must be 2-D (cols x k), got shape {tuple(x.shape)}")
@@ -159,11 +166,11 @@ def fused_matmul(q: QuantizedTensor, x, *, limbs: int | None = None):
             x = x.to(torch.float32)
         parity = x.dtype == torch.float64
         # the MMQ paths (k >= 16, perf mode) check finiteness inside their activation rotation
-        if parity or x.shape[1] < MMQ_MIN_TOKENS or not q.fast_layout():
+        if check_finite and (parity or x.shape[1] < MMQ_MIN_TOKENS or not q.fast_layout()):
             if not bool(torch.isfinite(x).all()):
                 raise DomainError("fused_matmul: X contains non-finite values")
         L = limbs or (PARITY_LIMBS if parity else perf_limbs(x.shape[1]))
-        return _matmul_device(q, x, torch.float64 if parity else torch.float32, L)
+        return _matmul_device(q, x, torch.float64 if parity else torch.float32, L, check_finite)
     a = np.asarray(x, dtype=np.float64)
     if a.ndim != 2:
         raise ShapeError(f"fused_matmul: X must be 2-D (cols x k), got shape {a.shape}")
@@ -176,12 +183,12 @@ def fused_matmul(q: QuantizedTensor, x, *, limbs: int | None = None):
     return _matmul_device(q, t, torch.float64, limbs or PARITY_LIMBS).cpu().numpy()
 
 
-def fused_matvec(q: QuantizedTensor, x, *, limbs: int | None = None):
+def fused_matvec(q: QuantizedTensor, x, *, limbs: int | None = None, check_finite: bool = True):
     """Matrix-vector product: exactly the k = 1 column of fused_matmul."""
     if isinstance(x, torch.Tensor) and x.is_cuda:
         if x.ndim != 1:
             raise ShapeError(f"fused_matvec: x must be 1-D, got shape {tuple(x.shape)}")
-        return fused_matmul(q, x[:, None], limbs=limbs)[:, 0]
+        return fused_matmul(q, x[:, None], limbs=limbs, check_finite=check_finite)[:, 0]
     a = np.asarray(x, dtype=np.float64)
     if a.ndim != 1:
         raise ShapeError(f"fused_matvec: x must be 1-D, got shape {a.shape}")
