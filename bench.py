@@ -225,12 +225,14 @@ def build_stack(n_layers: int, seed: int, dev, mode: str = "chain"):
 
 def run_tp(args):
     """--tp: ONE token stream row-sharded over the ranks (strong scaling): each rank holds
-    rows shard_bounds(r, world, rank) of every stage, computes them with the K3+K4 kernels and
-    all-gathers y with NCCL; the whole step (2 kernels + 1 collective per stage) is one CUDA graph."""
+    rows shard_bounds(r, world, rank) of every stage.  --tp-impl fused (default): one persistent chain
+    kernel per rank whose reducers store every output word into all ranks' copies of y over NVLink
+    (symmetric-memory peer pointers) -- the all-gather is fused, no NCCL call in the step.
+    --tp-impl nccl: K3+K4 kernels and an NCCL all_gather per stage, one CUDA graph per step."""
     import torch
 
     import paper_2603_27914_b200 as P
-    from paper_2603_27914_b200.parallel import TPStack, shard_bounds
+    from paper_2603_27914_b200.parallel import TPChainStack, TPStack, shard_bounds
 
     rank, world, local = dist_env()
     if world > 1:
@@ -252,7 +254,10 @@ def run_tp(args):
             rows.append(r)
             cols.append(c)
             del w
-    st = TPStack(qs, rows, cols)
+    if args.tp_impl == "fused":
+        st = TPChainStack(qs, rows, cols)  # one chain kernel per rank, all-gather fused into peer stores
+    else:
+        st = TPStack(qs, rows, cols)  # K3 + K4 + NCCL all_gather per stage
     st.capture()
     for _ in range(args.warmup):
         st.replay()
@@ -278,9 +283,11 @@ def run_tp(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8xs8->s32 mma + fp32",
             "data": "synthetic: random-init N(0,1/K) row shards quantized to ITQ3_S on each GPU",
             "config": {"workload": WORKLOAD, "model": f"{MODEL} (linear layers)", "global_batch": 1, "seq_len": 1,
-                       "parallelism": f"tp{world} (row-sharded stages + NCCL all-gather per stage)"},
+                       "parallelism": f"tp{world} (row-sharded stages; " + (
+                           "all-gather fused into the chain kernel's peer stores)" if args.tp_impl == "fused"
+                           else "NCCL all-gather per stage)")},
             "packed_weight_gbps": tiled_bytes / (ms / 1000.0) / 1e9,
-            "gpu_launches": 2 * len(qs) * args.steps}), flush=True)
+            "gpu_launches": (1 if args.tp_impl == "fused" else 2 * len(qs)) * args.steps}), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 
@@ -439,6 +446,8 @@ def main():
     ap.add_argument("--mode", choices=["chain", "kernels"], default="chain")
     ap.add_argument("--model", choices=sorted(MODELS), default=MODEL)
     ap.add_argument("--tp", action="store_true", help="row-shard one token stream over the ranks (C5)")
+    ap.add_argument("--tp-impl", choices=["fused", "nccl"], default="fused",
+                    help="--tp: fused chain kernel with NVLink peer stores, or per-stage kernels + NCCL all_gather")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -172,6 +172,15 @@ int itq3_chain_act_block_bytes(int limbs);
 int itq3_chain_smem_bytes(void);
 int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* tiled, void* y, const float* xin, int64_t rows,
                           int64_t cols, int asymmetric, int reserved);
+/* Tensor-parallel stage (no single reference counterpart: the reference's TP path is the per-stage
+ * matvec + all-gather of SURVEY.md C5).  This rank computes output rows [row0, row0 + rows) of a
+ * yrows-row stage from its row shard `tiled`, and the reducer stores every tagged output word into
+ * all npeer ranks' copies of y (d_peers: device array of npeer pointers, e.g. symmetric-memory peer
+ * addresses over NVLink; peer p's copy sits at the same layout as `y`).  y holds
+ * 2 x nch x yrows u64 words (epoch-parity double buffer), nch = ceil(cols / 4096).  All ranks launch
+ * itq3_chain_run the same number of times; consumers and the final fold read the full yrows rows. */
+int itq3_chain_write_desc_tp(void* host_desc, int index, const uint8_t* tiled, void* y, int64_t rows, int64_t cols,
+                             int asymmetric, int64_t row0, int64_t yrows, const void* d_peers, int npeer);
 int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch, float* out,
                    int grid, void* d_trace, void* stream);
 

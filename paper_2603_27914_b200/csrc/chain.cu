@@ -32,14 +32,22 @@ constexpr int kSlotZps = kUnitBlocks * 16;               // 256 B
 constexpr int kSlotBytes = kSlotCodes + kSlotScales + kSlotZps;
 constexpr int kNumSlots = 11;
 constexpr int kMaxChainNB = 256;                         // K up to 65536
+constexpr int kMaxChainPeers = 8;                        // tensor-parallel ranks (one NVLink domain)
 constexpr int kMaxLimbs = 4;
 
 struct ChainStage {
     const uint8_t* tiled;  // codes | scales | zps (itq3_repack_tiled layout)
     unsigned long long* y; // [nch][rows] tagged outputs: low 32 = fp32 bits, high 32 = step epoch
     const float* xin;      // optional: untagged fp32 input (independent stage, no dependency)
+    // Tensor-parallel stage (npeer > 0): this rank computes output rows [row0, row0 + rows) of a
+    // yrows-row stage and stores each tagged word straight into all npeer ranks' copies of y
+    // (ypeer[p] = rank p's y, NVLink peer pointers), so the all-gather is fused into the reducer.
+    // y is then double-buffered by epoch parity ([2][nch][yrows]) so a rank already in step t+1
+    // never overwrites words a slower peer still reads in step t.
+    unsigned long long* const* ypeer;
     int64_t rows, cols;
-    int32_t NB, RT, asym, reserved;
+    int32_t NB, RT, asym, npeer;
+    int32_t row0, yrows;
 };
 
 __host__ __device__ inline int act_block_bytes(int L) { return 256 * L + 32; }
@@ -107,24 +115,38 @@ __device__ __forceinline__ unsigned long long ld_u64_relaxed(const unsigned long
 __device__ __forceinline__ void st_u64_relaxed(unsigned long long* p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// system scope: words written by peer GPUs over NVLink (tensor-parallel stages)
+__device__ __forceinline__ unsigned long long ld_u64_relaxed_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_u64_relaxed_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+template <bool SYS>
+__device__ __forceinline__ unsigned long long ld_tag(const unsigned long long* p) {
+    return SYS ? ld_u64_relaxed_sys(p) : ld_u64_relaxed(p);
+}
 
 // Wait for, and sum, one 256-block of a producing stage's tagged K-chunk partials.  Each 64-bit
 // word carries its value and the step epoch in one single-copy-atomic access, so the consumer
 // needs no flag, counter or fence: it spins until all 256 x nparts tags equal `epoch`.
+template <bool SYS>
 __device__ __forceinline__ void load_tagged_block(const unsigned long long* src, int nparts, int64_t part_stride,
                                                   unsigned epoch, int lane, float (&f)[8]) {
     for (;;) {
         bool ok = true;
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-            const unsigned long long w = ld_u64_relaxed(src + lane + 32 * e);
+            const unsigned long long w = ld_tag<SYS>(src + lane + 32 * e);
             ok &= (unsigned)(w >> 32) == epoch;
             f[e] = __uint_as_float((unsigned)w);
         }
         for (int c = 1; c < nparts; ++c)  // K-chunk partials, fixed order
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                const unsigned long long w = ld_u64_relaxed(src + c * part_stride + lane + 32 * e);
+                const unsigned long long w = ld_tag<SYS>(src + c * part_stride + lane + 32 * e);
                 ok &= (unsigned)(w >> 32) == epoch;
                 f[e] += __uint_as_float((unsigned)w);
             }
@@ -233,13 +255,13 @@ constexpr int kSmemStages = 150;  // stage descriptors + this CTA's split cached
 // Work split of stage st for CTA cta: K-chunk ch (CTAs c with c % nch == ch), and the row
 // tiles rt = rt0, rt0 + Gc, ... (Gc CTAs per chunk); active = 0 if the CTA is idle.
 struct StageSplit {
-    int nch, ch, rt0, Gc, active, pad[3];
+    int nch, ch, rt0, Gc, active;
 };
 
 struct ChainSmem {
     ChainStage desc[kSmemStages];
     StageSplit split[kSmemStages];
-    uint8_t ring[kNumSlots][kSlotBytes];
+    alignas(128) uint8_t ring[kNumSlots][kSlotBytes];
     uint8_t rot[kChainConsumerWarps][kActSmemBlock];   // per-warp rotation scratch (own block only)
     float part[kNumSlots][kChainConsumerWarps][16];    // per-warp row partials of a unit
     uint64_t full[kNumSlots];
@@ -331,7 +353,10 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             StageSplit sp;
             if (!stage_get(sm, stages, cta, G, s, st, sp)) continue;
             const int n_units = (st.RT - 1 - sp.rt0) / sp.Gc + 1;
-            unsigned long long* yout = st.y + (int64_t)sp.ch * st.rows;
+            // y offset of this CTA's K-chunk (+ the epoch-parity half for tensor-parallel stages)
+            const int64_t yoff = (int64_t)sp.ch * st.yrows + st.row0 +
+                                 (st.npeer ? (int64_t)(epoch & 1u) * sp.nch * st.yrows : 0);
+            unsigned long long* yout = st.y + yoff;
             const unsigned long long tag = (unsigned long long)epoch << 32;
             for (int j = 0; j < n_units; ++j) {
                 const int useq = seq + j;
@@ -345,7 +370,14 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 #pragma unroll
                     for (int w = 1; w < kChainConsumerWarps; ++w) sum += part[w];
                     const int64_t row = (int64_t)(sp.rt0 + j * sp.Gc) * 16 + lane;
-                    if (row < st.rows) st_u64_relaxed(yout + row, tag | __float_as_uint(sum));
+                    if (row < st.rows) {
+                        const unsigned long long word = tag | __float_as_uint(sum);
+                        if (st.npeer == 0) {
+                            st_u64_relaxed(yout + row, word);
+                        } else {
+                            for (int p = 0; p < st.npeer; ++p) st_u64_relaxed_sys(st.ypeer[p] + yoff + row, word);
+                        }
+                    }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&sm.empty[slot]);
@@ -417,7 +449,12 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             } else {
                 const ChainStage pv = s - 1 < kSmemStages ? sm.desc[s - 1] : stages[s - 1];
                 const int pn = (pv.NB + kUnitBlocks - 1) / kUnitBlocks;
-                load_tagged_block(pv.y + 256 * (b0 + warp), pn, pv.rows, epoch, lane, f);
+                if (pv.npeer == 0) {
+                    load_tagged_block<false>(pv.y + 256 * (b0 + warp), pn, pv.yrows, epoch, lane, f);
+                } else {
+                    const int64_t par = (int64_t)(epoch & 1u) * pn * pv.yrows;
+                    load_tagged_block<true>(pv.y + par + 256 * (b0 + warp), pn, pv.yrows, epoch, lane, f);
+                }
             }
             if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 1] = globaltimer();
             if (prof) c_in += clock64() - c0;
@@ -504,16 +541,18 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     // fold the last stage's K-chunk partials into `out` (fixed order), waiting on the tags
     const ChainStage last = stages[S - 1];
     const int ln = (last.NB + kUnitBlocks - 1) / kUnitBlocks;
-    for (int64_t r = (int64_t)cta * (32 * kChainConsumerWarps) + tid; r < last.rows;
+    const unsigned long long* ylast = last.y + (last.npeer ? (int64_t)(epoch & 1u) * ln * last.yrows : 0);
+    for (int64_t r = (int64_t)cta * (32 * kChainConsumerWarps) + tid; r < last.yrows;
          r += (int64_t)G * 32 * kChainConsumerWarps) {
         float v;
         for (;;) {
             bool ok = true;
-            unsigned long long w = ld_u64_relaxed(last.y + r);
+            unsigned long long w = last.npeer ? ld_u64_relaxed_sys(ylast + r) : ld_u64_relaxed(ylast + r);
             ok &= (unsigned)(w >> 32) == epoch;
             v = __uint_as_float((unsigned)w);
             for (int c = 1; c < ln; ++c) {
-                w = ld_u64_relaxed(last.y + c * last.rows + r);
+                w = last.npeer ? ld_u64_relaxed_sys(ylast + c * last.yrows + r)
+                               : ld_u64_relaxed(ylast + c * last.yrows + r);
                 ok &= (unsigned)(w >> 32) == epoch;
                 v += __uint_as_float((unsigned)w);
             }
@@ -537,23 +576,44 @@ extern "C" int64_t itq3_chain_desc_nbytes(void) { return (int64_t)sizeof(ChainSt
 extern "C" int itq3_chain_act_block_bytes(int limbs) { return act_block_bytes(limbs); }
 extern "C" int itq3_chain_smem_bytes(void) { return (int)sizeof(ChainSmem); }
 
+extern "C" int itq3_chain_write_desc_tp(void*, int, const uint8_t*, void*, int64_t, int64_t, int, int64_t, int64_t,
+                                        const void*, int);
+
 extern "C" int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* tiled, void* y, const float* xin,
-                                     int64_t rows, int64_t cols, int asymmetric, int ycnt_off) {
+                                     int64_t rows, int64_t cols, int asymmetric, int reserved) {
+    (void)reserved;
+    const int rc = itq3_chain_write_desc_tp(host_desc, index, tiled, y, rows, cols, asymmetric, 0, rows, nullptr, 0);
+    if (rc == ITQ3_OK) reinterpret_cast<ChainStage*>(host_desc)[index].xin = xin;
+    return rc;
+}
+
+extern "C" int itq3_chain_write_desc_tp(void* host_desc, int index, const uint8_t* tiled, void* y, int64_t rows,
+                                        int64_t cols, int asymmetric, int64_t row0, int64_t yrows,
+                                        const void* d_peers, int npeer) {
     if (cols % 256 || cols / 256 > kMaxChainNB) {
         set_error("chain: stage %d needs cols %% 256 == 0 and cols <= %d (got %lld)", index, 256 * kMaxChainNB,
                   (long long)cols);
         return ITQ3_E_UNSUPPORTED;
     }
     ChainStage& st = reinterpret_cast<ChainStage*>(host_desc)[index];
+    if (npeer < 0 || npeer > kMaxChainPeers || (npeer > 0 && d_peers == nullptr) || row0 < 0 || rows < 0 ||
+        row0 + rows > yrows || yrows > INT32_MAX) {
+        set_error("chain: stage %d: bad tensor-parallel shard (row0 %lld, rows %lld, yrows %lld, npeer %d)", index,
+                  (long long)row0, (long long)rows, (long long)yrows, npeer);
+        return ITQ3_E_DOMAIN;
+    }
     st.tiled = tiled;
     st.y = (unsigned long long*)y;
-    st.xin = xin;
+    st.xin = nullptr;
+    st.ypeer = (unsigned long long* const*)d_peers;
     st.rows = rows;
     st.cols = cols;
     st.NB = (int)(cols / 256);
     st.RT = (int)((rows + 15) / 16);
     st.asym = asymmetric;
-    st.reserved = ycnt_off;
+    st.npeer = npeer;
+    st.row0 = (int32_t)row0;
+    st.yrows = (int32_t)yrows;
     return ITQ3_OK;
 }
 

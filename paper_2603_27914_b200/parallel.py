@@ -159,3 +159,121 @@ class TPStack:
 
     def output(self) -> torch.Tensor:
         return self.yfull[-1][: self.rows[-1]]
+
+
+def tp_chain_layout(rows: list[int], cols: list[int]) -> tuple[list[int], int]:
+    """Word offsets of each stage's tagged-output buffer inside one symmetric allocation, and the total.
+
+    Stage i holds 2 (epoch parity) x nch_i (K-chunks of 4096) x rows_i u64 words -- the layout
+    itq3_chain_write_desc_tp expects -- at the same offset on every rank, so rank p's copy of stage i
+    is peer_base[p] + 8 * offset_i."""
+    offs, total = [], 0
+    for r, c in zip(rows, cols):
+        offs.append(total)
+        total += 2 * (-(-c // 4096)) * r
+    return offs, total
+
+
+class TPChainStack:
+    """Tensor-parallel decode chain in ONE persistent kernel per rank, with the all-gather fused in.
+
+    Every rank runs the cooperative chain kernel (csrc/chain.cu) over its row shards; the reducer of
+    each stage stores its tagged output words directly into every rank's copy of the stage output
+    (NVLink peer stores through torch symmetric-memory peer pointers), and the next stage's consumers
+    on every rank spin on those tags exactly as in the single-GPU chain.  There is no NCCL call, no
+    per-stage launch and no separate gather pass: the transfer of stage i overlaps stage i's math
+    unit by unit (TPStack is the unfused NCCL baseline: 2 kernels + 1 all_gather per stage).
+
+    `local_qs[i]`: this rank's rows shard_bounds(rows[i], world, rank) of stage i.  `peer_bases`
+    (optional, testing): the per-rank base addresses of `ybuf` to use instead of a symmetric-memory
+    rendezvous -- with world 1 the only peer is the rank itself.
+    """
+
+    def __init__(self, local_qs, rows, cols, group=None, limbs: int = 3, world: int | None = None,
+                 rank: int | None = None, ybuf: torch.Tensor | None = None, peer_bases: list[int] | None = None,
+                 grid: int = 0):
+        import ctypes
+
+        from . import _lib
+
+        self._lib = _lib
+        self.group = group
+        if world is None:
+            world = dist.get_world_size(group) if dist.is_initialized() else 1
+        if rank is None:
+            rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world, self.rank = world, rank
+        self.qs, self.rows, self.cols, self.limbs, self.grid = local_qs, list(rows), list(cols), limbs, grid
+        if not local_qs:
+            raise ShapeError("TPChainStack: no stages")
+        for i in range(1, len(rows)):
+            if cols[i] > rows[i - 1]:
+                raise ShapeError("TPChainStack: stage input longer than the previous output")
+        for i, q in enumerate(local_qs):
+            r0, r1 = shard_bounds(rows[i], world, rank)
+            if q.rows != r1 - r0 or q.cols != cols[i]:
+                raise ShapeError(f"TPChainStack: stage {i} shard is {q.rows}x{q.cols}, expected {r1 - r0}x{cols[i]}")
+            if not q.fast_layout():
+                raise ShapeError("TPChainStack: stages need the tiled layout (block_n 256, variant s, cols % 256 == 0)")
+        self.dev = _lib.device()
+        lib = _lib.load()
+        self.tiled = [q.tiled() for q in local_qs]
+        self.offs, total = tp_chain_layout(self.rows, self.cols)
+        if ybuf is None:
+            if world > 1:
+                from torch.distributed import _symmetric_memory as symm
+
+                ybuf = symm.empty(total, dtype=torch.int64, device=self.dev)
+                ybuf.zero_()
+                hdl = symm.rendezvous(ybuf, group if group is not None else dist.group.WORLD)
+                peer_bases = list(hdl.buffer_ptrs)
+                torch.cuda.synchronize(self.dev)
+                dist.barrier(group)  # every copy zeroed before any peer stores into it
+            else:
+                ybuf = torch.zeros(total, dtype=torch.int64, device=self.dev)
+        if peer_bases is None:
+            peer_bases = [ybuf.data_ptr()]
+        if len(peer_bases) != world or peer_bases[rank] != ybuf.data_ptr():
+            raise ShapeError("TPChainStack: peer_bases must list every rank's buffer, this rank's at index rank")
+        self.ybuf = ybuf
+        S = len(local_qs)
+        self.peers = torch.tensor([[b + 8 * o for b in peer_bases] for o in self.offs], dtype=torch.int64,
+                                  device=self.dev)
+        host = ctypes.create_string_buffer(lib.itq3_chain_desc_nbytes() * S)
+        for i, q in enumerate(local_qs):
+            r0, _ = shard_bounds(rows[i], world, rank)
+            _lib.check(lib.itq3_chain_write_desc_tp(host, i, _lib.ptr(self.tiled[i]),
+                                                    ybuf.data_ptr() + 8 * self.offs[i], q.rows, q.cols,
+                                                    int(not q.symmetric), r0, rows[i],
+                                                    self.peers.data_ptr() + 8 * world * i, world))
+        self.desc = torch.frombuffer(bytearray(host.raw), dtype=torch.uint8).to(self.dev)
+        self.epoch = torch.zeros(2, dtype=torch.int32, device=self.dev)
+        self.x = torch.zeros(cols[0], dtype=torch.float32, device=self.dev)
+        self.out = torch.empty(rows[-1], dtype=torch.float32, device=self.dev)
+        self.graph = None
+
+    def launch_all(self, stream: int | None = None) -> None:
+        lib = self._lib
+        s = stream if stream is not None else lib.stream_ptr(self.dev)
+        lib.call("itq3_chain_run", lib.ptr(self.desc), len(self.qs), lib.ptr(self.x), self.limbs,
+                 lib.ptr(self.epoch), lib.ptr(self.out), self.grid, None, s)
+
+    def capture(self) -> None:
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(side):
+            self.launch_all()
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.launch_all()
+        self.graph = g
+
+    def replay(self) -> None:
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+
+    def output(self) -> torch.Tensor:
+        """The full last-stage output (all ranks' rows), identical on every rank."""
+        return self.out

@@ -105,3 +105,33 @@ def test_shard_bounds_cover_rows(rows, world):
     assert spans[0][0] == 0 and spans[-1][1] == rows
     for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
         assert a1 == b0 and a0 <= a1
+
+
+def test_tp_chain_layout_and_descriptors():
+    """Host side of the fused tensor-parallel chain: the symmetric y layout (2 parity halves x
+    K-chunks x full rows per stage, same offsets on every rank) and the descriptor checks of
+    itq3_chain_write_desc_tp (no GPU needed)."""
+    import ctypes
+
+    from paper_2603_27914_b200 import _lib
+    from paper_2603_27914_b200.parallel import shard_bounds, tp_chain_layout
+
+    rows, cols = [12288, 4096, 11008, 4096], [4096, 4096, 4096, 11008]
+    offs, total = tp_chain_layout(rows, cols)
+    assert offs == [0, 2 * 12288, 2 * 12288 + 2 * 4096, 2 * 12288 + 2 * 4096 + 2 * 11008]
+    assert total == offs[-1] + 2 * 3 * 4096  # cols 11008 -> 3 K-chunks of 4096
+    lib = _lib.load()
+    nd = lib.itq3_chain_desc_nbytes()
+    host = ctypes.create_string_buffer(nd * 4)
+    peers = 0x1000  # device address of the peer table: only stored, never dereferenced here
+    for world in (2, 8):
+        for rank in range(world):
+            for i in range(4):
+                r0, r1 = shard_bounds(rows[i], world, rank)
+                assert lib.itq3_chain_write_desc_tp(host, i, None, 0x2000, r1 - r0, cols[i], 0, r0, rows[i],
+                                                    peers, world) == 0
+    # a shard running past the stage's rows, a missing peer table and too many peers are refused
+    assert lib.itq3_chain_write_desc_tp(host, 0, None, 0x2000, 4096, 4096, 0, 10000, 12288, peers, 2) != 0
+    assert lib.itq3_chain_write_desc_tp(host, 0, None, 0x2000, 4096, 4096, 0, 0, 12288, None, 2) != 0
+    assert lib.itq3_chain_write_desc_tp(host, 0, None, 0x2000, 4096, 4096, 0, 0, 12288, peers, 9) != 0
+    assert lib.itq3_chain_write_desc_tp(host, 0, None, 0x2000, 4096, 4000, 0, 0, 12288, peers, 2) != 0
