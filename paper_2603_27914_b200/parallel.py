@@ -226,7 +226,8 @@ class TPChainStack:
                 ybuf = symm.empty(total, dtype=torch.int64, device=self.dev)
                 ybuf.zero_()
                 hdl = symm.rendezvous(ybuf, group if group is not None else dist.group.WORLD)
-                peer_bases = list(hdl.buffer_ptrs)
+                delta = ybuf.data_ptr() - hdl.buffer_ptrs[rank]  # tensor offset inside the symmetric block
+                peer_bases = [b + delta for b in hdl.buffer_ptrs]
                 torch.cuda.synchronize(self.dev)
                 dist.barrier(group)  # every copy zeroed before any peer stores into it
             else:
