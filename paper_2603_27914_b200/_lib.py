@@ -15,7 +15,7 @@ import torch
 from .errors import ItqError, from_status
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libitq3.so")
+LIB_PATH = os.environ.get("ITQ3_LIB") or os.path.join(_HERE, "lib", "libitq3.so")  # ITQ3_LIB: experiment builds
 
 F32, F64, BF16, F16 = 0, 1, 2, 3
 TORCH_DTYPE_CODE = {torch.float32: F32, torch.float64: F64, torch.bfloat16: BF16, torch.float16: F16}

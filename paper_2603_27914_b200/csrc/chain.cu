@@ -194,7 +194,9 @@ __device__ void chain_rotate_to_smem(const float (&fin)[8], int L, uint8_t* img,
     amax = __reduce_max_sync(FULL, amax);
     // shift k so that |q| <= 2^(8L-2) (limbs never overflow): bitlen(amax) - k <= 8L - 2
     const int bl = 32 - __clz(amax);
-    const int k = max(0, bl - (8 * L - 2));
+    // (limbs = 4 gives no more than 22 bits: q 4^3 and the class differences must fit the four
+    // balanced record limbs of an int32)
+    const int k = max(0, bl - min(8 * L - 2, 22));
     const int ex = e_in + k;
     int Q = 0;
     const int tt = (lane & 15) >> 2, beta = lane & 3, half = lane >> 4;
@@ -203,12 +205,21 @@ __device__ void chain_rotate_to_smem(const float (&fin)[8], int L, uint8_t* img,
     // accumulates 64 * sum(c x') into ONE integer accumulator (no per-tile class recombination).
     // |q| <= 2^22 -> |q 4^(3-i)| <= 2^28: four balanced base-256 limbs = the bytes of
     // (qs + 0x80808080) ^ 0x80808080, all four record columns used.
+    // Cumulative masks: with P_i = codes & (4^(i+1) - 1 per byte) (P_3 = the raw word, no mask),
+    // sum_i (c_i 4^i) A_i = sum_i P_i (A_i - A_{i+1}) (A_4 = 0, exact in int32), so chunk e stores
+    // the difference of its pre-scaled activation and the next class's: the tile needs 3 LOP3 per
+    // A register group instead of 4 and produces the same integer accumulators.
+    int qs[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
         const int q = k ? ((v[e] + (1 << (k - 1))) >> k) : v[e];
         Q += q;
-        const int qs = q << (2 * (3 - (e & 3)));
-        const uint32_t limbs = (uint32_t)(qs + (int)0x80808080u) ^ 0x80808080u;
+        qs[e] = q << (2 * (3 - (e & 3)));
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int dq = (e & 3) < 3 ? qs[e] - qs[e + 1] : qs[e];  // |dq| < 2^29
+        const uint32_t limbs = (uint32_t)(dq + (int)0x80808080u) ^ 0x80808080u;
         uint8_t* dst = img + (e * 16 + tt) * 8 + half * 4 + beta;  // (chunk e, column 0, t, byte)
 #pragma unroll
         for (int l = 0; l < 4; ++l) dst[l * 32] = (uint8_t)(limbs >> (8 * l));  // column l: +4*8 B
@@ -231,7 +242,7 @@ __device__ __forceinline__ float2 chain_tile(const uint8_t* ring, int warp, int 
     int C0[4] = {0, 0, 0, 0}, C1[4] = {0, 0, 0, 0};  // group 0 / group 1 (two 4-deep chains)
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const uint32_t mk = 0x03030303u << (2 * i);
+        const uint32_t mk = i == 3 ? 0xffffffffu : (0x04040404u << (2 * i)) - 0x01010101u;  // cumulative
         mma_u8s8_c(C0, wa0.x & mk, wa0.y & mk, wa0.z & mk, wa0.w & mk, bf[i].x, bf[i].y);
         mma_u8s8_c(C1, wa1.x & mk, wa1.y & mk, wa1.z & mk, wa1.w & mk, bf[4 + i].x, bf[4 + i].y);
     }
@@ -458,7 +469,9 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             }
             if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 1] = globaltimer();
             if (prof) c_in += clock64() - c0;
+#ifndef CHAIN_EXP_NOROT
             chain_rotate_to_smem(f, L, rot, lane);
+#endif
             __syncwarp();
             // fragments for lane (g, t): columns g < 4 hold limbs, columns >= 4 are zero
 #pragma unroll
@@ -496,7 +509,11 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                     c1 = c2;
                 }
                 float2 ra = make_float2(0.f, 0.f), rb = make_float2(0.f, 0.f);
+#ifdef CHAIN_EXP_NOTILE
+                if (false) {
+#else
                 if (has_block) {
+#endif
                     ra = chain_tile(sm.ring[slot0], warp, lane, g, bf, fcx, corr, st.asym);
                     if (two) rb = chain_tile(sm.ring[slot1], warp, lane, g, bf, fcx, corr, st.asym);
                     // combine the quad's limb-pair columns (lanes t = 0..3, fixed order)
