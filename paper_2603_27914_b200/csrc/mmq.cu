@@ -591,11 +591,9 @@ template <typename TX>
 __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restrict__ x, int64_t M, int64_t stride_k,
                                                              int64_t stride_m, int64_t NC, int BN,
                                                              uint8_t* __restrict__ out, unsigned* __restrict__ nonfinite) {
-    // fp32 inputs, token-major (257: conflict-free transposes); after the butterflies the same bytes hold
-    // the rotated f16 outputs as [32][264] (528-byte rows: 16-byte aligned, 4 wavefronts per 16-B warp load)
+    // fp32 inputs, token-major (257: conflict-free transposes)
     pdl_release();
     __shared__ __align__(16) float tile[32][257];
-    __half(&th)[32][264] = *reinterpret_cast<__half(*)[32][264]>(&tile[0][0]);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t b = blockIdx.y, m0 = (int64_t)blockIdx.x * 32;  // adjacent CTAs: adjacent token groups (DRAM locality)
     const TX* xb = x + b * 256 * stride_k;
@@ -625,55 +623,55 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
         }
     }
     __syncthreads();
-    float v[4][8];  // the warp's 4 tokens: lane holds k = lane + 32 e
+    // Butterfly: lane (token 4 warp + lane / 8, k bits 2..4 = lane % 8) holds the 32 values with
+    // k bits 0..1 and 5..7 in registers (v[4 kh + j]: k = j + 4 (lane % 8) + 32 kh), so five of the
+    // eight stages are register-only and three use shuffles (96 per thread instead of 160); the
+    // smem reads are conflict-free (row pitch 257: bank = token + 4 (lane % 8) + const).
+    const int tl = lane >> 3, kq = lane & 7, tok = 4 * warp + tl;
+    float v[32];
     bool bad = false;
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj)
+    for (int kh = 0; kh < 8; ++kh)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            v[jj][e] = tile[4 * warp + jj][lane + 32 * e];
-            bad |= !isfinite(v[jj][e]);
+        for (int j = 0; j < 4; ++j) {
+            v[4 * kh + j] = tile[tok][j + 4 * kq + 32 * kh];
+            bad |= !isfinite(v[4 * kh + j]);
         }
     // fused_matmul's DomainError check (compute.py): one flag word, set if any input is not finite
     if (nonfinite && __any_sync(FULL, bad) && lane == 0) atomicOr(nonfinite, 1u);
-    __syncthreads();  // the f16 outputs overwrite the fp32 tile
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
+    for (int hh = 1; hh < 32; hh <<= 1)
 #pragma unroll
-        for (int h = 1; h < 32; h <<= 1) {
-            const bool high = (lane & h) != 0;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const float p = __shfl_xor_sync(FULL, v[jj][e], h);
-                v[jj][e] = high ? p - v[jj][e] : v[jj][e] + p;
+        for (int r = 0; r < 32; ++r)
+            if ((r & hh) == 0) {
+                const float lo = v[r], hi = v[r + hh];
+                v[r] = lo + hi;
+                v[r + hh] = lo - hi;
             }
+#pragma unroll
+    for (int h = 1; h < 8; h <<= 1) {
+        const bool high = (lane & h) != 0;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+            const float p = __shfl_xor_sync(FULL, v[r], h);
+            v[r] = high ? p - v[r] : v[r] + p;
         }
-#pragma unroll
-        for (int hh = 1; hh < 8; hh <<= 1)
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-                if ((e & hh) == 0) {
-                    const float lo = v[jj][e], hi = v[jj][e + hh];
-                    v[jj][e] = lo + hi;
-                    v[jj][e + hh] = lo - hi;
-                }
-#pragma unroll
-        for (int e = 0; e < 8; ++e) th[4 * warp + jj][lane + 32 * e] = __float2half_rn(v[jj][e] * 0.0625f);
     }
-    __syncthreads();
+    // 8-byte stores of 4 consecutive k of one token (a warp covers 4 tokens x 64 contiguous bytes)
+    const int64_t m = m0 + tok;
+    const int hb = BN / 2;                 // tokens per CTA half of a tile
+    const int64_t half = m / hb;           // = 2 * tile + h
+    const int row = (int)(m % hb);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int idx = tid + 256 * i, j = idx >> 5, c8 = idx & 31;  // token j, k = 8 c8 .. 8 c8 + 7
-        const uint4 pv = *reinterpret_cast<const uint4*>(&th[j][8 * c8]);  // 528-byte rows: 4 wavefronts per warp
-        const uint32_t p[4] = {pv.x, pv.y, pv.z, pv.w};
-        const int64_t m = m0 + j;
-        const int64_t k = b * 256 + 8 * c8;
+    for (int kh = 0; kh < 8; ++kh) {
+        const int64_t k = b * 256 + 32 * kh + 4 * kq;
         const int64_t kc = k >> 6;
         const int kk = (int)(k & 63);
-        const int hb = BN / 2;                 // tokens per CTA half of a tile
-        const int64_t half = m / hb;           // = 2 * tile + h
-        uint8_t* t = out + (half * NC + kc) * (int64_t)(hb * 128);
-        *reinterpret_cast<uint4*>(t + sw128_off((int)(m % hb), kk >> 3)) = make_uint4(p[0], p[1], p[2], p[3]);
+        const __half2 p0 = __floats2half2_rn(v[4 * kh] * 0.0625f, v[4 * kh + 1] * 0.0625f);
+        const __half2 p1 = __floats2half2_rn(v[4 * kh + 2] * 0.0625f, v[4 * kh + 3] * 0.0625f);
+        uint8_t* t = out + (half * NC + kc) * (int64_t)(hb * 128) + sw128_off(row, kk >> 3) + (kk & 7) * 2;
+        *reinterpret_cast<uint2*>(t) = make_uint2(*reinterpret_cast<const uint32_t*>(&p0),
+                                                  *reinterpret_cast<const uint32_t*>(&p1));
     }
 }
 
