@@ -1190,10 +1190,25 @@ __global__ void rotate_act_i8_kernel(const TX* __restrict__ x, int64_t NB, int64
                                      int64_t stride_k, int64_t stride_m, int BN, uint8_t* __restrict__ out,
                                      unsigned* __restrict__ nonfinite) {
     pdl_release();
-    const int lane = threadIdx.x & 31;
-    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (wid >= NB * M_pad) return;
-    const int64_t b = wid % NB, m = wid / NB;
+    // CTA = (block b, 8 tokens): coalesced loads along whichever of k / token is contiguous into a
+    // padded smem tile, then warp w rotates token m0 + w from it (conflict-free: pitch 257)
+    __shared__ float tile[8][257];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t b = blockIdx.x, m0 = (int64_t)blockIdx.y * 8;
+    const TX* xb = x + b * 256 * stride_k;
+    if (stride_k == 1 && stride_m != 1) {  // token-major: threads along k
+#pragma unroll
+        for (int j = 0; j < 8; ++j) tile[j][tid] = m0 + j < M ? (float)xb[tid + (m0 + j) * stride_m] : 0.f;
+    } else {  // k-major: 8 consecutive tokens per k row, 32 k rows per pass
+        const int j = tid & 7, kl = tid >> 3;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int k = kl + 32 * i;
+            tile[j][k] = m0 + j < M ? (float)xb[k * stride_k + (m0 + j) * stride_m] : 0.f;
+        }
+    }
+    __syncthreads();
+    const int64_t m = m0 + (tid >> 5);
     const int N = 2 * BN;
     uint8_t* rec = out + ((m / BN) * NB + b) * (int64_t)(512 * BN + 8 * BN);
     const int mm = (int)(m % BN);
@@ -1202,7 +1217,7 @@ __global__ void rotate_act_i8_kernel(const TX* __restrict__ x, int64_t NB, int64
     if (m < M) {
         float f[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) f[e] = (float)x[(b * 256 + lane + 32 * e) * stride_k + m * stride_m];
+        for (int e = 0; e < 8; ++e) f[e] = tile[tid >> 5][lane + 32 * e];
         bool bad = false;
 #pragma unroll
         for (int e = 0; e < 8; ++e) bad |= !isfinite(f[e]);
@@ -1304,7 +1319,7 @@ extern "C" int itq3_rotate_act_i8(const void* x, int x_dtype, int64_t cols, int6
     }
     const int BN = itq3_mmq8_block_n(m);
     const int64_t NB = cols / 256, M_pad = (m + BN - 1) / BN * BN;
-    const unsigned grid = (unsigned)((NB * M_pad * 32 + 255) / 256);
+    const dim3 grid((unsigned)NB, (unsigned)(M_pad / 8));
     cudaStream_t s = (cudaStream_t)stream;
     switch (x_dtype) {
         case ITQ3_F32:
