@@ -105,9 +105,13 @@ int itq3_gemv(const uint8_t* tiled, int64_t rows, int64_t cols, int asymmetric, 
 /* ---- K5 batched MMQ on tcgen05 tensor cores (csrc/mmq.cu): Y = w_hat @ X for M >= 16 tokens.
  * Weights: itq3_repack_mmq layout (2-bit codes, 66 B per 256 weights + padding to 128 rows);
  * activations: itq3_rotate_act_f16 (x'' = H x / 16 as f16, pre-swizzled token tiles of
- * itq3_mmq_block_n(m) tokens).  A = d*t is exact in f16; fp32 accumulation in TMEM. */
-int64_t itq3_mmq_nbytes(int64_t rows, int64_t cols, int asymmetric);
-int itq3_repack_mmq(const uint8_t* payload, int64_t rows, int64_t cols, int asymmetric, uint8_t* out, void* stream);
+ * itq3_mmq_block_n(m) tokens).  A = d*t is exact in f16; fp32 accumulation in TMEM.
+ * flags (nbytes / repack / mmq): ITQ3_MMQ_ASYM (asymmetric zero-points) | ITQ3_MMQ_SS (variant ss:
+ * 116-byte blocks, t scaled by the stored per-32 sub-scale, codec.py:134-161); block_n must be 256. */
+#define ITQ3_MMQ_ASYM 1
+#define ITQ3_MMQ_SS 2
+int64_t itq3_mmq_nbytes(int64_t rows, int64_t cols, int flags);
+int itq3_repack_mmq(const uint8_t* payload, int64_t rows, int64_t cols, int flags, uint8_t* out, void* stream);
 int itq3_mmq_block_n(int64_t m);
 int64_t itq3_mmq_act_nbytes(int64_t cols, int64_t m);
 /* nonfinite (nullable device u32): OR-ed with 1 if any input element is not finite -- fused_matmul's
@@ -120,7 +124,7 @@ int64_t itq3_mmq_ws_nbytes(int64_t rows, int64_t cols, int64_t m);
 /* diagnostics: device buffer of 16 u64 counters per CTA (cycle accounting per warp role of the next
  * itq3_mmq launches; tools/mmq_trace.py), or NULL to switch the accounting off. */
 int itq3_mmq_set_trace(void* buf);
-int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asymmetric, const uint8_t* act, int64_t m, void* y,
+int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int flags, const uint8_t* act, int64_t m, void* y,
              int y_dtype, int64_t stride_r, int64_t stride_m, void* workspace, void* stream);
 
 /* ---- generic fused matmul for every other layout (any block_n, variant ss,

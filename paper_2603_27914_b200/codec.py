@@ -170,14 +170,22 @@ class QuantizedTensor:
             self._mmq8[p.device] = t
         return self._mmq8[p.device]
 
+    def mmq_ok(self) -> bool:
+        """K5 (tcgen05 f16 MMQ) handles block_n 256 with cols % 256 == 0 in both variants."""
+        return self.block_n == 256 and self.cols % 256 == 0
+
+    def mmq_flags(self) -> int:
+        """itq3_mmq* flags: ITQ3_MMQ_ASYM (1) | ITQ3_MMQ_SS (2)."""
+        return (0 if self.symmetric else 1) | (2 if self.variant == "ss" else 0)
+
     def mmq_layout(self) -> torch.Tensor:
         """tcgen05 MMQ layout (csrc/mmq.cu: 2-bit codes in 64-k slabs, rows padded to 128)."""
         p = self.ensure_decodable()
         if p.device not in self._mmq:
-            asym = 0 if self.symmetric else 1
-            t = torch.empty(_lib.load().itq3_mmq_nbytes(self.rows, self.cols, asym), dtype=torch.uint8,
+            flags = self.mmq_flags()
+            t = torch.empty(_lib.load().itq3_mmq_nbytes(self.rows, self.cols, flags), dtype=torch.uint8,
                             device=p.device)
-            _lib.call("itq3_repack_mmq", _lib.ptr(p), self.rows, self.cols, asym, _lib.ptr(t),
+            _lib.call("itq3_repack_mmq", _lib.ptr(p), self.rows, self.cols, flags, _lib.ptr(t),
                       _lib.stream_ptr(p.device))
             self._mmq[p.device] = t
         return self._mmq[p.device]

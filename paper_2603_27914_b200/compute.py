@@ -116,7 +116,8 @@ def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, 
         if flag is not None:
             _raise_if_nonfinite(flag)
         return Y
-    if q.fast_layout() and out_dtype != torch.float64 and k >= MMQ_MIN_TOKENS:
+    if q.mmq_ok() and out_dtype != torch.float64 and k >= MMQ_MIN_TOKENS:
+        # K5: variant s for k > MMQ8_MAX_TOKENS, and variant ss (per-32 sub-scales) for every k >= 16
         mmq = q.mmq_layout()
         s = _lib.stream_ptr(dev)
         act = torch.empty(_lib.load().itq3_mmq_act_nbytes(cols, k), dtype=torch.uint8, device=dev)
@@ -126,7 +127,7 @@ def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, 
         Y = torch.empty((rows, k), dtype=out_dtype, device=dev)
         wsn = _lib.load().itq3_mmq_ws_nbytes(rows, cols, k)
         ws = torch.empty(wsn, dtype=torch.uint8, device=dev) if wsn else None
-        _lib.call("itq3_mmq", _lib.ptr(mmq), rows, cols, int(not q.symmetric), _lib.ptr(act), k, _lib.ptr(Y),
+        _lib.call("itq3_mmq", _lib.ptr(mmq), rows, cols, q.mmq_flags(), _lib.ptr(act), k, _lib.ptr(Y),
                   _lib.TORCH_DTYPE_CODE[out_dtype], Y.stride(0), Y.stride(1), _lib.ptr(ws) if ws is not None else None,
                   s)
         if flag is not None:
@@ -166,7 +167,7 @@ def fused_matmul(q: QuantizedTensor, x, *, limbs: int | None = None, check_finit
             x = x.to(torch.float32)
         parity = x.dtype == torch.float64
         # the MMQ paths (k >= 16, perf mode) check finiteness inside their activation rotation
-        if check_finite and (parity or x.shape[1] < MMQ_MIN_TOKENS or not q.fast_layout()):
+        if check_finite and (parity or x.shape[1] < MMQ_MIN_TOKENS or not q.mmq_ok()):
             if not bool(torch.isfinite(x).all()):
                 raise DomainError("fused_matmul: X contains non-finite values")
         L = limbs or (PARITY_LIMBS if parity else perf_limbs(x.shape[1]))

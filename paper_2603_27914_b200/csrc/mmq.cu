@@ -144,6 +144,11 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
     return v;
 }
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ uint16_t lds16(uint32_t a) {
     uint16_t v;
     asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
@@ -181,12 +186,14 @@ __device__ unsigned long long* g_mmq_trace = nullptr;
 // a 128-k stage of f16 d*t, two k per 32-bit column).
 constexpr int kStK = 128;                       // k per stage
 constexpr int kWRec = 4096 + 256 + 128;         // weight record: codes [2 halves][128 rows][16 B] | f16 scales | int8 zps
+constexpr int kWRecSS = 4096 + 1024 + 128;      // variant ss: codes | f16 sub-scales [128 rows][4 per stage] | int8 zps
+constexpr int kMmqAsym = 1, kMmqSubScales = 2;  // itq3_mmq* flags
 constexpr int kPairNS = 4;  // stages in flight: load slot s and A slot s are freed by ONE commit (a
                              // tcgen05.commit costs the tensor pipe ~100-170 cycles; tc_f16_pair_probe)
 constexpr int kPairStage = 132;  // fp32 words per staged output row (128 + 4 pad: conflict-free v4 stores)
 struct PairSmem {
     uint8_t b[kPairNS][128 * 2 * 128];  // B half tile: 2 x (128 token rows x 64 k f16, SW128 K-major), 1024-aligned
-    uint8_t w[kPairNS][kWRec];          // weight record of the stage (this CTA's 128 rows)
+    uint8_t w[kPairNS][kWRecSS];        // weight record of the stage (this CTA's 128 rows)
     float stage[kMmqBM][kPairStage];    // epilogue staging for the bulk row stores
     uint64_t full[kPairNS];    // this CTA's weight record + B half landed (TMA)
     uint64_t empty[kPairNS];   // the pair's MMAs consumed stage slot s: smem slot + A slot (multicast commit)
@@ -228,7 +235,7 @@ struct PairWork {
 
 template <int BN, typename TY>  // BN = tokens per pair tile (256, or 128 for M <= 128)
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
-    mmq_pair_kernel(const uint8_t* __restrict__ wrec, int asym, PairWork wk, const uint8_t* __restrict__ act,
+    mmq_pair_kernel(const uint8_t* __restrict__ wrec, int flags, PairWork wk, const uint8_t* __restrict__ act,
                     int64_t rows, int64_t M, TY* __restrict__ y, int64_t stride_r, int64_t stride_m, int64_t slab,
                     float* __restrict__ tailws) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -260,6 +267,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
     const uint32_t tmem = sm.tmem_base;
     // diagnostics only (tools/mmq_trace.py --flags): 1 = no B loads, 2 = no A stores
     const unsigned dflags = g_mmq_trace ? (unsigned)g_mmq_trace[4095 * 16] : 0u;
+    const bool asym = flags & kMmqAsym, ss = flags & kMmqSubScales;
+    const int wbytes = ss ? kWRecSS : kWRec;
 
     if (warp == 0) {
         if (lane == 0) {  // producer: this CTA's weight record and 64-token half of B, one copy each per stage
@@ -270,7 +279,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
             for (int it = cluster; it < items; it += nclusters) {
                 int tr, tn, s0, s1, split;
                 wk.decode(it, tr, tn, s0, s1, split);
-                const uint8_t* wsrc = wrec + ((int64_t)(2 * tr + rank) * wk.NS) * kWRec;
+                const uint8_t* wsrc = wrec + ((int64_t)(2 * tr + rank) * wk.NS) * wbytes;
                 const uint8_t* bsrc = act + ((int64_t)(2 * tn + rank) * wk.NS) * (BN * 128);
                 for (int st = s0; st < s1; ++st, ++g) {
                     const int s = g % kPairNS;
@@ -280,8 +289,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
                         MMQ_ACC(0, tw);
                     }
                     const long long ti0 = clock64();
-                    mbar_expect_tx_(&sm.full[s], kWRec + ((dflags & 1) ? 0 : BN * 128));
-                    bulk_g2s_(sm.w[s], wsrc + (int64_t)st * kWRec, kWRec, &sm.full[s]);
+                    mbar_expect_tx_(&sm.full[s], wbytes + ((dflags & 1) ? 0 : BN * 128));
+                    bulk_g2s_(sm.w[s], wsrc + (int64_t)st * wbytes, wbytes, &sm.full[s]);
                     if (!(dflags & 1)) bulk_g2s_(sm.b[s], bsrc + (int64_t)st * (BN * 128), BN * 128, &sm.full[s]);
                     t_issue += clock64() - ti0;
                 }
@@ -365,12 +374,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
                 const long long tw0 = clock64();
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t wa = smem_addr(sm.w[s]);
-                const uint16_t dh = lds16(wa + 4096 + 2 * r);
-                const int z = asym ? lds_s8(wa + 4352 + r) : 0;
-                const __half d = __ushort_as_half(dh);
-                const __half ndz = __hmul(d, __int2half_rn(-1 - z));  // exact: -(1 + z) in {0,-1,-2}
-                const uint32_t d2 = (uint32_t)dh | ((uint32_t)dh << 16);
-                const uint32_t ndz2 = (uint32_t)__half_as_ushort(ndz) * 0x10001u;
+                // scale of each 32-k sub-block of the stage: the block scale (variant s) or the
+                // row's four stored sub-scales (variant ss: y = d_m (c - 1 - z), codec.py:152-161)
+                uint32_t dh[4];
+                if (ss) {
+                    const uint2 v = lds64(wa + 4096 + 8 * r);
+                    dh[0] = v.x & 0xffffu, dh[1] = v.x >> 16, dh[2] = v.y & 0xffffu, dh[3] = v.y >> 16;
+                } else {
+                    dh[0] = dh[1] = dh[2] = dh[3] = lds16(wa + 4096 + 2 * r);
+                }
+                const int z = asym ? lds_s8(wa + (ss ? kWRecSS - 128 : kWRec - 128) + r) : 0;
+                const __half nz1 = __int2half_rn(-1 - z);  // exact: -(1 + z) in {0,-1,-2}
+                uint32_t d2[4], ndz2[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    d2[i] = dh[i] * 0x10001u;
+                    ndz2[i] = (uint32_t)__half_as_ushort(__hmul(__ushort_as_half((uint16_t)dh[i]), nz1)) * 0x10001u;
+                }
 #pragma unroll
                 for (int j = 0; j < 2; ++j) {  // 64-k half j of the stage: A columns 32 j .. 32 j + 31
                     const uint4 w4 = lds128(wa + 2048 * j + 16 * r);
@@ -383,8 +403,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
                             const uint32_t v = ((wv[wi] >> (2 * m)) & 0x00030003u) | 0x64006400u;  // f16x2 1024 + c
                             __half2 hv =
                                 __hsub2(*reinterpret_cast<const __half2*>(&v), __floats2half2_rn(1024.f, 1024.f));
-                            hv = __hfma2(hv, *reinterpret_cast<const __half2*>(&d2),
-                                         *reinterpret_cast<const __half2*>(&ndz2));
+                            hv = __hfma2(hv, *reinterpret_cast<const __half2*>(&d2[2 * j + (wi >> 1)]),
+                                         *reinterpret_cast<const __half2*>(&ndz2[2 * j + (wi >> 1)]));
                             a[8 * wi + m] = *reinterpret_cast<uint32_t*>(&hv);
                         }
                     if (!(dflags & 2))
@@ -522,21 +542,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
 //   row's 64-k half holds k = 16w..16w+15: bits 2m..2m+1 = code of k = 16w + 2m, bits 16+2m.. =
 //   k = 16w + 2m + 1) | f16 scales [row] of the stage's 256-block | int8 zero-points [row].
 // ------------------------------------------------------------------------------------------
-__global__ void repack_mmq_kernel(const uint8_t* __restrict__ payload, int64_t rows, int64_t rows_pad, int NB, int asym,
+__global__ void repack_mmq_kernel(const uint8_t* __restrict__ payload, int64_t rows, int64_t rows_pad, int NB, int flags,
                                   uint8_t* __restrict__ out) {
+    const bool asym = flags & kMmqAsym, ss = flags & kMmqSubScales;
+    const int wbytes = ss ? kWRecSS : kWRec, bsize = ss ? 116 : 100;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (row, 64-chunk kc)
     const int NC = NB * 4, NS = NB * 2;
     if (idx >= rows_pad * NC) return;
     const int64_t row = idx / NC;
     const int kc = (int)(idx % NC);
     const int st = kc >> 1, j = kc & 1, b = kc >> 2;
-    uint8_t* rec = out + ((row >> 7) * NS + st) * (int64_t)kWRec;
+    uint8_t* rec = out + ((row >> 7) * NS + st) * (int64_t)wbytes;
     const int r = (int)(row & 127);
     uint32_t w[4] = {0, 0, 0, 0};
-    uint16_t sb = 0;
+    uint16_t sb = 0, sub[2] = {0, 0};
     int8_t z = 0;
     if (row < rows) {
-        const uint8_t* blk = payload + (row * NB + b) * 100;
+        const uint8_t* blk = payload + (row * NB + b) * bsize;
         const int kbase = (kc & 3) * 64;
         const uint32_t p0 = *reinterpret_cast<const uint32_t*>(blk + (kbase >> 3));
         const uint32_t p0b = *reinterpret_cast<const uint32_t*>(blk + (kbase >> 3) + 4);
@@ -551,9 +573,16 @@ __global__ void repack_mmq_kernel(const uint8_t* __restrict__ payload, int64_t r
         }
         sb = *reinterpret_cast<const uint16_t*>(blk + 96);
         if (asym) z = (int8_t)(int)f16_bits_to_f64(*reinterpret_cast<const uint16_t*>(blk + 98));
+        if (ss) {  // sub-scales of the chunk's two 32-k sub-blocks (block fields 100 + 2 i)
+            sub[0] = *reinterpret_cast<const uint16_t*>(blk + 100 + 4 * (kc & 3));
+            sub[1] = *reinterpret_cast<const uint16_t*>(blk + 102 + 4 * (kc & 3));
+        }
     }
     *reinterpret_cast<uint4*>(rec + 2048 * j + 16 * r) = make_uint4(w[0], w[1], w[2], w[3]);
-    if (j == 0) {
+    if (ss) {
+        *reinterpret_cast<uint32_t*>(rec + 4096 + 8 * r + 4 * j) = (uint32_t)sub[0] | ((uint32_t)sub[1] << 16);
+        if (j == 0) reinterpret_cast<int8_t*>(rec + kWRecSS - 128)[r] = z;
+    } else if (j == 0) {
         *reinterpret_cast<uint16_t*>(rec + 4096 + 2 * r) = sb;
         reinterpret_cast<int8_t*>(rec + 4352)[r] = z;
     }
@@ -709,12 +738,12 @@ using namespace itq3;
 
 static int mmq_rows_pad(int64_t rows) { return (int)((rows + 255) / 256 * 256); }  // whole CTA-pair tiles
 
-extern "C" int64_t itq3_mmq_nbytes(int64_t rows, int64_t cols, int asymmetric) {
-    (void)asymmetric;  // the zero-point bytes are part of every record
-    return (int64_t)(mmq_rows_pad(rows) / 128) * (cols / kStK) * kWRec;
+extern "C" int64_t itq3_mmq_nbytes(int64_t rows, int64_t cols, int flags) {
+    // the zero-point bytes are part of every record; variant ss records carry four sub-scales per row
+    return (int64_t)(mmq_rows_pad(rows) / 128) * (cols / kStK) * ((flags & kMmqSubScales) ? kWRecSS : kWRec);
 }
 
-extern "C" int itq3_repack_mmq(const uint8_t* payload, int64_t rows, int64_t cols, int asymmetric, uint8_t* out,
+extern "C" int itq3_repack_mmq(const uint8_t* payload, int64_t rows, int64_t cols, int flags, uint8_t* out,
                                void* stream) {
     if (rows <= 0 || cols <= 0 || cols % 256) {
         set_error("itq3_repack_mmq: needs cols %% 256 == 0 (got %lld x %lld)", (long long)rows, (long long)cols);
@@ -723,7 +752,7 @@ extern "C" int itq3_repack_mmq(const uint8_t* payload, int64_t rows, int64_t col
     const int64_t rp = mmq_rows_pad(rows);
     const int NB = (int)(cols / 256);
     const int64_t n = rp * NB * 4;
-    repack_mmq_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(payload, rows, rp, NB, asymmetric,
+    repack_mmq_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(payload, rows, rp, NB, flags,
                                                                                      out);
     return check_launch("itq3_repack_mmq");
 }
@@ -894,7 +923,7 @@ extern "C" int64_t itq3_mmq_ws_nbytes(int64_t rows, int64_t cols, int64_t m) {
     return R ? (int64_t)R * kt * 256 * BN * (int64_t)sizeof(float) : 0;
 }
 
-extern "C" int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asymmetric, const uint8_t* act, int64_t m,
+extern "C" int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int flags, const uint8_t* act, int64_t m,
                         void* y, int y_dtype, int64_t stride_r, int64_t stride_m, void* workspace, void* stream) {
     if (rows <= 0 || cols <= 0 || cols % 256 || m <= 0) {
         set_error("itq3_mmq: bad shape");
@@ -904,11 +933,11 @@ extern "C" int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym
     float* ws = (float*)workspace;
     const bool n128 = itq3_mmq_block_n(m) == 128;
     if (y_dtype == ITQ3_F32)
-        return n128 ? launch_mmq<128>(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, ws, s)
-                    : launch_mmq<256>(mmq, rows, cols, asymmetric, act, m, (float*)y, stride_r, stride_m, ws, s);
+        return n128 ? launch_mmq<128>(mmq, rows, cols, flags, act, m, (float*)y, stride_r, stride_m, ws, s)
+                    : launch_mmq<256>(mmq, rows, cols, flags, act, m, (float*)y, stride_r, stride_m, ws, s);
     if (y_dtype == ITQ3_BF16)
-        return n128 ? launch_mmq<128>(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s)
-                    : launch_mmq<256>(mmq, rows, cols, asymmetric, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s);
+        return n128 ? launch_mmq<128>(mmq, rows, cols, flags, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s)
+                    : launch_mmq<256>(mmq, rows, cols, flags, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s);
     set_error("itq3_mmq: output dtype must be float32 or bfloat16");
     return ITQ3_E_DOMAIN;
 }

@@ -19,14 +19,15 @@ pytestmark = pytest.mark.gpu
 P = pytest.importorskip("paper_2603_27914_b200")
 
 
-def mmq_bound(payload, rows, cols, X):
+def mmq_bound(payload, rows, cols, X, ss=False):
     n = 256
     nb = cols // n
-    deq = O.dequantize(payload, rows, cols, n, False)
-    quants, sb, zb, _ = O.split_payload(payload, n, False)
+    deq = O.dequantize(payload, rows, cols, n, ss)
+    quants, sb, zb, sub = O.split_payload(payload, n, ss)
     codes, _ = O.unpack_planes(quants, n)
     t = codes.astype(np.float64) - np.trunc(O.f16_value(zb))[:, None]
-    a = np.abs(t * O.f16_value(sb)[:, None]).reshape(rows, cols)        # |d t| per (row, k)
+    d = np.repeat(O.f16_value(sub), n // 8, axis=1) if ss else O.f16_value(sb)[:, None]
+    a = np.abs(t * d).reshape(rows, cols)                                # |d t| per (row, k)
     Xd = np.asarray(X, np.float64)
     xr = O.butterfly(Xd.T.reshape(-1, nb, n)).reshape(-1, cols).T / 16.0  # x'' (cols x m)
     l1 = np.abs(Xd).reshape(nb, n, -1).sum(axis=1)                      # (nb, m)
@@ -111,3 +112,17 @@ def test_mmq_nonfinite_input_raises(m, bad):
     X[300, m - 1] = 0.0
     Y = P.fused_matmul(q, X)  # clean call afterwards
     assert torch.isfinite(Y).all()
+
+
+@pytest.mark.parametrize("rows,cols,m", [(300, 512, 16), (1000, 768, 64), (4352, 1024, 300), (640, 256, 2048)])
+@pytest.mark.parametrize("asym", [False, True])
+def test_mmq_sub_scales(rows, cols, m, asym):
+    """Variant ss (per-32 sub-scales, 116-byte blocks) on K5: A = d_m t with the sub-block's scale."""
+    rng = np.random.default_rng(rows + m)
+    w = rng.standard_normal((rows, cols)) * np.repeat(rng.uniform(0.01, 0.3, (1, cols // 32)), 32, axis=1)
+    q = P.quantize_tensor(w, P.QuantConfig(variant="ss", symmetric=not asym))
+    assert q.mmq_ok() and not q.fast_layout()
+    X = rng.standard_normal((cols, m)).astype(np.float32)
+    Y = P.fused_matmul(q, torch.from_numpy(X).cuda()).cpu().numpy().astype(np.float64)
+    exact, bound = mmq_bound(q.payload().cpu().numpy(), rows, cols, X, ss=True)
+    assert np.all(np.abs(Y - exact) <= bound), np.max(np.abs(Y - exact) / bound)
