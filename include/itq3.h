@@ -106,12 +106,20 @@ int itq3_gemv(const uint8_t* tiled, int64_t rows, int64_t cols, int asymmetric, 
  * Weights: itq3_repack_mmq layout (2-bit codes, 66 B per 256 weights + padding to 128 rows);
  * activations: itq3_rotate_act_f16 (x'' = H x / 16 as f16, pre-swizzled token tiles of
  * itq3_mmq_block_n(m) tokens).  A = d*t is exact in f16; fp32 accumulation in TMEM.
- * flags (nbytes / repack / mmq): ITQ3_MMQ_ASYM (asymmetric zero-points) | ITQ3_MMQ_SS (variant ss:
- * 116-byte blocks, t scaled by the stored per-32 sub-scale, codec.py:134-161); block_n must be 256. */
+ * flags (nbytes / repack / mmq): ITQ3_MMQ_ASYM (asymmetric zero-points) | ITQ3_MMQ_PER32 (records with a
+ * scale and zero-point per 32-k group: variant ss -- t scaled by the stored per-32 sub-scale,
+ * codec.py:134-161 -- or block_n != 256).  itq3_repack_mmq covers block_n 256 (ITQ3_MMQ_PER32 there
+ * means variant ss); itq3_repack_mmq_n any block_n in {32..512} with cols % block_n == 0 (variant ss
+ * needs block_n >= 256) and always writes PER32 records.  The matching activations come from
+ * itq3_rotate_act_f16_n with the same block_n (x'' = H_n x / sqrt(n)). */
 #define ITQ3_MMQ_ASYM 1
-#define ITQ3_MMQ_SS 2
+#define ITQ3_MMQ_PER32 2
 int64_t itq3_mmq_nbytes(int64_t rows, int64_t cols, int flags);
 int itq3_repack_mmq(const uint8_t* payload, int64_t rows, int64_t cols, int flags, uint8_t* out, void* stream);
+int itq3_repack_mmq_n(const uint8_t* payload, int64_t rows, int64_t cols, int block_n, int variant_ss, int asymmetric,
+                      uint8_t* out, void* stream);
+int itq3_rotate_act_f16_n(const void* x, int x_dtype, int64_t cols, int64_t m, int64_t stride_k, int64_t stride_m,
+                          int block_n, uint8_t* out, unsigned* nonfinite, void* stream);
 int itq3_mmq_block_n(int64_t m);
 int64_t itq3_mmq_act_nbytes(int64_t cols, int64_t m);
 /* nonfinite (nullable device u32): OR-ed with 1 if any input element is not finite -- fused_matmul's

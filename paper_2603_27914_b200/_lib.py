@@ -45,6 +45,8 @@ SIGNATURES = {
     "itq3_matmul_generic": (_i32, [_vp, _i64, _i64, _i32, _i32, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "itq3_mmq_nbytes": (_i64, [_i64, _i64, _i32]),
     "itq3_repack_mmq": (_i32, [_vp, _i64, _i64, _i32, _vp, _vp]),
+    "itq3_repack_mmq_n": (_i32, [_vp, _i64, _i64, _i32, _i32, _i32, _vp, _vp]),
+    "itq3_rotate_act_f16_n": (_i32, [_vp, _i32, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _vp]),
     "itq3_mmq_block_n": (_i32, [_i64]),
     "itq3_mmq_act_nbytes": (_i64, [_i64, _i64]),
     "itq3_rotate_act_f16": (_i32, [_vp, _i32, _i64, _i64, _i64, _i64, _vp, _vp, _vp]),

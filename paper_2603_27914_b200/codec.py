@@ -171,12 +171,14 @@ class QuantizedTensor:
         return self._mmq8[p.device]
 
     def mmq_ok(self) -> bool:
-        """K5 (tcgen05 f16 MMQ) handles block_n 256 with cols % 256 == 0 in both variants."""
-        return self.block_n == 256 and self.cols % 256 == 0
+        """K5 (tcgen05 f16 MMQ) handles cols % 256 == 0 with whole blocks per row, block_n 32..256
+        (variant ss: block_n 256, whose sub-blocks are 32 wide)."""
+        return (self.cols % 256 == 0 and self.block_n <= 256 and self.cols % self.block_n == 0
+                and (self.variant == "s" or self.block_n == 256))
 
     def mmq_flags(self) -> int:
-        """itq3_mmq* flags: ITQ3_MMQ_ASYM (1) | ITQ3_MMQ_SS (2)."""
-        return (0 if self.symmetric else 1) | (2 if self.variant == "ss" else 0)
+        """itq3_mmq* flags: ITQ3_MMQ_ASYM (1) | ITQ3_MMQ_PER32 (2: variant ss or block_n != 256)."""
+        return (0 if self.symmetric else 1) | (2 if (self.variant == "ss" or self.block_n != 256) else 0)
 
     def mmq_layout(self) -> torch.Tensor:
         """tcgen05 MMQ layout (csrc/mmq.cu: 2-bit codes in 64-k slabs, rows padded to 128)."""
@@ -185,8 +187,12 @@ class QuantizedTensor:
             flags = self.mmq_flags()
             t = torch.empty(_lib.load().itq3_mmq_nbytes(self.rows, self.cols, flags), dtype=torch.uint8,
                             device=p.device)
-            _lib.call("itq3_repack_mmq", _lib.ptr(p), self.rows, self.cols, flags, _lib.ptr(t),
-                      _lib.stream_ptr(p.device))
+            if flags & 2:  # per-32 records: variant ss or block_n != 256
+                _lib.call("itq3_repack_mmq_n", _lib.ptr(p), self.rows, self.cols, self.block_n,
+                          int(self.variant == "ss"), int(not self.symmetric), _lib.ptr(t), _lib.stream_ptr(p.device))
+            else:
+                _lib.call("itq3_repack_mmq", _lib.ptr(p), self.rows, self.cols, flags, _lib.ptr(t),
+                          _lib.stream_ptr(p.device))
             self._mmq[p.device] = t
         return self._mmq[p.device]
 

@@ -117,13 +117,13 @@ def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, 
             _raise_if_nonfinite(flag)
         return Y
     if q.mmq_ok() and out_dtype != torch.float64 and k >= MMQ_MIN_TOKENS:
-        # K5: variant s for k > MMQ8_MAX_TOKENS, and variant ss (per-32 sub-scales) for every k >= 16
+        # K5: block_n 256 variant s for k > MMQ8_MAX_TOKENS; variant ss and block_n 32..128 for every k >= 16
         mmq = q.mmq_layout()
         s = _lib.stream_ptr(dev)
         act = torch.empty(_lib.load().itq3_mmq_act_nbytes(cols, k), dtype=torch.uint8, device=dev)
         flag = _nonfinite_flag(dev) if check_finite else None
-        _lib.call("itq3_rotate_act_f16", _lib.ptr(X), _lib.TORCH_DTYPE_CODE[X.dtype], cols, k, X.stride(0),
-                  X.stride(1), _lib.ptr(act), _lib.ptr(flag) if flag is not None else None, s)
+        _lib.call("itq3_rotate_act_f16_n", _lib.ptr(X), _lib.TORCH_DTYPE_CODE[X.dtype], cols, k, X.stride(0),
+                  X.stride(1), q.block_n, _lib.ptr(act), _lib.ptr(flag) if flag is not None else None, s)
         Y = torch.empty((rows, k), dtype=out_dtype, device=dev)
         wsn = _lib.load().itq3_mmq_ws_nbytes(rows, cols, k)
         ws = torch.empty(wsn, dtype=torch.uint8, device=dev) if wsn else None

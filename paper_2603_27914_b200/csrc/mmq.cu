@@ -149,6 +149,11 @@ __device__ __forceinline__ uint2 lds64(uint32_t a) {
     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
     return v;
 }
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ uint16_t lds16(uint32_t a) {
     uint16_t v;
     asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
@@ -186,14 +191,16 @@ __device__ unsigned long long* g_mmq_trace = nullptr;
 // a 128-k stage of f16 d*t, two k per 32-bit column).
 constexpr int kStK = 128;                       // k per stage
 constexpr int kWRec = 4096 + 256 + 128;         // weight record: codes [2 halves][128 rows][16 B] | f16 scales | int8 zps
-constexpr int kWRecSS = 4096 + 1024 + 128;      // variant ss: codes | f16 sub-scales [128 rows][4 per stage] | int8 zps
-constexpr int kMmqAsym = 1, kMmqSubScales = 2;  // itq3_mmq* flags
+// per-32-k tables (variant ss, or block_n != 256): codes | f16 scale [128 rows][4 sub-blocks of 32 k] |
+// int8 zero-point [128 rows][4]: every 32-k group of a row has one scale and one zero-point
+constexpr int kWRecT = 4096 + 1024 + 512;
+constexpr int kMmqAsym = 1, kMmqPer32 = 2;  // itq3_mmq* flags
 constexpr int kPairNS = 4;  // stages in flight: load slot s and A slot s are freed by ONE commit (a
                              // tcgen05.commit costs the tensor pipe ~100-170 cycles; tc_f16_pair_probe)
 constexpr int kPairStage = 132;  // fp32 words per staged output row (128 + 4 pad: conflict-free v4 stores)
 struct PairSmem {
     uint8_t b[kPairNS][128 * 2 * 128];  // B half tile: 2 x (128 token rows x 64 k f16, SW128 K-major), 1024-aligned
-    uint8_t w[kPairNS][kWRecSS];        // weight record of the stage (this CTA's 128 rows)
+    uint8_t w[kPairNS][kWRecT];         // weight record of the stage (this CTA's 128 rows)
     float stage[kMmqBM][kPairStage];    // epilogue staging for the bulk row stores
     uint64_t full[kPairNS];    // this CTA's weight record + B half landed (TMA)
     uint64_t empty[kPairNS];   // the pair's MMAs consumed stage slot s: smem slot + A slot (multicast commit)
@@ -267,8 +274,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
     const uint32_t tmem = sm.tmem_base;
     // diagnostics only (tools/mmq_trace.py --flags): 1 = no B loads, 2 = no A stores
     const unsigned dflags = g_mmq_trace ? (unsigned)g_mmq_trace[4095 * 16] : 0u;
-    const bool asym = flags & kMmqAsym, ss = flags & kMmqSubScales;
-    const int wbytes = ss ? kWRecSS : kWRec;
+    const bool asym = flags & kMmqAsym, ss = flags & kMmqPer32;
+    const int wbytes = ss ? kWRecT : kWRec;
 
     if (warp == 0) {
         if (lane == 0) {  // producer: this CTA's weight record and 64-token half of B, one copy each per stage
@@ -374,22 +381,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
                 const long long tw0 = clock64();
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t wa = smem_addr(sm.w[s]);
-                // scale of each 32-k sub-block of the stage: the block scale (variant s) or the
-                // row's four stored sub-scales (variant ss: y = d_m (c - 1 - z), codec.py:152-161)
+                // scale and zero-point of each 32-k sub-block of the stage: the 256-block's (plain
+                // records) or the row's per-32 tables (variant ss: y = d_m (c - 1 - z), codec.py:152-161;
+                // block_n < 256: several blocks per stage)
                 uint32_t dh[4];
+                int zz[4];
                 if (ss) {
                     const uint2 v = lds64(wa + 4096 + 8 * r);
                     dh[0] = v.x & 0xffffu, dh[1] = v.x >> 16, dh[2] = v.y & 0xffffu, dh[3] = v.y >> 16;
+                    const uint32_t zw = asym ? lds32(wa + 5120 + 4 * r) : 0u;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) zz[i] = (int)(int8_t)(zw >> (8 * i));
                 } else {
                     dh[0] = dh[1] = dh[2] = dh[3] = lds16(wa + 4096 + 2 * r);
+                    zz[0] = zz[1] = zz[2] = zz[3] = asym ? lds_s8(wa + 4352 + r) : 0;
                 }
-                const int z = asym ? lds_s8(wa + (ss ? kWRecSS - 128 : kWRec - 128) + r) : 0;
-                const __half nz1 = __int2half_rn(-1 - z);  // exact: -(1 + z) in {0,-1,-2}
                 uint32_t d2[4], ndz2[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
+                for (int i = 0; i < 4; ++i) {  // exact: -(1 + z) in {0,-1,-2}
                     d2[i] = dh[i] * 0x10001u;
-                    ndz2[i] = (uint32_t)__half_as_ushort(__hmul(__ushort_as_half((uint16_t)dh[i]), nz1)) * 0x10001u;
+                    ndz2[i] = (uint32_t)__half_as_ushort(__hmul(__ushort_as_half((uint16_t)dh[i]),
+                                                                __int2half_rn(-1 - zz[i]))) * 0x10001u;
                 }
 #pragma unroll
                 for (int j = 0; j < 2; ++j) {  // 64-k half j of the stage: A columns 32 j .. 32 j + 31
@@ -544,21 +556,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
 // ------------------------------------------------------------------------------------------
 __global__ void repack_mmq_kernel(const uint8_t* __restrict__ payload, int64_t rows, int64_t rows_pad, int NB, int flags,
                                   uint8_t* __restrict__ out) {
-    const bool asym = flags & kMmqAsym, ss = flags & kMmqSubScales;
-    const int wbytes = ss ? kWRecSS : kWRec, bsize = ss ? 116 : 100;
+    const bool asym = flags & kMmqAsym;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (row, 64-chunk kc)
     const int NC = NB * 4, NS = NB * 2;
     if (idx >= rows_pad * NC) return;
     const int64_t row = idx / NC;
     const int kc = (int)(idx % NC);
     const int st = kc >> 1, j = kc & 1, b = kc >> 2;
-    uint8_t* rec = out + ((row >> 7) * NS + st) * (int64_t)wbytes;
+    uint8_t* rec = out + ((row >> 7) * NS + st) * (int64_t)kWRec;
     const int r = (int)(row & 127);
     uint32_t w[4] = {0, 0, 0, 0};
-    uint16_t sb = 0, sub[2] = {0, 0};
+    uint16_t sb = 0;
     int8_t z = 0;
     if (row < rows) {
-        const uint8_t* blk = payload + (row * NB + b) * bsize;
+        const uint8_t* blk = payload + (row * NB + b) * 100;
         const int kbase = (kc & 3) * 64;
         const uint32_t p0 = *reinterpret_cast<const uint32_t*>(blk + (kbase >> 3));
         const uint32_t p0b = *reinterpret_cast<const uint32_t*>(blk + (kbase >> 3) + 4);
@@ -573,19 +584,52 @@ __global__ void repack_mmq_kernel(const uint8_t* __restrict__ payload, int64_t r
         }
         sb = *reinterpret_cast<const uint16_t*>(blk + 96);
         if (asym) z = (int8_t)(int)f16_bits_to_f64(*reinterpret_cast<const uint16_t*>(blk + 98));
-        if (ss) {  // sub-scales of the chunk's two 32-k sub-blocks (block fields 100 + 2 i)
-            sub[0] = *reinterpret_cast<const uint16_t*>(blk + 100 + 4 * (kc & 3));
-            sub[1] = *reinterpret_cast<const uint16_t*>(blk + 102 + 4 * (kc & 3));
-        }
     }
     *reinterpret_cast<uint4*>(rec + 2048 * j + 16 * r) = make_uint4(w[0], w[1], w[2], w[3]);
-    if (ss) {
-        *reinterpret_cast<uint32_t*>(rec + 4096 + 8 * r + 4 * j) = (uint32_t)sub[0] | ((uint32_t)sub[1] << 16);
-        if (j == 0) reinterpret_cast<int8_t*>(rec + kWRecSS - 128)[r] = z;
-    } else if (j == 0) {
+    if (j == 0) {
         *reinterpret_cast<uint16_t*>(rec + 4096 + 2 * r) = sb;
         reinterpret_cast<int8_t*>(rec + 4352)[r] = z;
     }
+}
+
+// Per-32 tables (kWRecT records): any block_n in {32, ..., 512} with cols % block_n == 0, variant s
+// or ss (sub-block n / 8 >= 32).  Thread = (row, 64-k chunk): codes bit by bit from the planes of the
+// block(s) the chunk covers, then the scale and zero-point of each of its two 32-k groups.
+__global__ void repack_mmq_tables_kernel(const uint8_t* __restrict__ payload, int64_t rows, int64_t rows_pad,
+                                         int64_t cols, int n, int ss, int asym, uint8_t* __restrict__ out) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (row, 64-chunk kc)
+    const int NC = (int)(cols / 64), NS = (int)(cols / 128);
+    if (idx >= rows_pad * NC) return;
+    const int64_t row = idx / NC;
+    const int kc = (int)(idx % NC);
+    const int st = kc >> 1, j = kc & 1;
+    uint8_t* rec = out + ((row >> 7) * NS + st) * (int64_t)kWRecT;
+    const int r = (int)(row & 127);
+    const int q = 3 * n / 8, bsize = q + 4 + (ss ? 16 : 0), nbr = (int)(cols / n);
+    uint32_t w[4] = {0, 0, 0, 0};
+    uint16_t sc[2] = {0, 0};
+    int8_t zp[2] = {0, 0};
+    if (row < rows) {
+        for (int kk = 0; kk < 64; ++kk) {
+            const int64_t k = (int64_t)kc * 64 + kk;
+            const uint8_t* blk = payload + (row * nbr + k / n) * bsize;
+            const int o = (int)(k % n);
+            const uint32_t c = ((blk[o >> 3] >> (o & 7)) & 1u) | (((blk[n / 8 + (o >> 3)] >> (o & 7)) & 1u) << 1);
+            const int wi = kk >> 4, wk = kk & 15;
+            w[wi] |= c << ((wk & 1) ? 16 + 2 * (wk >> 1) : 2 * (wk >> 1));
+        }
+        for (int g = 0; g < 2; ++g) {
+            const int64_t k = (int64_t)kc * 64 + 32 * g;
+            const uint8_t* blk = payload + (row * nbr + k / n) * bsize;
+            const int o = (int)(k % n);
+            sc[g] = ss ? *reinterpret_cast<const uint16_t*>(blk + q + 4 + 2 * (o / (n / 8)))
+                       : *reinterpret_cast<const uint16_t*>(blk + q);
+            if (asym) zp[g] = (int8_t)(int)f16_bits_to_f64(*reinterpret_cast<const uint16_t*>(blk + q + 2));
+        }
+    }
+    *reinterpret_cast<uint4*>(rec + 2048 * j + 16 * r) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint32_t*>(rec + 4096 + 8 * r + 4 * j) = (uint32_t)sc[0] | ((uint32_t)sc[1] << 16);
+    *reinterpret_cast<uint16_t*>(rec + 5120 + 4 * r + 2 * j) = (uint16_t)((uint8_t)zp[0] | ((uint16_t)(uint8_t)zp[1] << 8));
 }
 
 // ------------------------------------------------------------------------------------------
@@ -619,7 +663,8 @@ __device__ __forceinline__ void load4(const __nv_bfloat16* p, float (&f)[4]) {
 template <typename TX>
 __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restrict__ x, int64_t M, int64_t stride_k,
                                                              int64_t stride_m, int64_t NC, int BN,
-                                                             uint8_t* __restrict__ out, unsigned* __restrict__ nonfinite) {
+                                                             uint8_t* __restrict__ out, unsigned* __restrict__ nonfinite,
+                                                             int logn, float inv_sqrt_n) {
     // fp32 inputs, token-major (257: conflict-free transposes)
     pdl_release();
     __shared__ __align__(16) float tile[32][257];
@@ -668,8 +713,12 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
         }
     // fused_matmul's DomainError check (compute.py): one flag word, set if any input is not finite
     if (nonfinite && __any_sync(FULL, bad) && lane == 0) atomicOr(nonfinite, 1u);
+    // block_n = 2^logn <= 256: only the stages of k bits < logn (register index bit i is k bit i for
+    // i < 2, k bit i + 3 above; lane bit i is k bit i + 2)
 #pragma unroll
-    for (int hh = 1; hh < 32; hh <<= 1)
+    for (int i = 0; i < 5; ++i) {
+        if ((i < 2 ? i : i + 3) >= logn) continue;
+        const int hh = 1 << i;
 #pragma unroll
         for (int r = 0; r < 32; ++r)
             if ((r & hh) == 0) {
@@ -677,8 +726,11 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
                 v[r] = lo + hi;
                 v[r + hh] = lo - hi;
             }
+    }
 #pragma unroll
-    for (int h = 1; h < 8; h <<= 1) {
+    for (int i = 0; i < 3; ++i) {
+        if (i + 2 >= logn) continue;
+        const int h = 1 << i;
         const bool high = (lane & h) != 0;
 #pragma unroll
         for (int r = 0; r < 32; ++r) {
@@ -696,8 +748,8 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
         const int64_t k = b * 256 + 32 * kh + 4 * kq;
         const int64_t kc = k >> 6;
         const int kk = (int)(k & 63);
-        const __half2 p0 = __floats2half2_rn(v[4 * kh] * 0.0625f, v[4 * kh + 1] * 0.0625f);
-        const __half2 p1 = __floats2half2_rn(v[4 * kh + 2] * 0.0625f, v[4 * kh + 3] * 0.0625f);
+        const __half2 p0 = __floats2half2_rn(v[4 * kh] * inv_sqrt_n, v[4 * kh + 1] * inv_sqrt_n);
+        const __half2 p1 = __floats2half2_rn(v[4 * kh + 2] * inv_sqrt_n, v[4 * kh + 3] * inv_sqrt_n);
         uint8_t* t = out + (half * NC + kc) * (int64_t)(hb * 128) + sw128_off(row, kk >> 3) + (kk & 7) * 2;
         *reinterpret_cast<uint2*>(t) = make_uint2(*reinterpret_cast<const uint32_t*>(&p0),
                                                   *reinterpret_cast<const uint32_t*>(&p1));
@@ -739,9 +791,26 @@ using namespace itq3;
 static int mmq_rows_pad(int64_t rows) { return (int)((rows + 255) / 256 * 256); }  // whole CTA-pair tiles
 
 extern "C" int64_t itq3_mmq_nbytes(int64_t rows, int64_t cols, int flags) {
-    // the zero-point bytes are part of every record; variant ss records carry four sub-scales per row
-    return (int64_t)(mmq_rows_pad(rows) / 128) * (cols / kStK) * ((flags & kMmqSubScales) ? kWRecSS : kWRec);
+    // the zero-point bytes are part of every record; per-32 records carry four scales and zero-points per row
+    return (int64_t)(mmq_rows_pad(rows) / 128) * (cols / kStK) * ((flags & kMmqPer32) ? kWRecT : kWRec);
 }
+
+extern "C" int itq3_repack_mmq_n(const uint8_t* payload, int64_t rows, int64_t cols, int block_n, int variant_ss,
+                                 int asymmetric, uint8_t* out, void* stream) {
+    if (rows <= 0 || cols <= 0 || cols % 256 || block_n < 32 || block_n > 512 || (block_n & (block_n - 1)) ||
+        cols % block_n || (variant_ss && block_n < 256)) {
+        set_error("itq3_repack_mmq_n: needs cols %% 256 == 0, cols %% block_n == 0, block_n in 32..512 "
+                  "(>= 256 for variant ss) (got %lld x %lld, block_n %d)", (long long)rows, (long long)cols, block_n);
+        return ITQ3_E_UNSUPPORTED;
+    }
+    const int64_t rp = mmq_rows_pad(rows);
+    const int64_t n = rp * (cols / 64);
+    repack_mmq_tables_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        payload, rows, rp, cols, block_n, variant_ss, asymmetric, out);
+    return check_launch("itq3_repack_mmq_n");
+}
+
+extern "C" int itq3_repack_mmq_n(const uint8_t*, int64_t, int64_t, int, int, int, uint8_t*, void*);
 
 extern "C" int itq3_repack_mmq(const uint8_t* payload, int64_t rows, int64_t cols, int flags, uint8_t* out,
                                void* stream) {
@@ -749,6 +818,8 @@ extern "C" int itq3_repack_mmq(const uint8_t* payload, int64_t rows, int64_t col
         set_error("itq3_repack_mmq: needs cols %% 256 == 0 (got %lld x %lld)", (long long)rows, (long long)cols);
         return ITQ3_E_UNSUPPORTED;
     }
+    if (flags & kMmqPer32)  // variant ss at block_n 256
+        return itq3_repack_mmq_n(payload, rows, cols, 256, 1, flags & kMmqAsym, out, stream);
     const int64_t rp = mmq_rows_pad(rows);
     const int NB = (int)(cols / 256);
     const int64_t n = rp * NB * 4;
@@ -765,12 +836,19 @@ extern "C" int64_t itq3_mmq_act_nbytes(int64_t cols, int64_t m) {
     return M_pad * cols * 2;
 }
 
-extern "C" int itq3_rotate_act_f16(const void* x, int x_dtype, int64_t cols, int64_t m, int64_t stride_k,
-                                   int64_t stride_m, uint8_t* out, unsigned* nonfinite, void* stream) {
+extern "C" int itq3_rotate_act_f16_n(const void* x, int x_dtype, int64_t cols, int64_t m, int64_t stride_k,
+                                     int64_t stride_m, int block_n, uint8_t* out, unsigned* nonfinite, void* stream) {
     if (cols <= 0 || cols % 256 || m <= 0) {
         set_error("itq3_rotate_act_f16: need cols %% 256 == 0 and m > 0");
         return ITQ3_E_SHAPE;
     }
+    if (block_n < 32 || block_n > 256 || (block_n & (block_n - 1))) {
+        set_error("itq3_rotate_act_f16: block_n must be a power of two in [32, 256] (got %d)", block_n);
+        return ITQ3_E_UNSUPPORTED;
+    }
+    const int logn = 31 - __builtin_clz((unsigned)block_n);
+    // x'' = H_n x / sqrt(n): 1/16 exactly at n = 256; fl32(1/sqrt(n)) otherwise (fwht_inverse, transform.py:86-87)
+    const float isn = (float)(1.0 / sqrt((double)block_n));
     const int BN = itq3_mmq_block_n(m);
     const int64_t NB = cols / 256, M_pad = (m + BN - 1) / BN * BN;
     const dim3 grid((unsigned)(M_pad / 32), (unsigned)NB);
@@ -778,25 +856,30 @@ extern "C" int itq3_rotate_act_f16(const void* x, int x_dtype, int64_t cols, int
     switch (x_dtype) {
         case ITQ3_F32:
             rotate_act_f16_kernel<float><<<grid, 256, 0, s>>>((const float*)x, m, stride_k, stride_m, NB * 4, BN, out,
-                                                             nonfinite);
+                                                             nonfinite, logn, isn);
             break;
         case ITQ3_F64:
             rotate_act_f16_kernel<double><<<grid, 256, 0, s>>>((const double*)x, m, stride_k, stride_m, NB * 4, BN, out,
-                                                             nonfinite);
+                                                             nonfinite, logn, isn);
             break;
         case ITQ3_BF16:
             rotate_act_f16_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, m, stride_k, stride_m,
-                                                                      NB * 4, BN, out, nonfinite);
+                                                                      NB * 4, BN, out, nonfinite, logn, isn);
             break;
         case ITQ3_F16:
             rotate_act_f16_kernel<__half><<<grid, 256, 0, s>>>((const __half*)x, m, stride_k, stride_m, NB * 4, BN, out,
-                                                             nonfinite);
+                                                             nonfinite, logn, isn);
             break;
         default:
             set_error("itq3_rotate_act_f16: unsupported dtype %d", x_dtype);
             return ITQ3_E_DOMAIN;
     }
-    return check_launch("itq3_rotate_act_f16");
+    return check_launch("itq3_rotate_act_f16_n");
+}
+
+extern "C" int itq3_rotate_act_f16(const void* x, int x_dtype, int64_t cols, int64_t m, int64_t stride_k,
+                                   int64_t stride_m, uint8_t* out, unsigned* nonfinite, void* stream) {
+    return itq3_rotate_act_f16_n(x, x_dtype, cols, m, stride_k, stride_m, 256, out, nonfinite, stream);
 }
 
 static int mmq_max_clusters() {

@@ -19,8 +19,7 @@ pytestmark = pytest.mark.gpu
 P = pytest.importorskip("paper_2603_27914_b200")
 
 
-def mmq_bound(payload, rows, cols, X, ss=False):
-    n = 256
+def mmq_bound(payload, rows, cols, X, ss=False, n=256):
     nb = cols // n
     deq = O.dequantize(payload, rows, cols, n, ss)
     quants, sb, zb, sub = O.split_payload(payload, n, ss)
@@ -29,9 +28,10 @@ def mmq_bound(payload, rows, cols, X, ss=False):
     d = np.repeat(O.f16_value(sub), n // 8, axis=1) if ss else O.f16_value(sb)[:, None]
     a = np.abs(t * d).reshape(rows, cols)                                # |d t| per (row, k)
     Xd = np.asarray(X, np.float64)
-    xr = O.butterfly(Xd.T.reshape(-1, nb, n)).reshape(-1, cols).T / 16.0  # x'' (cols x m)
+    rs = 1.0 / np.sqrt(n)
+    xr = O.butterfly(Xd.T.reshape(-1, nb, n)).reshape(-1, cols).T * rs   # x'' (cols x m)
     l1 = np.abs(Xd).reshape(nb, n, -1).sum(axis=1)                      # (nb, m)
-    term = 2.0 ** -10 * np.abs(xr) + 2.0 ** -18 * np.repeat(l1, n, axis=0) / 16.0
+    term = 2.0 ** -10 * np.abs(xr) + 2.0 ** -18 * np.repeat(l1, n, axis=0) * rs
     return deq @ Xd, a @ term + 1e-5 * (np.abs(deq) @ np.abs(Xd))
 
 
@@ -125,4 +125,20 @@ def test_mmq_sub_scales(rows, cols, m, asym):
     X = rng.standard_normal((cols, m)).astype(np.float32)
     Y = P.fused_matmul(q, torch.from_numpy(X).cuda()).cpu().numpy().astype(np.float64)
     exact, bound = mmq_bound(q.payload().cpu().numpy(), rows, cols, X, ss=True)
+    assert np.all(np.abs(Y - exact) <= bound), np.max(np.abs(Y - exact) / bound)
+
+
+@pytest.mark.parametrize("n", [32, 64, 128])
+@pytest.mark.parametrize("rows,cols,m", [(300, 512, 16), (1000, 768, 100), (640, 1024, 2048)])
+@pytest.mark.parametrize("asym", [False, True])
+def test_mmq_block_sizes(n, rows, cols, m, asym):
+    """block_n 32..128 on K5: per-32 scale/zero-point tables (several blocks per 128-k stage) and the
+    n-point activation rotation x'' = H_n x / sqrt(n)."""
+    rng = np.random.default_rng(n + rows + m)
+    w = rng.standard_normal((rows, cols)) * 0.05 + (0.02 if asym else 0.0)
+    q = P.quantize_tensor(w, P.QuantConfig(block_n=n, symmetric=not asym))
+    assert q.mmq_ok()
+    X = rng.standard_normal((cols, m)).astype(np.float32)
+    Y = P.fused_matmul(q, torch.from_numpy(X).cuda()).cpu().numpy().astype(np.float64)
+    exact, bound = mmq_bound(q.payload().cpu().numpy(), rows, cols, X, n=n)
     assert np.all(np.abs(Y - exact) <= bound), np.max(np.abs(Y - exact) / bound)

@@ -1,4 +1,5 @@
-"""Variant ss (per-32 sub-scales) on the fast MMQ path vs variant s and vs the generic fp64 kernel.
+"""Variant ss (per-32 sub-scales) and block_n 32..128 on the fast MMQ path vs block_n 256 variant s, and vs
+the generic fp64 kernel those formats took before.
 
     python tools/ss_bench.py [--rows 4096 --cols 4096] [--out profiles/r01/ss_mmq.json]
 
@@ -39,7 +40,9 @@ def main():
     g = torch.Generator(device=dev)
     g.manual_seed(0)
     w = torch.randn((a.rows, a.cols), generator=g, device=dev) / a.cols ** 0.5
-    qs = {v: P.quantize_tensor(w, P.QuantConfig(variant=v)) for v in ("s", "ss")}
+    qs = {"s": P.quantize_tensor(w), "ss": P.quantize_tensor(w, P.QuantConfig(variant="ss"))}
+    for n in (128, 64, 32):
+        qs[f"s{n}"] = P.quantize_tensor(w, P.QuantConfig(block_n=n))
     res = []
     for m in (16, 64, 256, 2048):
         X = torch.randn((a.cols, m), generator=g, device=dev)
