@@ -171,10 +171,10 @@ class QuantizedTensor:
         return self._mmq8[p.device]
 
     def mmq_ok(self) -> bool:
-        """K5 (tcgen05 f16 MMQ) handles cols % 256 == 0 with whole blocks per row, block_n 32..256
-        (variant ss: block_n 256, whose sub-blocks are 32 wide)."""
-        return (self.cols % 256 == 0 and self.block_n <= 256 and self.cols % self.block_n == 0
-                and (self.variant == "s" or self.block_n == 256))
+        """K5 (tcgen05 f16 MMQ) handles cols % 256 == 0 with whole blocks per row, every block_n
+        (variant ss: block_n >= 256, whose sub-blocks are at least 32 wide)."""
+        return (self.cols % 256 == 0 and self.cols % self.block_n == 0
+                and (self.variant == "s" or self.block_n >= 256))
 
     def mmq_flags(self) -> int:
         """itq3_mmq* flags: ITQ3_MMQ_ASYM (1) | ITQ3_MMQ_PER32 (2: variant ss or block_n != 256)."""

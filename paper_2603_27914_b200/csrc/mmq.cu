@@ -660,7 +660,7 @@ __device__ __forceinline__ void load4(const __nv_bfloat16* p, float (&f)[4]) {
     f[0] = a.x, f[1] = a.y, f[2] = b.x, f[3] = b.y;
 }
 
-template <typename TX>
+template <typename TX, int NH, bool ALL>
 __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restrict__ x, int64_t M, int64_t stride_k,
                                                              int64_t stride_m, int64_t NC, int BN,
                                                              uint8_t* __restrict__ out, unsigned* __restrict__ nonfinite,
@@ -670,7 +670,17 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
     __shared__ __align__(16) float tile[32][257];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t b = blockIdx.y, m0 = (int64_t)blockIdx.x * 32;  // adjacent CTAs: adjacent token groups (DRAM locality)
-    const TX* xb = x + b * 256 * stride_k;
+    // block_n 512: the CTA transforms both 256-halves of the block (kept in registers) and joins them
+    // with the k-bit-8 stage; otherwise one 256-k slice of n-blocks
+    constexpr int nh = NH;  // = 2 iff logn == 9 (a separate instantiation: the n <= 256 kernel keeps 48 registers)
+    const int tl = lane >> 3, kq = lane & 7, tok = 4 * warp + tl;
+    float vv[2][32];
+    bool bad = false;
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+    if (h2 >= nh) break;
+    if (h2) __syncthreads();  // every read of the first half is done before the tile is overwritten
+    const TX* xb = x + (b * nh + h2) * 256 * stride_k;
     if (stride_k == 1 && stride_m != 1) {  // token-major input: threads along k
 #pragma unroll 4
         for (int j = 0; j < 32; ++j) {
@@ -701,9 +711,7 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
     // k bits 0..1 and 5..7 in registers (v[4 kh + j]: k = j + 4 (lane % 8) + 32 kh), so five of the
     // eight stages are register-only and three use shuffles (96 per thread instead of 160); the
     // smem reads are conflict-free (row pitch 257: bank = token + 4 (lane % 8) + const).
-    const int tl = lane >> 3, kq = lane & 7, tok = 4 * warp + tl;
-    float v[32];
-    bool bad = false;
+    float(&v)[32] = vv[h2];
 #pragma unroll
     for (int kh = 0; kh < 8; ++kh)
 #pragma unroll
@@ -711,13 +719,11 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
             v[4 * kh + j] = tile[tok][j + 4 * kq + 32 * kh];
             bad |= !isfinite(v[4 * kh + j]);
         }
-    // fused_matmul's DomainError check (compute.py): one flag word, set if any input is not finite
-    if (nonfinite && __any_sync(FULL, bad) && lane == 0) atomicOr(nonfinite, 1u);
     // block_n = 2^logn <= 256: only the stages of k bits < logn (register index bit i is k bit i for
     // i < 2, k bit i + 3 above; lane bit i is k bit i + 2)
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-        if ((i < 2 ? i : i + 3) >= logn) continue;
+        if (!ALL && (i < 2 ? i : i + 3) >= logn) continue;
         const int hh = 1 << i;
 #pragma unroll
         for (int r = 0; r < 32; ++r)
@@ -729,7 +735,7 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
     }
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-        if (i + 2 >= logn) continue;
+        if (!ALL && i + 2 >= logn) continue;
         const int h = 1 << i;
         const bool high = (lane & h) != 0;
 #pragma unroll
@@ -738,14 +744,29 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
             v[r] = high ? p - v[r] : v[r] + p;
         }
     }
+    }  // h2
+    // fused_matmul's DomainError check (compute.py): one flag word, set if any input is not finite
+    if (nonfinite && __any_sync(FULL, bad) && lane == 0) atomicOr(nonfinite, 1u);
+    if (nh == 2) {
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+            const float lo = vv[0][r], hi = vv[1][r];
+            vv[0][r] = lo + hi;
+            vv[1][r] = lo - hi;
+        }
+    }
     // 8-byte stores of 4 consecutive k of one token (a warp covers 4 tokens x 64 contiguous bytes)
     const int64_t m = m0 + tok;
     const int hb = BN / 2;                 // tokens per CTA half of a tile
     const int64_t half = m / hb;           // = 2 * tile + h
     const int row = (int)(m % hb);
 #pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+    if (h2 >= nh) break;
+    const float(&v)[32] = vv[h2];
+#pragma unroll
     for (int kh = 0; kh < 8; ++kh) {
-        const int64_t k = b * 256 + 32 * kh + 4 * kq;
+        const int64_t k = (b * nh + h2) * 256 + 32 * kh + 4 * kq;
         const int64_t kc = k >> 6;
         const int kk = (int)(k & 63);
         const __half2 p0 = __floats2half2_rn(v[4 * kh] * inv_sqrt_n, v[4 * kh + 1] * inv_sqrt_n);
@@ -754,6 +775,7 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
         *reinterpret_cast<uint2*>(t) = make_uint2(*reinterpret_cast<const uint32_t*>(&p0),
                                                   *reinterpret_cast<const uint32_t*>(&p1));
     }
+    }  // h2
 }
 
 // Sum the kt fp32 partials of the R tail tiles (fixed split order) into Y.
@@ -842,8 +864,8 @@ extern "C" int itq3_rotate_act_f16_n(const void* x, int x_dtype, int64_t cols, i
         set_error("itq3_rotate_act_f16: need cols %% 256 == 0 and m > 0");
         return ITQ3_E_SHAPE;
     }
-    if (block_n < 32 || block_n > 256 || (block_n & (block_n - 1))) {
-        set_error("itq3_rotate_act_f16: block_n must be a power of two in [32, 256] (got %d)", block_n);
+    if (block_n < 32 || block_n > 512 || (block_n & (block_n - 1)) || cols % block_n) {
+        set_error("itq3_rotate_act_f16: block_n must be a power of two in [32, 512] dividing cols (got %d)", block_n);
         return ITQ3_E_UNSUPPORTED;
     }
     const int logn = 31 - __builtin_clz((unsigned)block_n);
@@ -851,23 +873,23 @@ extern "C" int itq3_rotate_act_f16_n(const void* x, int x_dtype, int64_t cols, i
     const float isn = (float)(1.0 / sqrt((double)block_n));
     const int BN = itq3_mmq_block_n(m);
     const int64_t NB = cols / 256, M_pad = (m + BN - 1) / BN * BN;
-    const dim3 grid((unsigned)(M_pad / 32), (unsigned)NB);
+    const dim3 grid((unsigned)(M_pad / 32), (unsigned)(block_n > 256 ? NB / 2 : NB));
     cudaStream_t s = (cudaStream_t)stream;
     switch (x_dtype) {
         case ITQ3_F32:
-            rotate_act_f16_kernel<float><<<grid, 256, 0, s>>>((const float*)x, m, stride_k, stride_m, NB * 4, BN, out,
+            (block_n > 256 ? rotate_act_f16_kernel<float, 2, true> : block_n == 256 ? rotate_act_f16_kernel<float, 1, true> : rotate_act_f16_kernel<float, 1, false>)<<<grid, 256, 0, s>>>((const float*)x, m, stride_k, stride_m, NB * 4, BN, out,
                                                              nonfinite, logn, isn);
             break;
         case ITQ3_F64:
-            rotate_act_f16_kernel<double><<<grid, 256, 0, s>>>((const double*)x, m, stride_k, stride_m, NB * 4, BN, out,
+            (block_n > 256 ? rotate_act_f16_kernel<double, 2, true> : block_n == 256 ? rotate_act_f16_kernel<double, 1, true> : rotate_act_f16_kernel<double, 1, false>)<<<grid, 256, 0, s>>>((const double*)x, m, stride_k, stride_m, NB * 4, BN, out,
                                                              nonfinite, logn, isn);
             break;
         case ITQ3_BF16:
-            rotate_act_f16_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, m, stride_k, stride_m,
+            (block_n > 256 ? rotate_act_f16_kernel<__nv_bfloat16, 2, true> : block_n == 256 ? rotate_act_f16_kernel<__nv_bfloat16, 1, true> : rotate_act_f16_kernel<__nv_bfloat16, 1, false>)<<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, m, stride_k, stride_m,
                                                                       NB * 4, BN, out, nonfinite, logn, isn);
             break;
         case ITQ3_F16:
-            rotate_act_f16_kernel<__half><<<grid, 256, 0, s>>>((const __half*)x, m, stride_k, stride_m, NB * 4, BN, out,
+            (block_n > 256 ? rotate_act_f16_kernel<__half, 2, true> : block_n == 256 ? rotate_act_f16_kernel<__half, 1, true> : rotate_act_f16_kernel<__half, 1, false>)<<<grid, 256, 0, s>>>((const __half*)x, m, stride_k, stride_m, NB * 4, BN, out,
                                                              nonfinite, logn, isn);
             break;
         default:

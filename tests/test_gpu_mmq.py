@@ -128,8 +128,8 @@ def test_mmq_sub_scales(rows, cols, m, asym):
     assert np.all(np.abs(Y - exact) <= bound), np.max(np.abs(Y - exact) / bound)
 
 
-@pytest.mark.parametrize("n", [32, 64, 128])
-@pytest.mark.parametrize("rows,cols,m", [(300, 512, 16), (1000, 768, 100), (640, 1024, 2048)])
+@pytest.mark.parametrize("n", [32, 64, 128, 512])
+@pytest.mark.parametrize("rows,cols,m", [(300, 512, 16), (1000, 1536, 100), (640, 1024, 2048)])
 @pytest.mark.parametrize("asym", [False, True])
 def test_mmq_block_sizes(n, rows, cols, m, asym):
     """block_n 32..128 on K5: per-32 scale/zero-point tables (several blocks per 128-k stage) and the
@@ -141,4 +141,18 @@ def test_mmq_block_sizes(n, rows, cols, m, asym):
     X = rng.standard_normal((cols, m)).astype(np.float32)
     Y = P.fused_matmul(q, torch.from_numpy(X).cuda()).cpu().numpy().astype(np.float64)
     exact, bound = mmq_bound(q.payload().cpu().numpy(), rows, cols, X, n=n)
+    assert np.all(np.abs(Y - exact) <= bound), np.max(np.abs(Y - exact) / bound)
+
+
+@pytest.mark.parametrize("asym", [False, True])
+def test_mmq_sub_scales_512(asym):
+    """Variant ss at block_n 512: 64-wide sub-blocks, so both 32-k groups of a sub-block share its scale."""
+    rng = np.random.default_rng(51)
+    rows, cols, m = 700, 1536, 200
+    w = rng.standard_normal((rows, cols)) * np.repeat(rng.uniform(0.01, 0.3, (1, cols // 64)), 64, axis=1)
+    q = P.quantize_tensor(w, P.QuantConfig(block_n=512, variant="ss", symmetric=not asym))
+    assert q.mmq_ok()
+    X = rng.standard_normal((cols, m)).astype(np.float32)
+    Y = P.fused_matmul(q, torch.from_numpy(X).cuda()).cpu().numpy().astype(np.float64)
+    exact, bound = mmq_bound(q.payload().cpu().numpy(), rows, cols, X, ss=True, n=512)
     assert np.all(np.abs(Y - exact) <= bound), np.max(np.abs(Y - exact) / bound)
