@@ -73,6 +73,7 @@ class QuantizedTensor:
         self._tiled = {}
         self._mmq = {}
         self._mmq8 = {}
+        self._k5_range = None
         self._chain1 = {}  # device -> one-stage chain context of the k = 1 path (compute.py)
 
     # -- reference-compatible surface ------------------------------------------------------------
@@ -175,6 +176,18 @@ class QuantizedTensor:
         (variant ss: block_n >= 256, whose sub-blocks are at least 32 wide)."""
         return (self.cols % 256 == 0 and self.cols % self.block_n == 0
                 and (self.variant == "s" or self.block_n >= 256))
+
+    def k5_range_ok(self) -> bool:
+        """K5 forms A = d t in binary16: exact as long as |2 d| <= 65504, i.e. every stored scale (or
+        sub-scale) magnitude is below 2^15 and finite.  Checked once per tensor on the device; a tensor
+        with a larger scale takes a path with fp32 scales (K4 GEMV, or the exact generic kernel)."""
+        if self._k5_range is None:
+            p = self.ensure_decodable()
+            q = 3 * self.block_n // 8
+            lo, hi = (q + 4, q + 20) if self.variant == "ss" else (q, q + 2)
+            bits = p.reshape(-1, p.shape[-1])[:, lo:hi].contiguous().view(torch.int16)
+            self._k5_range = bool(((bits & 0x7FFF) <= 0x77FF).all()) if bits.numel() else True
+        return self._k5_range
 
     def mmq_flags(self) -> int:
         """itq3_mmq* flags: ITQ3_MMQ_ASYM (1) | ITQ3_MMQ_PER32 (2: variant ss or block_n != 256)."""

@@ -116,7 +116,7 @@ def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, 
         if flag is not None:
             _raise_if_nonfinite(flag)
         return Y
-    if q.mmq_ok() and out_dtype != torch.float64 and k >= MMQ_MIN_TOKENS:
+    if q.mmq_ok() and out_dtype != torch.float64 and k >= MMQ_MIN_TOKENS and q.k5_range_ok():
         # K5: block_n 256 variant s for k > MMQ8_MAX_TOKENS; variant ss and block_n 32..128 for every k >= 16
         mmq = q.mmq_layout()
         s = _lib.stream_ptr(dev)
@@ -167,7 +167,7 @@ def fused_matmul(q: QuantizedTensor, x, *, limbs: int | None = None, check_finit
             x = x.to(torch.float32)
         parity = x.dtype == torch.float64
         # the MMQ paths (k >= 16, perf mode) check finiteness inside their activation rotation
-        if check_finite and (parity or x.shape[1] < MMQ_MIN_TOKENS or not q.mmq_ok()):
+        if check_finite and (parity or x.shape[1] < MMQ_MIN_TOKENS or not (q.mmq_ok() and q.k5_range_ok())):
             if not bool(torch.isfinite(x).all()):
                 raise DomainError("fused_matmul: X contains non-finite values")
         L = limbs or (PARITY_LIMBS if parity else perf_limbs(x.shape[1]))

@@ -156,3 +156,20 @@ def test_mmq_sub_scales_512(asym):
     Y = P.fused_matmul(q, torch.from_numpy(X).cuda()).cpu().numpy().astype(np.float64)
     exact, bound = mmq_bound(q.payload().cpu().numpy(), rows, cols, X, ss=True, n=512)
     assert np.all(np.abs(Y - exact) <= bound), np.max(np.abs(Y - exact) / bound)
+
+
+@pytest.mark.parametrize("variant", ["s", "ss"])
+def test_mmq_huge_scale_takes_exact_path(variant):
+    """A block whose scale is >= 2^15 would overflow K5's binary16 A = d t; such tensors take a path
+    with fp32 scales instead (the K4 GEMV for the default format, the exact generic kernel otherwise),
+    so fused_matmul stays finite and within the perf-mode bound."""
+    rng = np.random.default_rng(77)
+    w = rng.standard_normal((256, 512)) * 0.05
+    w[3, :256] *= 2.0e6  # sigma ~1e5 -> stored scale saturates near 65504
+    q = P.quantize_tensor(w, P.QuantConfig(variant=variant))
+    assert not q.k5_range_ok()
+    X = rng.standard_normal((512, 100)).astype(np.float32)  # k > 64: the K5 range
+    Y = P.fused_matmul(q, torch.from_numpy(X).cuda()).cpu().numpy().astype(np.float64)
+    exact, bound = mmq_bound(q.payload().cpu().numpy(), 256, 512, X, ss=variant == "ss")
+    assert np.all(np.isfinite(Y))
+    assert np.all(np.abs(Y - exact) <= bound), np.max(np.abs(Y - exact) / bound)
