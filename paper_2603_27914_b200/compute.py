@@ -23,8 +23,8 @@ from .codec import QuantizedTensor
 from .errors import DomainError, ShapeError
 
 PARITY_LIMBS = 6
-MMQ_MIN_TOKENS = 16  # perf mode: k >= 16 columns go to the tcgen05 MMQ kernels (csrc/mmq.cu)
-MMQ8_MAX_TOKENS = 64  # ... 16 <= k <= 64 to the kind::i8 one (K5b), larger k to the kind::f16 one (K5)
+MMQ_MIN_TOKENS = 8  # perf mode: k >= 8 columns go to the tcgen05 MMQ kernels (csrc/mmq.cu; tools/crossover.py)
+MMQ8_MAX_TOKENS = 64  # ... 8 <= k <= 64 to the kind::i8 one (K5b), larger k to the kind::f16 one (K5)
 
 
 _NONFINITE: dict = {}
@@ -117,7 +117,7 @@ def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, 
             _raise_if_nonfinite(flag)
         return Y
     if q.mmq_ok() and out_dtype != torch.float64 and k >= MMQ_MIN_TOKENS and q.k5_range_ok():
-        # K5: block_n 256 variant s for k > MMQ8_MAX_TOKENS; variant ss and block_n 32..128 for every k >= 16
+        # K5: block_n 256 variant s for k > MMQ8_MAX_TOKENS; variant ss and block_n != 256 for every k >= MMQ_MIN_TOKENS
         mmq = q.mmq_layout()
         s = _lib.stream_ptr(dev)
         act = torch.empty(_lib.load().itq3_mmq_act_nbytes(cols, k), dtype=torch.uint8, device=dev)
@@ -166,7 +166,7 @@ def fused_matmul(q: QuantizedTensor, x, *, limbs: int | None = None, check_finit
         if x.dtype not in _lib.TORCH_DTYPE_CODE:
             x = x.to(torch.float32)
         parity = x.dtype == torch.float64
-        # the MMQ paths (k >= 16, perf mode) check finiteness inside their activation rotation
+        # the MMQ paths (k >= MMQ_MIN_TOKENS, perf mode) check finiteness inside their activation rotation
         if check_finite and (parity or x.shape[1] < MMQ_MIN_TOKENS or not (q.mmq_ok() and q.k5_range_ok())):
             if not bool(torch.isfinite(x).all()):
                 raise DomainError("fused_matmul: X contains non-finite values")

@@ -47,7 +47,7 @@ def matmul_bound(payload, rows, cols, X):
 
 
 @pytest.mark.parametrize("rows,cols", [(300, 512), (128, 1024), (1000, 256)])
-@pytest.mark.parametrize("m", [16, 64, 100, 256, 300])
+@pytest.mark.parametrize("m", [8, 12, 16, 64, 100, 256, 300])
 @pytest.mark.parametrize("asym", [False, True])
 def test_mmq_matches_exact(rows, cols, m, asym):
     rng = np.random.default_rng(rows + cols + m)
