@@ -134,6 +134,16 @@ int64_t itq3_mmq_ws_nbytes(int64_t rows, int64_t cols, int64_t m);
 int itq3_mmq_set_trace(void* buf);
 int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int flags, const uint8_t* act, int64_t m, void* y,
              int y_dtype, int64_t stride_r, int64_t stride_m, void* workspace, void* stream);
+/* Row-sharded MMQ with the output all-gather fused into the epilogue: this
+ * rank's `rows` weight rows are output rows [row0, row0 + rows) of a stage whose full Y lives on every
+ * rank; each finished row-half is written to all npeer copies (d_ypeers: device array of npeer
+ * pointers, e.g. torch symmetric-memory peer addresses over NVLink, each a full rows_total x m
+ * output with strides stride_r / stride_m) by one bulk copy per peer from the epilogue's staging row,
+ * or by the split reduce kernels when the workspace (itq3_mmq_ws_nbytes, may be NULL) splits K.
+ * The caller orders the peers' reads after every rank's launch (a symmetric-memory barrier). */
+int itq3_mmq_peers(const uint8_t* mmq, int64_t rows, int64_t cols, int flags, const uint8_t* act, int64_t m,
+                   const void* d_ypeers, int npeer, int64_t row0, int y_dtype, int64_t stride_r, int64_t stride_m,
+                   void* workspace, void* stream);
 
 /* ---- generic fused matmul for every other layout (any block_n, variant ss,
  * row-straddling blocks): fp64 exact decode + fp64 dot, deterministic block order.

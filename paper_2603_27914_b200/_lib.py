@@ -54,6 +54,7 @@ SIGNATURES = {
     "itq3_mmq_set_trace": (_i32, [_vp]),
     "itq3_dequant_set_trace": (_i32, [_vp]),
     "itq3_mmq": (_i32, [_vp, _i64, _i64, _i32, _vp, _i64, _vp, _i32, _i64, _i64, _vp, _vp]),
+    "itq3_mmq_peers": (_i32, [_vp, _i64, _i64, _i32, _vp, _i64, _vp, _i32, _i64, _i32, _i64, _i64, _vp, _vp]),
     "itq3_pack_codes": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp]),
     "itq3_unpack_codes": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp]),
     "itq3_mmq8_block_n": (_i32, [_i64]),

@@ -244,7 +244,8 @@ template <int BN, typename TY>  // BN = tokens per pair tile (256, or 128 for M 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
     mmq_pair_kernel(const uint8_t* __restrict__ wrec, int flags, PairWork wk, const uint8_t* __restrict__ act,
                     int64_t rows, int64_t M, TY* __restrict__ y, int64_t stride_r, int64_t stride_m, int64_t slab,
-                    float* __restrict__ tailws) {
+                    float* __restrict__ tailws, const unsigned long long* __restrict__ ypeer, int npeer,
+                    int64_t row0) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     PairSmem& sm = *reinterpret_cast<PairSmem*>(base);
@@ -450,6 +451,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
         const uint32_t td_row = tmem + ((uint32_t)(32 * q) << 16);
         const bool bulk_ok = stride_m == 1 && ((stride_r * (int64_t)sizeof(TY)) & 15) == 0 &&
                              (reinterpret_cast<uintptr_t>(y) & 15) == 0;
+        // Row-sharded output with the all-gather fused in (npeer > 0): output row row0 + grow goes to
+        // every rank's copy of Y (ypeer[p], NVLink peer addresses) -- one bulk copy of the staged
+        // row-half per peer, asynchronous like the local store.
+        bool peer_ok = npeer > 0 && stride_m == 1 && ((stride_r * (int64_t)sizeof(TY)) & 15) == 0;
+        for (int p = 0; p < npeer; ++p) peer_ok &= (ypeer[p] & 15) == 0;
         uint32_t t = 0;
         long long tw_dfull = 0;
         const long long te0 = clock64();
@@ -470,7 +476,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
 #pragma unroll 1
             for (int h = 0; h < BN / 128; ++h) {
                 const int64_t m0 = (int64_t)tn * BN + 128 * h;
-                const bool bulk = live && !tail && bulk_ok && m0 + 128 <= M;
+                const bool bulk = live && !tail && (npeer == 0 ? bulk_ok : peer_ok) && m0 + 128 <= M;
                 // the previous bulk store has finished reading the staging row
                 if (bulk) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 #pragma unroll
@@ -515,6 +521,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
 #pragma unroll
                         for (int j = 0; j < 32; j += 4)
                             *reinterpret_cast<uint4*>(pt + j) = make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    } else if (live && !tail && npeer > 0) {
+                        for (int p = 0; p < npeer; ++p) {
+                            TY* yp = reinterpret_cast<TY*>(ypeer[p]) + (row0 + grow) * stride_r;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                const int64_t m = m0 + 32 * c + j;
+                                if (m < M) yp[m * stride_m] = (TY)__uint_as_float(v[j]);
+                            }
+                        }
                     } else if (live) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
@@ -525,10 +540,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
                 }
                 if (bulk) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
-                                     yt + grow * stride_r + m0),
-                                 "r"(sa), "r"((uint32_t)(128 * sizeof(TY)))
-                                 : "memory");
+                    for (int p = 0; p < (npeer ? npeer : 1); ++p) {
+                        TY* dst = npeer ? reinterpret_cast<TY*>(ypeer[p]) + (row0 + grow) * stride_r + m0
+                                        : yt + grow * stride_r + m0;
+                        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(sa),
+                                     "r"((uint32_t)(128 * sizeof(TY)))
+                                     : "memory");
+                    }
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
             }
@@ -781,7 +799,8 @@ __global__ void __launch_bounds__(256) rotate_act_f16_kernel(const TX* __restric
 // Sum the kt fp32 partials of the R tail tiles (fixed split order) into Y.
 template <typename TY>
 __global__ void mmq_tail_reduce(const float* __restrict__ tws, int F, int R, int kt, int tiles_r, int BN, int64_t rows,
-                                int64_t M, TY* __restrict__ y, int64_t stride_r, int64_t stride_m) {
+                                int64_t M, TY* __restrict__ y, int64_t stride_r, int64_t stride_m,
+                                const unsigned long long* __restrict__ ypeer, int npeer, int64_t row0) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t per = (int64_t)256 * BN;
     if (i >= (int64_t)R * per) return;
@@ -792,18 +811,21 @@ __global__ void mmq_tail_reduce(const float* __restrict__ tws, int F, int R, int
     if (row >= rows || m >= M) return;
     float v = tws[((int64_t)tl * 256 + lr) * BN + lc];
     for (int sp = 1; sp < kt; ++sp) v += tws[(((int64_t)sp * R + tl) * 256 + lr) * BN + lc];
-    y[row * stride_r + m * stride_m] = (TY)v;
+    if (npeer == 0) y[row * stride_r + m * stride_m] = (TY)v;
+    for (int p = 0; p < npeer; ++p) reinterpret_cast<TY*>(ypeer[p])[(row0 + row) * stride_r + m * stride_m] = (TY)v;
 }
 
 template <typename TY>
 __global__ void mmq_splitk_reduce(const float* __restrict__ ws, int ks, int64_t rows, int64_t M, TY* __restrict__ y,
-                                  int64_t stride_r, int64_t stride_m) {
+                                  int64_t stride_r, int64_t stride_m, const unsigned long long* __restrict__ ypeer,
+                                  int npeer, int64_t row0) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= rows * M) return;
     const int64_t r = i / M, m = i % M;
     float v = ws[i];
     for (int z = 1; z < ks; ++z) v += ws[(int64_t)z * rows * M + i];  // fixed order
-    y[r * stride_r + m * stride_m] = (TY)v;
+    if (npeer == 0) y[r * stride_r + m * stride_m] = (TY)v;
+    for (int p = 0; p < npeer; ++p) reinterpret_cast<TY*>(ypeer[p])[(row0 + r) * stride_r + m * stride_m] = (TY)v;
 }
 
 }  // namespace itq3
@@ -963,7 +985,8 @@ static void mmq_tail_plan(int64_t tiles, int NS, int P, bool allowed, int& F, in
 
 template <int BN, typename TY>
 static int launch_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym, const uint8_t* act, int64_t m, TY* y,
-                      int64_t sr, int64_t sm_, float* ws, cudaStream_t s) {
+                      int64_t sr, int64_t sm_, float* ws, cudaStream_t s,
+                      const unsigned long long* ypeer = nullptr, int npeer = 0, int64_t row0 = 0) {
     const int smem = (int)sizeof(PairSmem) + 1024;
     static bool attr = false, attr32 = false;
     if (!attr) {
@@ -996,20 +1019,21 @@ static int launch_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym, 
     float* tws = reinterpret_cast<float*>(ws);
     if (wk.ks == 1) {
         launch_pdl(mmq_pair_kernel<BN, TY>, grid, dim3(kMmqThreads), smem, s, mmq, asym, wk, act, rows, m, y, sr, sm_,
-                   (int64_t)0, tws);
+                   (int64_t)0, tws, ypeer, npeer, row0);
         int rc = check_launch("itq3_mmq");
         if (rc || wk.R == 0) return rc;
         const int64_t n = (int64_t)wk.R * 256 * BN;
         mmq_tail_reduce<TY><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(tws, wk.F, wk.R, wk.kt, wk.tiles_r, BN, rows, m,
-                                                                      y, sr, sm_);
+                                                                      y, sr, sm_, ypeer, npeer, row0);
         return check_launch("itq3_mmq (tail reduce)");
     }
     launch_pdl(mmq_pair_kernel<BN, float>, grid, dim3(kMmqThreads), smem, s, mmq, asym, wk, act, rows, m, tws, m,
-               (int64_t)1, rows * m, tws);
+               (int64_t)1, rows * m, tws, (const unsigned long long*)nullptr, 0, (int64_t)0);
     int rc = check_launch("itq3_mmq (split-K)");
     if (rc) return rc;
     const int64_t n = rows * m;
-    mmq_splitk_reduce<TY><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(tws, wk.ks, rows, m, y, sr, sm_);
+    mmq_splitk_reduce<TY><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(tws, wk.ks, rows, m, y, sr, sm_, ypeer, npeer,
+                                                                      row0);
     return check_launch("itq3_mmq (split-K reduce)");
 }
 
@@ -1044,6 +1068,36 @@ extern "C" int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int flag
         return n128 ? launch_mmq<128>(mmq, rows, cols, flags, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s)
                     : launch_mmq<256>(mmq, rows, cols, flags, act, m, (__nv_bfloat16*)y, stride_r, stride_m, ws, s);
     set_error("itq3_mmq: output dtype must be float32 or bfloat16");
+    return ITQ3_E_DOMAIN;
+}
+
+extern "C" int itq3_mmq_peers(const uint8_t* mmq, int64_t rows, int64_t cols, int flags, const uint8_t* act, int64_t m,
+                              const void* d_ypeers, int npeer, int64_t row0, int y_dtype, int64_t stride_r,
+                              int64_t stride_m, void* workspace, void* stream) {
+    if (rows <= 0 || cols <= 0 || cols % 256 || m <= 0 || row0 < 0) {
+        set_error("itq3_mmq_peers: bad shape");
+        return ITQ3_E_SHAPE;
+    }
+    if (npeer < 1 || npeer > 8 || d_ypeers == nullptr) {
+        set_error("itq3_mmq_peers: need 1..8 peer output pointers (got %d)", npeer);
+        return ITQ3_E_DOMAIN;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const auto* yp = (const unsigned long long*)d_ypeers;
+    const bool n128 = itq3_mmq_block_n(m) == 128;
+    // every output row is written once -- by its tile's epilogue, or by the split reduce -- to all peers
+    float* ws = (float*)workspace;
+    if (y_dtype == ITQ3_F32)
+        return n128 ? launch_mmq<128>(mmq, rows, cols, flags, act, m, (float*)nullptr, stride_r, stride_m, ws, s, yp,
+                                      npeer, row0)
+                    : launch_mmq<256>(mmq, rows, cols, flags, act, m, (float*)nullptr, stride_r, stride_m, ws, s, yp,
+                                      npeer, row0);
+    if (y_dtype == ITQ3_BF16)
+        return n128 ? launch_mmq<128>(mmq, rows, cols, flags, act, m, (__nv_bfloat16*)nullptr, stride_r, stride_m, ws,
+                                      s, yp, npeer, row0)
+                    : launch_mmq<256>(mmq, rows, cols, flags, act, m, (__nv_bfloat16*)nullptr, stride_r, stride_m, ws,
+                                      s, yp, npeer, row0);
+    set_error("itq3_mmq_peers: output dtype must be float32 or bfloat16");
     return ITQ3_E_DOMAIN;
 }
 
@@ -1516,7 +1570,8 @@ static int launch_mmq8(const uint8_t* w, int64_t rows, int64_t cols, const uint8
     int rc = check_launch("itq3_mmq8 (split-K)");
     if (rc) return rc;
     const int64_t n = rows * m;
-    mmq_splitk_reduce<TY><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ws, ks, rows, m, y, sr, sm_);
+    mmq_splitk_reduce<TY><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ws, ks, rows, m, y, sr, sm_,
+                                                                      (const unsigned long long*)nullptr, 0, 0);
     return check_launch("itq3_mmq8 (split-K reduce)");
 }
 

@@ -278,3 +278,73 @@ class TPChainStack:
     def output(self) -> torch.Tensor:
         """The full last-stage output (all ranks' rows), identical on every rank."""
         return self.out
+
+
+class TPMatmul:
+    """Row-sharded batched product (fused_matmul, k >= 16) with the all-gather fused into the K5 MMQ
+    epilogue: every finished output row goes straight to all ranks' copies of Y through NVLink peer
+    pointers (torch symmetric memory), then one symmetric-memory barrier orders the reads.  The
+    unfused equivalent is ShardedLinear (local fused_matmul + NCCL all_gather_into_tensor).
+
+    `local_q`: this rank's rows shard_bounds(rows, world, rank); Y is rows x max_tokens (fp32) on every
+    rank.  `peer_bases` / `ybuf` (testing): explicit per-rank output buffers instead of a rendezvous.
+    """
+
+    def __init__(self, local_q: QuantizedTensor, rows: int, max_tokens: int, group=None, world: int | None = None,
+                 rank: int | None = None, ybuf: torch.Tensor | None = None, peer_bases: list[int] | None = None):
+        from . import _lib
+
+        self._lib = _lib
+        self.group = group
+        if world is None:
+            world = dist.get_world_size(group) if dist.is_initialized() else 1
+        if rank is None:
+            rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world, self.rank, self.rows, self.cols, self.max_tokens = world, rank, rows, local_q.cols, max_tokens
+        self.r0, r1 = shard_bounds(rows, world, rank)
+        if local_q.rows != r1 - self.r0:
+            raise ShapeError(f"TPMatmul: shard has {local_q.rows} rows, expected {r1 - self.r0}")
+        if not (local_q.mmq_ok() and local_q.k5_range_ok()):
+            raise ShapeError("TPMatmul: the shard's format is not on the K5 path (cols % 256, whole blocks)")
+        self.q = local_q
+        self.dev = _lib.device()
+        self.hdl = None
+        if ybuf is None:
+            if world > 1:
+                from torch.distributed import _symmetric_memory as symm
+
+                ybuf = symm.empty(rows * max_tokens, dtype=torch.float32, device=self.dev)
+                self.hdl = symm.rendezvous(ybuf, group if group is not None else dist.group.WORLD)
+                delta = ybuf.data_ptr() - self.hdl.buffer_ptrs[rank]
+                peer_bases = [b + delta for b in self.hdl.buffer_ptrs]
+            else:
+                ybuf = torch.empty(rows * max_tokens, dtype=torch.float32, device=self.dev)
+        if peer_bases is None:
+            peer_bases = [ybuf.data_ptr()]
+        if len(peer_bases) != world or peer_bases[rank] != ybuf.data_ptr():
+            raise ShapeError("TPMatmul: peer_bases must list every rank's buffer, this rank's at index rank")
+        self.ybuf = ybuf
+        self.peers = torch.tensor(peer_bases, dtype=torch.int64, device=self.dev)
+
+    def launch(self, X: torch.Tensor, stream: int | None = None) -> None:
+        """Rotate X (cols x k, this rank's device) and run the peer-store MMQ; no synchronisation."""
+        lib, k = self._lib, X.shape[1]
+        if X.shape[0] != self.cols or not 1 <= k <= self.max_tokens:
+            raise ShapeError(f"TPMatmul: X must be {self.cols} x (1..{self.max_tokens}), got {tuple(X.shape)}")
+        s = stream if stream is not None else lib.stream_ptr(self.dev)
+        self._act = torch.empty(lib.load().itq3_mmq_act_nbytes(self.cols, k), dtype=torch.uint8, device=self.dev)
+        lib.call("itq3_rotate_act_f16_n", lib.ptr(X), lib.TORCH_DTYPE_CODE[X.dtype], self.cols, k, X.stride(0),
+                 X.stride(1), self.q.block_n, lib.ptr(self._act), None, s)
+        wsn = lib.load().itq3_mmq_ws_nbytes(self.q.rows, self.cols, k)
+        self._ws = torch.empty(wsn, dtype=torch.uint8, device=self.dev) if wsn else None
+        lib.call("itq3_mmq_peers", lib.ptr(self.q.mmq_layout()), self.q.rows, self.cols, self.q.mmq_flags(),
+                 lib.ptr(self._act), k, lib.ptr(self.peers), self.world, self.r0, lib.F32, k, 1,
+                 lib.ptr(self._ws) if self._ws is not None else None, s)
+
+    def __call__(self, X: torch.Tensor) -> torch.Tensor:
+        """Y = w_hat @ X for the full `rows`, identical on every rank (a view of the symmetric buffer)."""
+        self.launch(X)
+        if self.hdl is not None:
+            self.hdl.barrier()  # every rank's peer stores have landed before anyone reads Y
+        k = X.shape[1]
+        return self.ybuf[: self.rows * k].view(self.rows, k)

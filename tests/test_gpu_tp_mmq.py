@@ -1,0 +1,58 @@
+"""GPU: row-sharded MMQ with the all-gather fused into the K5 epilogue (parallel.TPMatmul,
+itq3_mmq_peers).  World 1 (the rank's own buffer as its only peer) must equal the plain K5 call bit for
+bit (same shape, same split plan); worlds 2 and 3 are simulated on the one GPU with one buffer per
+virtual rank: every rank's copy of Y is identical, complete, and within the K5 bound of the oracle
+(a shard's K-split plan can differ from the full matrix's, so not bitwise equal to it)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+P = pytest.importorskip("paper_2603_27914_b200")
+from paper_2603_27914_b200 import _lib  # noqa: E402
+from paper_2603_27914_b200.parallel import TPMatmul, shard_quantized  # noqa: E402
+from test_gpu_mmq import mmq_bound  # noqa: E402
+
+
+def unsharded(q, X):
+    """The plain K5 call (itq3_mmq with its workspace) on the full matrix, rows x k fp32."""
+    k = X.shape[1]
+    act = torch.empty(_lib.load().itq3_mmq_act_nbytes(q.cols, k), dtype=torch.uint8, device=X.device)
+    _lib.call("itq3_rotate_act_f16_n", _lib.ptr(X), _lib.F32, q.cols, k, X.stride(0), X.stride(1), q.block_n,
+              _lib.ptr(act), None, _lib.stream_ptr(X.device))
+    Y = torch.empty((q.rows, k), dtype=torch.float32, device=X.device)
+    wsn = _lib.load().itq3_mmq_ws_nbytes(q.rows, q.cols, k)
+    ws = torch.empty(wsn, dtype=torch.uint8, device=X.device) if wsn else None
+    _lib.call("itq3_mmq", _lib.ptr(q.mmq_layout()), q.rows, q.cols, q.mmq_flags(), _lib.ptr(act), k, _lib.ptr(Y),
+              _lib.F32, Y.stride(0), Y.stride(1), _lib.ptr(ws) if ws is not None else None, _lib.stream_ptr(X.device))
+    return Y
+
+
+@pytest.mark.parametrize("m", [16, 100, 300])
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_tp_mmq_peer_stores(world, m):
+    rows, cols = 1000, 1024
+    rng = np.random.default_rng(world * 100 + m)
+    q = P.quantize_tensor(rng.standard_normal((rows, cols)) * 0.05)
+    X = torch.from_numpy(rng.standard_normal((cols, m)).astype(np.float32)).cuda()
+    ref = unsharded(q, X)
+    if world == 1:
+        Y = TPMatmul(q, rows, 512)(X)
+        torch.cuda.synchronize()
+        torch.testing.assert_close(Y, ref, rtol=0, atol=0)
+        exact, bound = mmq_bound(q.payload().cpu().numpy(), rows, cols, X.cpu().numpy())
+        assert np.all(np.abs(Y.cpu().numpy() - exact) <= bound)
+        return
+    bufs = [torch.full((rows * 512,), float("nan"), dtype=torch.float32, device="cuda") for _ in range(world)]
+    bases = [b.data_ptr() for b in bufs]
+    tps = [TPMatmul(shard_quantized(q, world, r), rows, 512, world=world, rank=r, ybuf=bufs[r], peer_bases=bases)
+           for r in range(world)]
+    for tp in tps:
+        tp.launch(X)
+    torch.cuda.synchronize()
+    y0 = bufs[0][: rows * m].view(rows, m)
+    for r in range(1, world):
+        torch.testing.assert_close(bufs[r][: rows * m].view(rows, m), y0, rtol=0, atol=0)
+    exact, bound = mmq_bound(q.payload().cpu().numpy(), rows, cols, X.cpu().numpy())
+    assert np.all(np.abs(y0.cpu().numpy() - exact) <= bound)  # also: no NaN left from the fill
