@@ -240,7 +240,7 @@ struct PairWork {
     }
 };
 
-template <int BN, typename TY>  // BN = tokens per pair tile (256, or 128 for M <= 128)
+template <int BN, typename TY, bool PEERS = false>  // BN = tokens per pair tile (256, or 128 for M <= 128)
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
     mmq_pair_kernel(const uint8_t* __restrict__ wrec, int flags, PairWork wk, const uint8_t* __restrict__ act,
                     int64_t rows, int64_t M, TY* __restrict__ y, int64_t stride_r, int64_t stride_m, int64_t slab,
@@ -277,6 +277,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
     const unsigned dflags = g_mmq_trace ? (unsigned)g_mmq_trace[4095 * 16] : 0u;
     const bool asym = flags & kMmqAsym, ss = flags & kMmqPer32;
     const int wbytes = ss ? kWRecT : kWRec;
+    if constexpr (!PEERS) npeer = 0;  // the plain instantiation carries no peer code
 
     if (warp == 0) {
         if (lane == 0) {  // producer: this CTA's weight record and 64-token half of B, one copy each per stage
@@ -990,7 +991,9 @@ static int launch_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym, 
     const int smem = (int)sizeof(PairSmem) + 1024;
     static bool attr = false, attr32 = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(mmq_pair_kernel<BN, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        if (cudaFuncSetAttribute(mmq_pair_kernel<BN, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+            cudaFuncSetAttribute(mmq_pair_kernel<BN, TY, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+                cudaSuccess)
             return check_launch("itq3_mmq: smem attribute");
         attr = true;
     }
@@ -1018,8 +1021,12 @@ static int launch_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym, 
     const dim3 grid((unsigned)(2 * clusters));
     float* tws = reinterpret_cast<float*>(ws);
     if (wk.ks == 1) {
-        launch_pdl(mmq_pair_kernel<BN, TY>, grid, dim3(kMmqThreads), smem, s, mmq, asym, wk, act, rows, m, y, sr, sm_,
-                   (int64_t)0, tws, ypeer, npeer, row0);
+        if (npeer)
+            launch_pdl(mmq_pair_kernel<BN, TY, true>, grid, dim3(kMmqThreads), smem, s, mmq, asym, wk, act, rows, m, y,
+                       sr, sm_, (int64_t)0, tws, ypeer, npeer, row0);
+        else
+            launch_pdl(mmq_pair_kernel<BN, TY>, grid, dim3(kMmqThreads), smem, s, mmq, asym, wk, act, rows, m, y, sr,
+                       sm_, (int64_t)0, tws, ypeer, 0, (int64_t)0);
         int rc = check_launch("itq3_mmq");
         if (rc || wk.R == 0) return rc;
         const int64_t n = (int64_t)wk.R * 256 * BN;
