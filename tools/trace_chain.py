@@ -69,6 +69,18 @@ def main():
     # publish skew: last-first publish time of a stage
     sk = t[:, :, 3].max(axis=0) - t[:, :, 3].min(axis=0)
     print(f"publish skew across CTAs median {np.median(sk):.2f} us")
+    # dependency latency: stage s+1 input ready on a CTA minus the LAST CTA's tiles-done of stage s
+    # (min over CTAs ~ store -> visible -> poll; median adds the CTAs that were still busy), and the
+    # imbalance of stage s (last tiles-done minus the median one)
+    last = t[:, :, 3].max(axis=0)
+    lat = t[:, 1:, 1] - last[None, :-1]
+    imb = last - np.median(t[:, :, 3], axis=0)
+    for k, n in enumerate(names):
+        idx = [i for i in range(k, S, len(names)) if i >= 1]
+        lo = np.median(np.nanmin(np.where(t[:, idx, 1] > 0, lat[:, [i - 1 for i in idx]], np.nan), axis=0))
+        md = np.median(np.median(lat[:, [i - 1 for i in idx]], axis=0))
+        print(f"  {n:8s} input ready after the last producer: min {lo:5.2f} median {md:5.2f} us; "
+              f"producer-stage imbalance {np.median(imb[[i - 1 for i in idx]]):5.2f} us")
 
 
 if __name__ == "__main__":
