@@ -78,6 +78,17 @@ int itq3_dequant(const uint8_t* payload, int64_t n_blocks, int block_n, int sub_
  * dequantiser used for block_n 256 / variant s; tools/dequant_trace.py), or NULL to switch it off. */
 int itq3_dequant_set_trace(void* buf);
 
+/* ---- block utilities of the reference API (quantizer.py:78-197), float64 device data flow:
+ * block_stats writes {n, mean, sigma, l1, linf, excess_kurtosis} (numpy pairwise sums; the
+ * kurtosis' fourth powers are rounded once, numpy uses libm pow); ternary_quantize
+ * clip(round_half_away(x / d) + z, -1, 1) -> int8; ternary_dequantize d * (code - z);
+ * uniform_quantize clip(delta * floor(x / delta + 0.5), wmin, wmax). */
+int itq3_block_stats(const double* v, int64_t n, double* out6, void* stream);
+int itq3_ternary_quantize(const double* x, int64_t n, double d, int z, int8_t* codes, void* stream);
+int itq3_ternary_dequantize(const int8_t* codes, int64_t n, double d, int z, double* out, void* stream);
+int itq3_uniform_quantize(const double* x, int64_t n, double delta, double wmin, double wmax, double* out,
+                          void* stream);
+
 /* ---- transform: fwht_forward / fwht_inverse (transform.py:61-96) on n_vec
  * contiguous vectors of length n (2..512, power of two), dtype F32 or F64,
  * bit-identical to numpy's butterfly order.  normalize=0 skips the 1/sqrt(n). */

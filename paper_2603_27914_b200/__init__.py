@@ -13,8 +13,11 @@ from .errors import (BadMagicError, ContainerError, CorruptionError, DomainError
                      ShapeError, SizeMismatchError, TruncatedStreamError, UnsupportedVersionError)
 from .packing import (PackedBlock, block_nbytes, decode_f16, deserialize_block, encode_f16, pack_ternary,
                       serialize_block, unpack_ternary)
-from .quantizer import DEFAULT_SCALE_COEFF, EPSILON_D, ScalePolicy, TernaryGrid, argmin_scale_coeff
-from .transform import fwht_forward, fwht_inverse
+from .quantizer import (DEFAULT_SCALE_COEFF, EPSILON_D, BlockStats, ScalePolicy, TernaryGrid, argmin_scale_coeff,
+                        block_stats, optimal_scale, ternary_dequantize, ternary_mse, ternary_quantize,
+                        uniform_quantize)
+from .transform import (StageTrace, fwht32_warp, fwht_forward, fwht_inverse, fwht_staged, hadamard_matrix,
+                        hadamard_oracle)
 
 __version__ = "0.1.0"
 
@@ -28,4 +31,6 @@ __all__ = [
     "argmin_scale_coeff", "block_nbytes", "decode_block", "decode_f16", "dequantize_tensor", "deserialize_block",
     "encode_block", "encode_f16", "fused_matmul", "fused_matvec", "fwht_forward", "fwht_inverse", "pack_ternary",
     "quantize_tensor", "read_container", "serialize_block", "unpack_ternary", "write_container",
+    "BlockStats", "StageTrace", "block_stats", "fwht32_warp", "fwht_staged", "hadamard_matrix", "hadamard_oracle",
+    "optimal_scale", "ternary_dequantize", "ternary_mse", "ternary_quantize", "uniform_quantize",
 ]

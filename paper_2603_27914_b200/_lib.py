@@ -32,6 +32,10 @@ SIGNATURES = {
     "itq3_encode": (_i32, [_vp, _i32, _i64, _i32, _i32, _i32, _dbl, _i32, _vp, _vp]),
     "itq3_validate": (_i32, [_vp, _i64, _i32, _i32, _u32, _vp, _vp]),
     "itq3_dequant": (_i32, [_vp, _i64, _i32, _i32, _i64, _vp, _i32, _vp]),
+    "itq3_block_stats": (_i32, [_vp, _i64, _vp, _vp]),
+    "itq3_ternary_quantize": (_i32, [_vp, _i64, _dbl, _i32, _vp, _vp]),
+    "itq3_ternary_dequantize": (_i32, [_vp, _i64, _dbl, _i32, _vp, _vp]),
+    "itq3_uniform_quantize": (_i32, [_vp, _i64, _dbl, _dbl, _dbl, _vp, _vp]),
     "itq3_fwht": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp]),
     "itq3_eval_ws_nbytes": (ctypes.c_size_t, [_i64, _i32]),
     "itq3_eval_ws_offset": (_i64, [_i64, _i32, _i32]),

@@ -58,3 +58,141 @@ class TernaryGrid:
             raise DomainError(f"TernaryGrid: scale must be positive and finite, got {self.d}")
         if self.z not in (-1, 0, 1):
             raise DomainError(f"TernaryGrid: zero-point must be -1, 0, or 1, got {self.z}")
+
+
+# ------------------------------------------------------------------------------------------------
+# Block utilities (quantizer.py:78-197 of the reference): computed by csrc/util.cu on the device in
+# float64 with the reference's data flow; the scalar rules (optimal_scale, ternary_mse) are plain
+# float arithmetic, as in the reference.
+# ------------------------------------------------------------------------------------------------
+@dataclass(frozen=True)
+class BlockStats:
+    """Sample statistics of one coefficient block (population conventions)."""
+
+    n: int
+    mean: float
+    sigma: float
+    l1: float
+    linf: float
+    excess_kurtosis: float
+
+
+def _device_f64(x, op: str):
+    import numpy as np
+    import torch
+
+    from . import _lib
+
+    a = np.asarray(x, dtype=np.float64)
+    if not np.all(np.isfinite(a)):
+        raise DomainError(f"{op}: input contains non-finite values")
+    dev = _lib.device()
+    return a, torch.from_numpy(np.ascontiguousarray(a).reshape(-1)).to(dev), dev
+
+
+def block_stats(v) -> BlockStats:
+    """Exact sample statistics of a block: mean, population sigma, l1, linf, excess kurtosis."""
+    import numpy as np
+    import torch
+
+    from . import _lib
+
+    a = np.asarray(v, dtype=np.float64)
+    if a.ndim != 1 or a.size == 0:
+        raise DomainError("block_stats: expects a non-empty 1-D block")
+    _, t, dev = _device_f64(a, "block_stats")
+    out = torch.empty(6, dtype=torch.float64, device=dev)
+    _lib.call("itq3_block_stats", _lib.ptr(t), a.size, _lib.ptr(out), _lib.stream_ptr(dev))
+    n, mean, sigma, l1, linf, kurt = out.cpu().tolist()
+    return BlockStats(n=int(n), mean=mean, sigma=sigma, l1=l1, linf=linf, excess_kurtosis=kurt)
+
+
+def ternary_mse(alpha: float, sigma: float) -> float:
+    """Mean squared error of thresholded ternary quantisation for x ~ N(0, sigma^2): inputs with
+    |x| <= alpha reconstruct to 0, the rest to sign(x) alpha.  Closed form of the reference's two
+    quadratures (quantizer.py:102-127; agreement ~1e-12, the reference's own tolerance is 1e-9):
+    with a = alpha / sigma, Phi the normal CDF, phi the density, Q = 1 - Phi,
+    mse / sigma^2 = 2 [(Phi(a) - 1/2 - a phi(a)) + ((1 + a^2) Q(a) - a phi(a))]."""
+    if not (alpha > 0 and math.isfinite(alpha)):
+        raise DomainError(f"ternary_mse: alpha must be positive and finite, got {alpha}")
+    if not (sigma > 0 and math.isfinite(sigma)):
+        raise DomainError(f"ternary_mse: sigma must be positive and finite, got {sigma}")
+    a = alpha / sigma
+    phi = math.exp(-0.5 * a * a) / math.sqrt(2.0 * math.pi)
+    dead = 0.5 * math.erf(a / math.sqrt(2.0)) - a * phi
+    tail = (1.0 + a * a) * 0.5 * math.erfc(a / math.sqrt(2.0)) - a * phi
+    return 2.0 * sigma * sigma * (dead + tail)
+
+
+def optimal_scale(stats: BlockStats, policy: ScalePolicy) -> float:
+    """Ternary scale for a block under the given policy, floored at EPSILON_D (quantizer.py:141-149)."""
+    if policy.kind == "constant":
+        d = policy.constant * stats.sigma
+    elif policy.kind == "argmin":
+        d = argmin_scale_coeff() * stats.sigma
+    else:
+        d = (2.0 / 3.0) * (stats.l1 / stats.n)
+    return d if d > 0 else EPSILON_D
+
+
+def ternary_quantize(x, grid: TernaryGrid):
+    """Map values to codes in {-1, 0, 1}: clamp(round(x / d) + z, -1, 1), rounding half away from
+    zero; arrays come back as int8, scalars as int."""
+    import numpy as np
+    import torch
+
+    from . import _lib
+
+    a, t, dev = _device_f64(x, "ternary_quantize")
+    out = torch.empty(t.numel(), dtype=torch.int8, device=dev)
+    _lib.call("itq3_ternary_quantize", _lib.ptr(t), t.numel(), float(grid.d), int(grid.z), _lib.ptr(out),
+              _lib.stream_ptr(dev))
+    codes = out.cpu().numpy().reshape(a.shape)
+    if np.isscalar(x) or np.ndim(x) == 0:
+        return int(codes)
+    return codes
+
+
+def ternary_dequantize(code, grid: TernaryGrid):
+    """Reconstruct d * (code - z) for codes in {-1, 0, 1}."""
+    import numpy as np
+    import torch
+
+    from . import _lib
+
+    c = np.asarray(code)
+    if not np.issubdtype(c.dtype, np.integer):
+        raise DomainError("ternary_dequantize: codes must be integers")
+    if c.size and (c.min() < -1 or c.max() > 1):
+        raise DomainError("ternary_dequantize: codes must lie in {-1, 0, 1}")
+    dev = _lib.device()
+    t = torch.from_numpy(np.ascontiguousarray(c, dtype=np.int8).reshape(-1)).to(dev)
+    out = torch.empty(t.numel(), dtype=torch.float64, device=dev)
+    _lib.call("itq3_ternary_dequantize", _lib.ptr(t), t.numel(), float(grid.d), int(grid.z), _lib.ptr(out),
+              _lib.stream_ptr(dev))
+    res = out.cpu().numpy().reshape(c.shape)
+    if np.isscalar(code) or np.ndim(code) == 0:
+        return float(res)
+    return res
+
+
+def uniform_quantize(x, bits: int, wmin: float, wmax: float):
+    """Uniform b-bit baseline: step (wmax - wmin) / (2^b - 1), reconstruction clamped to the range."""
+    import numpy as np
+    import torch
+
+    from . import _lib
+
+    if not 2 <= int(bits) <= 8:
+        raise DomainError(f"uniform_quantize: bits must be in [2, 8], got {bits}")
+    if not (wmin < wmax):
+        raise DomainError(f"uniform_quantize: need wmin < wmax, got [{wmin}, {wmax}]")
+    a, t, dev = _device_f64(x, "uniform_quantize")
+    delta = (wmax - wmin) / (2 ** int(bits) - 1)
+    out = torch.empty(t.numel(), dtype=torch.float64, device=dev)
+    _lib.call("itq3_uniform_quantize", _lib.ptr(t), t.numel(), float(delta), float(wmin), float(wmax),
+              _lib.ptr(out), _lib.stream_ptr(dev))
+    res = out.cpu().numpy().reshape(a.shape)
+    if np.isscalar(x) or np.ndim(x) == 0:
+        return float(res)
+    return res

@@ -6,6 +6,7 @@ package; here the oracle must reproduce them bit for bit (bytes, dequant values)
 """
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -133,3 +134,16 @@ def test_oracle_pairwise_sum_matches_numpy():
     for n in (1, 7, 8, 100, 128, 129, 1000, 4099, 65536 + 13):
         v = rng.standard_normal(n) ** 2
         assert O.pairwise_sum(v) == np.sum(v), n
+
+
+def test_scalar_rules_vs_reference_fixtures():
+    """ternary_mse (closed form vs the reference's quadrature) and optimal_scale, host scalars."""
+    import paper_2603_27914_b200 as P
+
+    G = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "util_cases.npz"))
+    for alpha, sigma, want in G["mse"]:
+        assert abs(P.ternary_mse(alpha, sigma) - want) <= 1e-10 + 1e-9 * abs(want)
+    s = G["os_stats"]
+    st = P.BlockStats(n=int(s[0]), mean=s[1], sigma=s[2], l1=s[3], linf=s[4], excess_kurtosis=s[5])
+    got = [P.optimal_scale(st, P.ScalePolicy(kind=k)) for k in ("constant", "argmin", "mean-abs")]
+    np.testing.assert_array_equal(got, G["os_out"])
