@@ -16,6 +16,7 @@ from .packing import (PackedBlock, block_nbytes, decode_f16, deserialize_block, 
 from .quantizer import (DEFAULT_SCALE_COEFF, EPSILON_D, BlockStats, ScalePolicy, TernaryGrid, argmin_scale_coeff,
                         block_stats, optimal_scale, ternary_dequantize, ternary_mse, ternary_quantize,
                         uniform_quantize)
+from .selfcheck import CheckResult, run_selfcheck
 from .transform import (StageTrace, fwht32_warp, fwht_forward, fwht_inverse, fwht_staged, hadamard_matrix,
                         hadamard_oracle)
 
@@ -33,4 +34,5 @@ __all__ = [
     "quantize_tensor", "read_container", "serialize_block", "unpack_ternary", "write_container",
     "BlockStats", "StageTrace", "block_stats", "fwht32_warp", "fwht_staged", "hadamard_matrix", "hadamard_oracle",
     "optimal_scale", "ternary_dequantize", "ternary_mse", "ternary_quantize", "uniform_quantize",
+    "CheckResult", "run_selfcheck",
 ]
