@@ -67,7 +67,7 @@ class TernaryGrid:
 # ------------------------------------------------------------------------------------------------
 @dataclass(frozen=True)
 class BlockStats:
-    """Sample statistics of one coefficient block (population conventions)."""
+    """Statistics of one block: size, mean, population sigma, l1 and linf norms, excess kurtosis."""
 
     n: int
     mean: float
@@ -91,7 +91,7 @@ def _device_f64(x, op: str):
 
 
 def block_stats(v) -> BlockStats:
-    """Exact sample statistics of a block: mean, population sigma, l1, linf, excess kurtosis."""
+    """Population statistics of one block (one device launch, numpy's summation order)."""
     import numpy as np
     import torch
 
@@ -108,8 +108,8 @@ def block_stats(v) -> BlockStats:
 
 
 def ternary_mse(alpha: float, sigma: float) -> float:
-    """Mean squared error of thresholded ternary quantisation for x ~ N(0, sigma^2): inputs with
-    |x| <= alpha reconstruct to 0, the rest to sign(x) alpha.  Closed form of the reference's two
+    """Gaussian MSE of the dead-zone ternary quantiser with threshold and level alpha (values with
+    |x| <= alpha map to 0, the others to +-alpha), x ~ N(0, sigma^2).  Closed form of the reference's two
     quadratures (quantizer.py:102-127; agreement ~1e-12, the reference's own tolerance is 1e-9):
     with a = alpha / sigma, Phi the normal CDF, phi the density, Q = 1 - Phi,
     mse / sigma^2 = 2 [(Phi(a) - 1/2 - a phi(a)) + ((1 + a^2) Q(a) - a phi(a))]."""
@@ -125,7 +125,8 @@ def ternary_mse(alpha: float, sigma: float) -> float:
 
 
 def optimal_scale(stats: BlockStats, policy: ScalePolicy) -> float:
-    """Ternary scale for a block under the given policy, floored at EPSILON_D (quantizer.py:141-149)."""
+    """Block scale chosen by `policy` from the block's statistics, never below EPSILON_D
+    (quantizer.py:141-149)."""
     if policy.kind == "constant":
         d = policy.constant * stats.sigma
     elif policy.kind == "argmin":
@@ -136,8 +137,8 @@ def optimal_scale(stats: BlockStats, policy: ScalePolicy) -> float:
 
 
 def ternary_quantize(x, grid: TernaryGrid):
-    """Map values to codes in {-1, 0, 1}: clamp(round(x / d) + z, -1, 1), rounding half away from
-    zero; arrays come back as int8, scalars as int."""
+    """Codes of x on the grid (device kernel): x / d rounded half away from zero, shifted by z and
+    clipped to [-1, 1]; int8 array for array input, int for a scalar."""
     import numpy as np
     import torch
 
@@ -154,7 +155,7 @@ def ternary_quantize(x, grid: TernaryGrid):
 
 
 def ternary_dequantize(code, grid: TernaryGrid):
-    """Reconstruct d * (code - z) for codes in {-1, 0, 1}."""
+    """Grid values d (code - z) of integer codes in [-1, 1] (device kernel)."""
     import numpy as np
     import torch
 
@@ -177,7 +178,8 @@ def ternary_dequantize(code, grid: TernaryGrid):
 
 
 def uniform_quantize(x, bits: int, wmin: float, wmax: float):
-    """Uniform b-bit baseline: step (wmax - wmin) / (2^b - 1), reconstruction clamped to the range."""
+    """The b-bit uniform baseline on [wmin, wmax]: nearest multiple of (wmax - wmin) / (2^b - 1),
+    clamped to the range (device kernel)."""
     import numpy as np
     import torch
 
