@@ -223,6 +223,62 @@ def build_stack(n_layers: int, seed: int, dev, mode: str = "chain"):
     return LinearStack(qs, limbs=3, mode=mode)
 
 
+def run_decoder(args):
+    """--decoder: BASELINE configs[3], a full Llama-3-8B-shaped decoder (RMSNorm, RoPE, grouped-query
+    attention over a KV cache, SiLU gating) with every linear an ITQ3_S tensor on the fused GEMV;
+    random N(0, 0.02^2) weights quantised on the GPU.  One CUDA graph per token; the timed tokens
+    decode positions 512.. of a 1024-position cache.  Replicas only (no collective) for N > 1."""
+    import torch
+
+    from paper_2603_27914_b200.decoder import DecoderStack
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    st = DecoderStack(layers=args.layers, max_ctx=1024, seed=3000 + rank, dev=dev)
+    st.capture()
+    st.reset(512)
+    g = torch.Generator(device=dev)
+    g.manual_seed(rank)
+    st.x.copy_(torch.randn(st.h, generator=g, device=dev))
+    for _ in range(args.warmup):
+        st.graph.replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        st.graph.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    tiled = sum(int(t.numel()) for row in st.q for q in row for t in q._tiled.values())
+    if rank == 0:
+        print(json.dumps({
+            "metric": "decode tokens/sec (batch-1 ITQ3_S decoder: fused IFWHT-dequant GEMVs + torch attention glue)",
+            "value": world * 1000.0 / ms, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8xs8->s32 mma + fp32",
+            "data": "synthetic: random-init N(0, 0.02^2) weights quantized to ITQ3_S on the GPU, random hidden state",
+            "config": {"workload": f"llama3-8b decoder decode: {args.layers} layers (hidden 4096, ffn 14336, "
+                                   "32 heads / 8 kv heads, head_dim 128), positions 512+ of a 1024 KV cache",
+                       "model": "llama3-8b (decoder, random init)", "global_batch": world, "seq_len": 1,
+                       "parallelism": "single" if world == 1 else f"replicas{world}"},
+            "packed_weight_gbps": tiled / (ms / 1000.0) / 1e9,
+            "gpu_launches_per_step_itq3": 4 * args.layers}), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def run_tp(args):
     """--tp: ONE token stream row-sharded over the ranks (strong scaling): each rank holds
     rows shard_bounds(r, world, rank) of every stage.  --tp-impl fused (default): one persistent chain
@@ -446,6 +502,7 @@ def main():
     ap.add_argument("--mode", choices=["chain", "kernels"], default="chain")
     ap.add_argument("--model", choices=sorted(MODELS), default=MODEL)
     ap.add_argument("--tp", action="store_true", help="row-shard one token stream over the ranks (C5)")
+    ap.add_argument("--decoder", action="store_true", help="configs[3]: full Llama-3-8B-shaped decoder decode step")
     ap.add_argument("--tp-impl", choices=["fused", "nccl"], default="fused",
                     help="--tp: fused chain kernel with NVLink peer stores, or per-stage kernels + NCCL all_gather")
     args = ap.parse_args()
@@ -457,6 +514,8 @@ def main():
         run_reference(args)
     elif args.tp:
         run_tp(args)
+    elif args.decoder:
+        run_decoder(args)
     else:
         run_ours(args)
 

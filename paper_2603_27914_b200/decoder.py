@@ -1,0 +1,151 @@
+"""Decoder-stack harness (BASELINE configs[3]): a Llama-style decoder
+whose every linear is an ITQ3_S tensor multiplied by the fused kernels of this package, for the
+batch-1 decode tokens/s metric.  None of it exists in the reference; it only frames the hot path.
+
+Per layer and token: RMSNorm -> qkv GEMV -> RoPE -> KV-cache append -> attention over the cache
+(grouped-query, two batched GEMMs + masked softmax) -> o GEMV -> residual -> RMSNorm -> gate_up GEMV -> SiLU(gate) * up ->
+down GEMV -> residual.  The GEMVs are one-stage chain launches (csrc/chain.cu, one cooperative
+kernel each); norms, RoPE, attention and the gating are torch glue.  A whole token step is ONE CUDA
+graph: the position lives in a device tensor that the graph itself advances, the attention reads
+the full cache under a position mask, so replays need no host work.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from .codec import QuantizedTensor, quantize_tensor
+from .compute import fused_matvec
+
+LLAMA3_8B = dict(hidden=4096, inter=14336, n_heads=32, n_kv=8, head_dim=128, rope_theta=500000.0)
+
+
+class DecoderStack:
+    """`layers` x (qkv, o, gate_up, down) ITQ3_S linears with random N(0, 0.02^2) weights (quantised
+    on the GPU by K1), RMSNorm gains near 1, a KV cache of `max_ctx` positions (fp32)."""
+
+    def __init__(self, layers: int = 32, max_ctx: int = 1024, seed: int = 0, dev=None, shapes: dict | None = None,
+                 eps: float = 1e-5, serving: bool = True):
+        cfg = dict(LLAMA3_8B, **(shapes or {}))
+        self.dev = dev or torch.device("cuda", torch.cuda.current_device())
+        self.layers, self.max_ctx, self.eps = layers, max_ctx, eps
+        self.h, self.inter = cfg["hidden"], cfg["inter"]
+        self.nh, self.nkv, self.hd = cfg["n_heads"], cfg["n_kv"], cfg["head_dim"]
+        g = torch.Generator(device=self.dev)
+        g.manual_seed(seed)
+        kv = self.nkv * self.hd
+        shapes_l = [(self.h + 2 * kv, self.h), (self.h, self.h), (2 * self.inter, self.h), (self.h, self.inter)]
+        self.q: list[list[QuantizedTensor]] = []
+        for _ in range(layers):
+            row = []
+            for r, c in shapes_l:
+                w = torch.randn((r, c), generator=g, device=self.dev).mul_(0.02)
+                q = quantize_tensor(w)
+                q.tiled()
+                if serving:
+                    q.drop_payload()  # only the tiled GEMV copy stays on the device
+                row.append(q)
+                del w
+            self.q.append(row)
+        self.gain = [(1.0 + 0.1 * torch.randn((2, self.h), generator=g, device=self.dev)) for _ in range(layers)]
+        inv = 1.0 / (cfg["rope_theta"] ** (torch.arange(0, self.hd, 2, device=self.dev, dtype=torch.float64) / self.hd))
+        ang = torch.arange(max_ctx, device=self.dev, dtype=torch.float64)[:, None] * inv[None, :]
+        self.cos, self.sin = ang.cos().float(), ang.sin().float()
+        self.k_cache = torch.zeros((layers, 1, self.nkv, max_ctx, self.hd), device=self.dev)
+        self.v_cache = torch.zeros_like(self.k_cache)
+        self.pos = torch.zeros(1, dtype=torch.long, device=self.dev)
+        self.x = torch.zeros(self.h, device=self.dev)
+        self.out = torch.zeros(self.h, device=self.dev)
+        self.kpos = torch.arange(max_ctx, device=self.dev)
+        self.graph = None
+
+    def _rms(self, x, gain):
+        return torch.nn.functional.rms_norm(x, (self.h,), weight=gain, eps=self.eps)
+
+    def _attend(self, q, li):
+        """One query over the cache: per kv head, its group of query heads against every position,
+        positions > pos masked out (two batched GEMMs and a softmax)."""
+        grp = self.nh // self.nkv
+        K, V = self.k_cache[li, 0], self.v_cache[li, 0]  # (nkv, ctx, hd)
+        s = torch.bmm(q.view(self.nkv, grp, self.hd), K.transpose(1, 2)) * (1.0 / math.sqrt(self.hd))
+        s = s.masked_fill(self.kpos.view(1, 1, -1) > self.pos, float("-inf"))
+        return torch.bmm(torch.softmax(s, dim=-1), V).reshape(self.h)
+
+    def _rope(self, t, cos, sin):  # t: (heads, hd), rotate-half convention
+        a, b = t[:, : self.hd // 2], t[:, self.hd // 2:]
+        return torch.cat((a * cos - b * sin, a * sin + b * cos), dim=1)
+
+    def _step(self) -> None:
+        x = self.x.clone()
+        cos = self.cos.index_select(0, self.pos)
+        sin = self.sin.index_select(0, self.pos)
+        kvd = self.nkv * self.hd
+        for li in range(self.layers):
+            qkv_w, o_w, gu_w, down_w = self.q[li]
+            g1, g2 = self.gain[li][0], self.gain[li][1]
+            qkv = fused_matvec(qkv_w, self._rms(x, g1), check_finite=False)
+            q = self._rope(qkv[: self.h].view(self.nh, self.hd), cos, sin)
+            k = self._rope(qkv[self.h: self.h + kvd].view(self.nkv, self.hd), cos, sin)
+            v = qkv[self.h + kvd:].view(self.nkv, self.hd)
+            self.k_cache[li, 0].index_copy_(1, self.pos, k[:, None, :])
+            self.v_cache[li, 0].index_copy_(1, self.pos, v[:, None, :])
+            x = x + fused_matvec(o_w, self._attend(q, li), check_finite=False)
+            gu = fused_matvec(gu_w, self._rms(x, g2), check_finite=False)
+            a = torch.nn.functional.silu(gu[: self.inter]) * gu[self.inter:]
+            x = x + fused_matvec(down_w, a, check_finite=False)
+        self.out.copy_(x)
+        self.pos.add_(1)
+
+    def capture(self) -> None:
+        """Record one token step (all layers, position advance included) as a CUDA graph."""
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(side):
+            self._step()  # warm-up: builds the per-tensor chain contexts outside capture
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        self.reset()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._step()
+        self.graph = g
+
+    def reset(self, pos: int = 0) -> None:
+        self.pos.fill_(pos)
+        self.k_cache.zero_()
+        self.v_cache.zero_()
+
+    def step(self, x: torch.Tensor | None = None) -> torch.Tensor:
+        """Decode one token: hidden state in (device, len hidden), hidden state out; advances the position."""
+        if x is not None:
+            self.x.copy_(x)
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+        return self.out
+
+    def reference_step(self, x: torch.Tensor, pos: int, k_hist: list, v_hist: list) -> torch.Tensor:  # noqa: C901
+        """The same token step in plain torch fp32 with dequantised weights (numerics test only)."""
+        from .codec import dequantize_tensor
+
+        h = x.clone()
+        cos, sin = self.cos[pos:pos + 1], self.sin[pos:pos + 1]
+        kvd = self.nkv * self.hd
+        for li in range(self.layers):
+            W = [torch.as_tensor(dequantize_tensor(q), device=self.dev).float() for q in self.q[li]]
+            g1, g2 = self.gain[li][0], self.gain[li][1]
+            qkv = W[0] @ self._rms(h, g1)
+            q = self._rope(qkv[: self.h].view(self.nh, self.hd), cos, sin)
+            k = self._rope(qkv[self.h: self.h + kvd].view(self.nkv, self.hd), cos, sin)
+            v = qkv[self.h + kvd:].view(self.nkv, self.hd)
+            k_hist[li].append(k)
+            v_hist[li].append(v)
+            K = torch.stack(k_hist[li], dim=1).repeat_interleave(self.nh // self.nkv, 0)  # (nh, t, hd)
+            V = torch.stack(v_hist[li], dim=1).repeat_interleave(self.nh // self.nkv, 0)
+            s = (K @ q[:, :, None])[:, :, 0] / math.sqrt(self.hd)
+            att = (torch.softmax(s, dim=1)[:, None, :] @ V)[:, 0, :]
+            h = h + W[1] @ att.reshape(self.h)
+            gu = W[2] @ self._rms(h, g2)
+            h = h + W[3] @ (torch.nn.functional.silu(gu[: self.inter]) * gu[self.inter:])
+        return h
