@@ -2,10 +2,10 @@
 whose every linear is an ITQ3_S tensor multiplied by the fused kernels of this package, for the
 batch-1 decode tokens/s metric.  None of it exists in the reference; it only frames the hot path.
 
-Per layer and token: RMSNorm -> qkv GEMV -> RoPE -> KV-cache append -> attention over the cache
-(grouped-query, two batched GEMMs + masked softmax) -> o GEMV -> residual -> RMSNorm -> gate_up GEMV -> SiLU(gate) * up ->
-down GEMV -> residual.  The GEMVs are one-stage chain launches (csrc/chain.cu, one cooperative
-kernel each); norms, RoPE, attention and the gating are torch glue.  A whole token step is ONE CUDA
+Per layer and token: [residual +] RMSNorm -> qkv GEMV -> RoPE + KV-cache append + grouped-query
+attention over the cache -> o GEMV -> residual + RMSNorm -> gate_up GEMV -> SiLU(gate) * up -> down
+GEMV.  The GEMVs are one-stage chain launches (csrc/chain.cu, one cooperative kernel each); the glue
+is three small kernels (csrc/decoder_glue.cu), so a layer is 8 launches.  A whole token step is ONE CUDA
 graph: the position lives in a device tensor that the graph itself advances, the attention reads
 the full cache under a position mask, so replays need no host work.
 """
@@ -59,43 +59,45 @@ class DecoderStack:
         self.x = torch.zeros(self.h, device=self.dev)
         self.out = torch.zeros(self.h, device=self.dev)
         self.kpos = torch.arange(max_ctx, device=self.dev)
+        self.xs = torch.zeros(self.h, device=self.dev)          # residual stream
+        self.hbuf = torch.zeros(self.h, device=self.dev)        # normalised input of a projection
+        self.att = torch.zeros(self.h, device=self.dev)         # attention output (nh * hd)
+        self.act = torch.zeros(self.inter, device=self.dev)     # SiLU(gate) * up
+        if self.hd != 128 or max_ctx > 1024 or self.nh * self.hd != self.h:
+            raise ValueError("DecoderStack: the glue kernels need head_dim 128, max_ctx <= 1024, nh * hd = hidden")
         self.graph = None
 
     def _rms(self, x, gain):
         return torch.nn.functional.rms_norm(x, (self.h,), weight=gain, eps=self.eps)
-
-    def _attend(self, q, li):
-        """One query over the cache: per kv head, its group of query heads against every position,
-        positions > pos masked out (two batched GEMMs and a softmax)."""
-        grp = self.nh // self.nkv
-        K, V = self.k_cache[li, 0], self.v_cache[li, 0]  # (nkv, ctx, hd)
-        s = torch.bmm(q.view(self.nkv, grp, self.hd), K.transpose(1, 2)) * (1.0 / math.sqrt(self.hd))
-        s = s.masked_fill(self.kpos.view(1, 1, -1) > self.pos, float("-inf"))
-        return torch.bmm(torch.softmax(s, dim=-1), V).reshape(self.h)
 
     def _rope(self, t, cos, sin):  # t: (heads, hd), rotate-half convention
         a, b = t[:, : self.hd // 2], t[:, self.hd // 2:]
         return torch.cat((a * cos - b * sin, a * sin + b * cos), dim=1)
 
     def _step(self) -> None:
-        x = self.x.clone()
-        cos = self.cos.index_select(0, self.pos)
-        sin = self.sin.index_select(0, self.pos)
-        kvd = self.nkv * self.hd
+        """One token: 4 GEMV launches + 4 glue launches per layer (csrc/decoder_glue.cu)."""
+        from . import _lib
+
+        st = _lib.stream_ptr(self.dev)
+        xs, h = self.xs, self.hbuf
+        xs.copy_(self.x)
+        prev = None
         for li in range(self.layers):
             qkv_w, o_w, gu_w, down_w = self.q[li]
-            g1, g2 = self.gain[li][0], self.gain[li][1]
-            qkv = fused_matvec(qkv_w, self._rms(x, g1), check_finite=False)
-            q = self._rope(qkv[: self.h].view(self.nh, self.hd), cos, sin)
-            k = self._rope(qkv[self.h: self.h + kvd].view(self.nkv, self.hd), cos, sin)
-            v = qkv[self.h + kvd:].view(self.nkv, self.hd)
-            self.k_cache[li, 0].index_copy_(1, self.pos, k[:, None, :])
-            self.v_cache[li, 0].index_copy_(1, self.pos, v[:, None, :])
-            x = x + fused_matvec(o_w, self._attend(q, li), check_finite=False)
-            gu = fused_matvec(gu_w, self._rms(x, g2), check_finite=False)
-            a = torch.nn.functional.silu(gu[: self.inter]) * gu[self.inter:]
-            x = x + fused_matvec(down_w, a, check_finite=False)
-        self.out.copy_(x)
+            _lib.call("itq3_glue_residual_rmsnorm", _lib.ptr(xs), _lib.ptr(prev) if prev is not None else None,
+                      _lib.ptr(self.gain[li][0]), _lib.ptr(h), self.h, self.eps, st)
+            qkv = fused_matvec(qkv_w, h, check_finite=False)
+            _lib.call("itq3_glue_rope_attention", _lib.ptr(qkv), _lib.ptr(self.cos), _lib.ptr(self.sin),
+                      _lib.ptr(self.pos), _lib.ptr(self.k_cache[li, 0]), _lib.ptr(self.v_cache[li, 0]),
+                      _lib.ptr(self.att), self.nh, self.nkv, self.hd, self.max_ctx, st)
+            o = fused_matvec(o_w, self.att, check_finite=False)
+            _lib.call("itq3_glue_residual_rmsnorm", _lib.ptr(xs), _lib.ptr(o), _lib.ptr(self.gain[li][1]),
+                      _lib.ptr(h), self.h, self.eps, st)
+            gu = fused_matvec(gu_w, h, check_finite=False)
+            _lib.call("itq3_glue_silu_mul", _lib.ptr(gu), _lib.ptr(self.act), self.inter, st)
+            prev = fused_matvec(down_w, self.act, check_finite=False)
+        _lib.call("itq3_glue_residual_rmsnorm", _lib.ptr(xs), _lib.ptr(prev), None, _lib.ptr(self.out), self.h,
+                  self.eps, st)
         self.pos.add_(1)
 
     def capture(self) -> None:
