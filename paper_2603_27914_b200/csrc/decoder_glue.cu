@@ -18,29 +18,34 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
     return v;
 }
 
-// x += r (if r), then out = x * rsqrt(mean(x^2) + eps) * gain (if gain; else out = x).  One CTA.
+// x += r (if r), then out = x * rsqrt(mean(x^2) + eps) * gain (if gain; else out = x).  One CTA;
+// each thread keeps its (up to 8) elements in registers across the reduction.
 __global__ void __launch_bounds__(kGlueThreads) glue_residual_rmsnorm(float* __restrict__ x,
                                                                      const float* __restrict__ r,
                                                                      const float* __restrict__ gain,
                                                                      float* __restrict__ out, int n, float eps) {
     __shared__ float red[32];
+    constexpr int kPer = 8;  // n <= 8 * 1024
+    float v[kPer];
     float ss = 0.f;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        float v = x[i];
-        if (r) {
-            v += r[i];
-            x[i] = v;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const int i = threadIdx.x + j * kGlueThreads;
+        v[j] = 0.f;
+        if (i < n) {
+            v[j] = x[i] + (r ? r[i] : 0.f);
+            if (r) x[i] = v[j];
+            ss += v[j] * v[j];
         }
-        ss += v * v;
     }
-    if (!gain) {
-        if (out)
-            for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = x[i];
-        return;
+    float s = 1.f;
+    if (gain) s = rsqrtf(block_sum(ss, red) / (float)n + eps);
+    if (!out) return;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const int i = threadIdx.x + j * kGlueThreads;
+        if (i < n) out[i] = gain ? v[j] * s * gain[i] : v[j];
     }
-    const float tot = block_sum(ss, red);
-    const float s = rsqrtf(tot / (float)n + eps);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = x[i] * s * gain[i];
 }
 
 // One CTA (1024 threads) per query head: RoPE (rotate-half) of its query and of its kv head's key at
@@ -148,6 +153,10 @@ using namespace itq3;
 
 extern "C" int itq3_glue_residual_rmsnorm(float* x, const float* r, const float* gain, float* out, int n, float eps,
                                           void* stream) {
+    if (n <= 0 || n > 8 * kGlueThreads) {
+        set_error("itq3_glue_residual_rmsnorm: 0 < n <= %d", 8 * kGlueThreads);
+        return ITQ3_E_SHAPE;
+    }
     glue_residual_rmsnorm<<<1, kGlueThreads, 0, (cudaStream_t)stream>>>(x, r, gain, out, n, eps);
     return check_launch("itq3_glue_residual_rmsnorm");
 }
