@@ -93,9 +93,10 @@ int itq3_uniform_quantize(const double* x, int64_t n, double delta, double wmin,
  * (r / gain may be NULL); RoPE + KV append + grouped-query decode attention (head_dim 128,
  * ctx <= 1024, position read from *pos); SiLU(gate) * up. */
 int itq3_glue_residual_rmsnorm(float* x, const float* r, const float* gain, float* out, int n, float eps, void* stream);
+int64_t itq3_glue_attention_ws_nbytes(int n_heads);  /* zero-initialise once */
 int itq3_glue_rope_attention(const float* qkv, const float* cos_tab, const float* sin_tab, const int64_t* pos,
                              float* k_cache, float* v_cache, float* out, int n_heads, int n_kv, int head_dim, int ctx,
-                             void* stream);
+                             void* ws, void* stream);
 int itq3_glue_silu_mul(const float* gu, float* out, int inter, void* stream);
 
 /* ---- transform: fwht_forward / fwht_inverse (transform.py:61-96) on n_vec

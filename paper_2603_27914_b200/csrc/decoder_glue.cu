@@ -48,23 +48,30 @@ __global__ void __launch_bounds__(kGlueThreads) glue_residual_rmsnorm(float* __r
     }
 }
 
-// One CTA (1024 threads) per query head: RoPE (rotate-half) of its query and of its kv head's key at
-// position pos, append k / v at pos (the group's first head writes the cache), then softmax
-// attention over positions 0..pos -- the current position from shared memory, earlier ones from
-// the cache.  Scores: one warp per position; P V: 8 position classes x 128 dims, reduced in smem.
+// Flash-decoding attention: CTA (h, sp) of a (query head, position split) grid handles positions
+// [lo, hi) of 0..pos.  Every CTA applies RoPE (rotate-half) to its query and to its kv head's key at
+// pos; the (group-leader head, split 0) CTA appends k / v to the cache.  A CTA writes its partial
+// (max, sum of exp, exp-weighted V) to `ws`; the last split of a head to arrive (per-head counter,
+// reset for the next launch) combines them.  Scores: one warp per position, four in flight;
+// P V: 8 position classes x 128 dims, reduced in smem.
 // qkv = [q (nh*hd) | k (nkv*hd) | v (nkv*hd)]; caches [nkv][ctx][hd]; out [nh*hd].
+constexpr int kAttnSplits = 4;
 __global__ void __launch_bounds__(1024) glue_rope_attention(const float* __restrict__ qkv, const float* __restrict__ cosb,
                                                            const float* __restrict__ sinb,
                                                            const int64_t* __restrict__ pos_p, float* __restrict__ kc,
                                                            float* __restrict__ vc, float* __restrict__ out, int nh,
-                                                           int nkv, int ctx) {
+                                                           int nkv, int ctx, float* __restrict__ ws,
+                                                           unsigned* __restrict__ counters) {
     constexpr int HD = 128;
     __shared__ float qs[HD], kcur[HD], vcur[HD];
     __shared__ float ps[1024];
     __shared__ float red[32];
     __shared__ float part[8][HD];
-    const int h = blockIdx.x, t = threadIdx.x, w = t >> 5, l = t & 31, kvh = h / (nh / nkv);
+    __shared__ bool last;
+    const int h = blockIdx.x, sp = blockIdx.y, t = threadIdx.x, w = t >> 5, l = t & 31, kvh = h / (nh / nkv);
     const int pos = (int)*pos_p;
+    const int chunk = (pos + kAttnSplits) / kAttnSplits;  // ceil((pos + 1) / splits)
+    const int lo = sp * chunk, hi = min(pos + 1, lo + chunk);
     float* kch = kc + (int64_t)kvh * ctx * HD;
     float* vch = vc + (int64_t)kvh * ctx * HD;
     if (t < HD) {
@@ -79,7 +86,7 @@ __global__ void __launch_bounds__(1024) glue_rope_attention(const float* __restr
         qs[t] = rope(qkv + (int64_t)h * HD) * rsqrtf((float)HD);
         kcur[t] = kv;
         vcur[t] = vv;
-        if (h % (nh / nkv) == 0) {
+        if (sp == 0 && h % (nh / nkv) == 0) {
             kch[(int64_t)pos * HD + t] = kv;
             vch[(int64_t)pos * HD + t] = vv;
         }
@@ -87,20 +94,20 @@ __global__ void __launch_bounds__(1024) glue_rope_attention(const float* __restr
     __syncthreads();
     float mx = -INFINITY;
     const float q0 = qs[l], q1 = qs[l + 32], q2 = qs[l + 64], q3 = qs[l + 96];
-    for (int p0 = w; p0 <= pos; p0 += 32 * 4) {  // four positions per warp in flight
+    for (int p0 = lo + w; p0 < hi; p0 += 32 * 4) {  // four positions per warp in flight
         float d[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int p = p0 + 32 * u;
             const float* kp = p == pos ? kcur : kch + (int64_t)min(p, pos) * HD;
-            d[u] = p <= pos ? q0 * kp[l] + q1 * kp[l + 32] + q2 * kp[l + 64] + q3 * kp[l + 96] : -INFINITY;
+            d[u] = p < hi ? q0 * kp[l] + q1 * kp[l + 32] + q2 * kp[l + 64] + q3 * kp[l + 96] : -INFINITY;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             for (int o = 16; o; o >>= 1) d[u] += __shfl_xor_sync(FULL, d[u], o);
             const int p = p0 + 32 * u;
-            if (p <= pos) {
-                if (l == 0) ps[p] = d[u];
+            if (p < hi) {
+                if (l == 0) ps[p - lo] = d[u];
                 mx = fmaxf(mx, d[u]);
             }
         }
@@ -111,9 +118,9 @@ __global__ void __launch_bounds__(1024) glue_rope_attention(const float* __restr
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
     __syncthreads();
     float se = 0.f;
-    for (int p = t; p <= pos; p += blockDim.x) {
-        const float e = __expf(ps[p] - mx);
-        ps[p] = e;
+    for (int p = lo + t; p < hi; p += blockDim.x) {
+        const float e = __expf(ps[p - lo] - mx);
+        ps[p - lo] = e;
         se += e;
     }
     for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(FULL, se, o);
@@ -122,22 +129,50 @@ __global__ void __launch_bounds__(1024) glue_rope_attention(const float* __restr
     se = red[l];
     for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(FULL, se, o);
     const int g = t >> 7, dcol = t & (HD - 1);
+    const int vend = min(hi, pos);  // positions read from the cache; pos itself from smem
     float a8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // eight independent loads in flight
-    int p = g;
-    for (; p + 56 < pos; p += 64)
+    int p = lo + g;
+    for (; p + 56 < vend; p += 64)
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a8[u] += ps[p + 8 * u] * vch[(int64_t)(p + 8 * u) * HD + dcol];
-    for (; p < pos; p += 8) a8[0] += ps[p] * vch[(int64_t)p * HD + dcol];
+        for (int u = 0; u < 8; ++u) a8[u] += ps[p + 8 * u - lo] * vch[(int64_t)(p + 8 * u) * HD + dcol];
+    for (; p < vend; p += 8) a8[0] += ps[p - lo] * vch[(int64_t)p * HD + dcol];
     float acc = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
-    if ((pos & 7) == g) acc += ps[pos] * vcur[dcol];
+    if (hi == pos + 1 && lo <= pos && ((pos - lo) & 7) == g) acc += ps[pos - lo] * vcur[dcol];
     part[g][dcol] = acc;
     __syncthreads();
+    float* mine = ws + ((int64_t)h * kAttnSplits + sp) * (HD + 2);
     if (t < HD) {
         float o = 0.f;
 #pragma unroll
         for (int j = 0; j < 8; ++j) o += part[j][t];
-        out[(int64_t)h * HD + t] = o / se;
+        mine[2 + t] = o;
     }
+    if (t == 0) {
+        mine[0] = mx;
+        mine[1] = se;
+    }
+    __threadfence();
+    __syncthreads();
+    if (t == 0) {
+        last = atomicAdd(counters + h, 1u) == kAttnSplits - 1;
+        if (last) counters[h] = 0;  // ready for the next launch (graph replays)
+    }
+    __syncthreads();
+    if (!last || t >= HD) return;
+    __threadfence();
+    const float* hw = ws + (int64_t)h * kAttnSplits * (HD + 2);
+    float m = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < kAttnSplits; ++j) m = fmaxf(m, __ldcg(hw + j * (HD + 2)));
+    float num = 0.f, den = 0.f;
+#pragma unroll
+    for (int j = 0; j < kAttnSplits; ++j) {
+        const float mj = __ldcg(hw + j * (HD + 2));
+        const float f = mj == -INFINITY ? 0.f : __expf(mj - m);
+        den += f * __ldcg(hw + j * (HD + 2) + 1);
+        num += f * __ldcg(hw + j * (HD + 2) + 2 + t);
+    }
+    out[(int64_t)h * HD + t] = num / den;
 }
 
 __global__ void glue_silu_mul(const float* __restrict__ gu, float* __restrict__ out, int inter) {
@@ -161,15 +196,22 @@ extern "C" int itq3_glue_residual_rmsnorm(float* x, const float* r, const float*
     return check_launch("itq3_glue_residual_rmsnorm");
 }
 
+extern "C" int64_t itq3_glue_attention_ws_nbytes(int n_heads) {
+    return (int64_t)n_heads * (kAttnSplits * (128 + 2) * 4 + 4);
+}
+
 extern "C" int itq3_glue_rope_attention(const float* qkv, const float* cos_tab, const float* sin_tab,
                                         const int64_t* pos, float* k_cache, float* v_cache, float* out, int n_heads,
-                                        int n_kv, int head_dim, int ctx, void* stream) {
+                                        int n_kv, int head_dim, int ctx, void* ws, void* stream) {
     if (head_dim != 128 || ctx > 1024 || n_kv <= 0 || n_heads % n_kv) {
         set_error("itq3_glue_rope_attention: head_dim 128, ctx <= 1024, n_heads a multiple of n_kv");
         return ITQ3_E_UNSUPPORTED;
     }
-    glue_rope_attention<<<n_heads, 1024, 0, (cudaStream_t)stream>>>(qkv, cos_tab, sin_tab, pos, k_cache, v_cache, out,
-                                                                   n_heads, n_kv, ctx);
+    // ws: [n_heads][splits][2 + 128] fp32 partials, then n_heads u32 counters (zero before first use)
+    float* part = (float*)ws;
+    unsigned* cnt = (unsigned*)(part + (int64_t)n_heads * kAttnSplits * (128 + 2));
+    glue_rope_attention<<<dim3(n_heads, kAttnSplits), 1024, 0, (cudaStream_t)stream>>>(
+        qkv, cos_tab, sin_tab, pos, k_cache, v_cache, out, n_heads, n_kv, ctx, part, cnt);
     return check_launch("itq3_glue_rope_attention");
 }
 

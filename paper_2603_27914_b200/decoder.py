@@ -63,6 +63,10 @@ class DecoderStack:
         self.hbuf = torch.zeros(self.h, device=self.dev)        # normalised input of a projection
         self.att = torch.zeros(self.h, device=self.dev)         # attention output (nh * hd)
         self.act = torch.zeros(self.inter, device=self.dev)     # SiLU(gate) * up
+        from . import _lib
+
+        self.attn_ws = torch.zeros(_lib.load().itq3_glue_attention_ws_nbytes(self.nh), dtype=torch.uint8,
+                                   device=self.dev)  # split partials + per-head counters
         if self.hd != 128 or max_ctx > 1024 or self.nh * self.hd != self.h:
             raise ValueError("DecoderStack: the glue kernels need head_dim 128, max_ctx <= 1024, nh * hd = hidden")
         self.graph = None
@@ -89,7 +93,7 @@ class DecoderStack:
             qkv = fused_matvec(qkv_w, h, check_finite=False)
             _lib.call("itq3_glue_rope_attention", _lib.ptr(qkv), _lib.ptr(self.cos), _lib.ptr(self.sin),
                       _lib.ptr(self.pos), _lib.ptr(self.k_cache[li, 0]), _lib.ptr(self.v_cache[li, 0]),
-                      _lib.ptr(self.att), self.nh, self.nkv, self.hd, self.max_ctx, st)
+                      _lib.ptr(self.att), self.nh, self.nkv, self.hd, self.max_ctx, _lib.ptr(self.attn_ws), st)
             o = fused_matvec(o_w, self.att, check_finite=False)
             _lib.call("itq3_glue_residual_rmsnorm", _lib.ptr(xs), _lib.ptr(o), _lib.ptr(self.gain[li][1]),
                       _lib.ptr(h), self.h, self.eps, st)
@@ -135,7 +139,11 @@ class DecoderStack:
         cos, sin = self.cos[pos:pos + 1], self.sin[pos:pos + 1]
         kvd = self.nkv * self.hd
         for li in range(self.layers):
-            W = [torch.as_tensor(dequantize_tensor(q), device=self.dev).float() for q in self.q[li]]
+            if not hasattr(self, "_ref_w"):
+                self._ref_w = {}
+            if li not in self._ref_w:
+                self._ref_w[li] = [torch.as_tensor(dequantize_tensor(q), device=self.dev).float() for q in self.q[li]]
+            W = self._ref_w[li]
             g1, g2 = self.gain[li][0], self.gain[li][1]
             qkv = W[0] @ self._rms(h, g1)
             q = self._rope(qkv[: self.h].view(self.nh, self.hd), cos, sin)
