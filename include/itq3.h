@@ -221,11 +221,17 @@ int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* tiled, void
  * all npeer ranks' copies of y (d_peers: device array of npeer pointers, e.g. symmetric-memory peer
  * addresses over NVLink; peer p's copy sits at the same layout as `y`).  y holds
  * 2 x nch x yrows u64 words (epoch-parity double buffer), nch = ceil(cols / 4096).  All ranks launch
- * itq3_chain_run the same number of times; consumers and the final fold read the full yrows rows. */
+ * itq3_chain_run the same number of times; consumers and the final fold read the full yrows rows.
+ * `asymmetric` (both write_desc calls) is a flag word: bit 0 = asymmetric zero-points, bit 1 = gated
+ * input -- the stage reads SiLU(prev[i]) * prev[cols + i] from the previous stage's output (a
+ * gate | up projection feeding a down projection). */
 int itq3_chain_write_desc_tp(void* host_desc, int index, const uint8_t* tiled, void* y, int64_t rows, int64_t cols,
                              int asymmetric, int64_t row0, int64_t yrows, const void* d_peers, int npeer);
 int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch, float* out,
                    int grid, void* d_trace, void* stream);
+/* the same, for chains with gated stages (descriptor flag bit 1) */
+int itq3_chain_run_gated(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch, float* out,
+                         int grid, void* d_trace, void* stream);
 
 /* ---- K8 evaluation harness: replaces eval_error / eval_container / rotation_benefit
  * (compute.py:221-356).  One call quantises (payload == NULL: eval_error with the given

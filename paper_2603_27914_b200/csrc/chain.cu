@@ -323,6 +323,8 @@ __device__ __forceinline__ bool stage_get(const ChainSmem& sm, const ChainStage*
 //   0 stage entered, 1 input observed ready, 2 input rotated, 3 own units done
 // 18 warps: the per-SMSP register file (16K) caps a 5-warp SMSP at 96 registers/thread
 
+template <bool GATED>  // GATED: some stage reads SiLU(gate) * up (a separate instantiation keeps the
+                      // plain kernel's register allocation)
 __global__ void __launch_bounds__(kChainThreads, 1)
     chain_kernel(const ChainStage* __restrict__ stages, int S, const float* __restrict__ x0, int L,
                  unsigned* __restrict__ epoch_ptr, float* __restrict__ out,
@@ -410,7 +412,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                 const uint8_t* zps = scales + (int64_t)st.RT * st.NB * 32;
                 const int b0 = sp.ch * kUnitBlocks;
                 const int nb = min(kUnitBlocks, st.NB - b0);
-                const unsigned bytes = nb * (1024 + 32 + (st.asym ? 16 : 0));
+                const unsigned bytes = nb * (1024 + 32 + ((st.asym & 1) ? 16 : 0));
                 for (int rt = sp.rt0; rt < st.RT; rt += sp.Gc) {
                     mbar_wait(&sm.empty[slot], phase ^ 1u);
                     const int64_t t0 = (int64_t)rt * st.NB + b0;
@@ -418,7 +420,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                     uint8_t* dst = sm.ring[slot];
                     bulk_g2s(dst, st.tiled + t0 * 1024, nb * 1024, &sm.full[slot]);
                     bulk_g2s(dst + kSlotCodes, scales + t0 * 32, nb * 32, &sm.full[slot]);
-                    if (st.asym) bulk_g2s(dst + kSlotCodes + kSlotScales, zps + t0 * 16, nb * 16, &sm.full[slot]);
+                    if (st.asym & 1) bulk_g2s(dst + kSlotCodes + kSlotScales, zps + t0 * 16, nb * 16, &sm.full[slot]);
                     if (++slot == kNumSlots) {
                         slot = 0;
                         phase ^= 1u;
@@ -460,11 +462,21 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             } else {
                 const ChainStage pv = s - 1 < kSmemStages ? sm.desc[s - 1] : stages[s - 1];
                 const int pn = (pv.NB + kUnitBlocks - 1) / kUnitBlocks;
+                const unsigned long long* src = pv.y + 256 * (b0 + warp);
                 if (pv.npeer == 0) {
-                    load_tagged_block<false>(pv.y + 256 * (b0 + warp), pn, pv.yrows, epoch, lane, f);
+                    load_tagged_block<false>(src, pn, pv.yrows, epoch, lane, f);
                 } else {
-                    const int64_t par = (int64_t)(epoch & 1u) * pn * pv.yrows;
-                    load_tagged_block<true>(pv.y + par + 256 * (b0 + warp), pn, pv.yrows, epoch, lane, f);
+                    src += (int64_t)(epoch & 1u) * pn * pv.yrows;
+                    load_tagged_block<true>(src, pn, pv.yrows, epoch, lane, f);
+                }
+                if (GATED && (st.asym & 2)) {  // gated input: SiLU(prev[i]) * prev[cols + i] (gate | up halves)
+                    float u[8];
+                    if (pv.npeer == 0)
+                        load_tagged_block<false>(src + st.cols, pn, pv.yrows, epoch, lane, u);
+                    else
+                        load_tagged_block<true>(src + st.cols, pn, pv.yrows, epoch, lane, u);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) f[e] = f[e] / (1.f + __expf(-f[e])) * u[e];
                 }
             }
             if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 1] = globaltimer();
@@ -514,8 +526,8 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 #else
                 if (has_block) {
 #endif
-                    ra = chain_tile(sm.ring[slot0], warp, lane, g, bf, fcx, corr, st.asym);
-                    if (two) rb = chain_tile(sm.ring[slot1], warp, lane, g, bf, fcx, corr, st.asym);
+                    ra = chain_tile(sm.ring[slot0], warp, lane, g, bf, fcx, corr, st.asym & 1);
+                    if (two) rb = chain_tile(sm.ring[slot1], warp, lane, g, bf, fcx, corr, st.asym & 1);
                     // combine the quad's limb-pair columns (lanes t = 0..3, fixed order)
                     ra.x += __shfl_xor_sync(FULL, ra.x, 1);
                     ra.y += __shfl_xor_sync(FULL, ra.y, 1);
@@ -634,8 +646,9 @@ extern "C" int itq3_chain_write_desc_tp(void* host_desc, int index, const uint8_
     return ITQ3_OK;
 }
 
-extern "C" int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch,
-                              float* out, int grid, void* d_trace, void* stream) {
+template <bool GATED>
+static int chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch, float* out,
+                     int grid, void* d_trace, void* stream) {
     if (limbs < 1 || limbs > kMaxLimbs) {
         set_error("chain: limbs must be in [1, %d]", kMaxLimbs);
         return ITQ3_E_DOMAIN;
@@ -643,7 +656,7 @@ extern "C" int itq3_chain_run(const void* d_desc, int n_stages, const float* x0,
     static bool attr_set = false;
     const int smem = (int)sizeof(ChainSmem);
     if (!attr_set) {
-        if (cudaFuncSetAttribute(chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        if (cudaFuncSetAttribute(chain_kernel<GATED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
             return check_launch("chain: smem attribute");
         attr_set = true;
     }
@@ -663,11 +676,21 @@ extern "C" int itq3_chain_run(const void* d_desc, int n_stages, const float* x0,
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, chain_kernel, (const ChainStage*)d_desc, n_stages, x0, limbs,
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, chain_kernel<GATED>, (const ChainStage*)d_desc, n_stages, x0, limbs,
                                              d_epoch, out, (unsigned long long*)d_trace);
     if (e != cudaSuccess) {
         set_error("chain: launch failed: %s", cudaGetErrorString(e));
         return ITQ3_E_CUDA;
     }
     return check_launch("itq3_chain_run");
+}
+
+extern "C" int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch,
+                              float* out, int grid, void* d_trace, void* stream) {
+    return chain_run<false>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
+}
+
+extern "C" int itq3_chain_run_gated(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch,
+                                    float* out, int grid, void* d_trace, void* stream) {
+    return chain_run<true>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
 }

@@ -4,8 +4,10 @@ batch-1 decode tokens/s metric.  None of it exists in the reference; it only fra
 
 Per layer and token: [residual +] RMSNorm -> qkv GEMV -> RoPE + KV-cache append + grouped-query
 attention over the cache -> o GEMV -> residual + RMSNorm -> gate_up GEMV -> SiLU(gate) * up -> down
-GEMV.  The GEMVs are one-stage chain launches (csrc/chain.cu, one cooperative kernel each); the glue
-is three small kernels (csrc/decoder_glue.cu), so a layer is 8 launches.  A whole token step is ONE CUDA
+GEMV.  qkv and o are one-stage chain launches (csrc/chain.cu, one cooperative kernel each); gate_up,
+the SiLU gating and down are ONE two-stage chain launch (the down stage applies the gating while
+loading its input); the rest of the glue is two small kernels (csrc/decoder_glue.cu), so a layer
+is 6 launches.  A whole token step is ONE CUDA
 graph: the position lives in a device tensor that the graph itself advances, the attention reads
 the full cache under a position mask, so replays need no host work.
 """
@@ -20,6 +22,37 @@ from .codec import QuantizedTensor, quantize_tensor
 from .compute import fused_matvec
 
 LLAMA3_8B = dict(hidden=4096, inter=14336, n_heads=32, n_kv=8, head_dim=128, rope_theta=500000.0)
+
+
+class _GatedPair:
+    """gate_up -> SiLU(gate) * up -> down as ONE two-stage chain launch (csrc/chain.cu, gated stage
+    flag): the down projection's consumers read both halves of the gate_up output and apply the
+    gating while loading, so neither the intermediate activation nor a second launch exists."""
+
+    def __init__(self, q_gu: QuantizedTensor, q_down: QuantizedTensor, dev):
+        import ctypes
+
+        from . import _lib
+
+        self._lib = _lib
+        lib = _lib.load()
+        host = ctypes.create_string_buffer(lib.itq3_chain_desc_nbytes() * 2)
+        self.y = []
+        for i, (q, flag) in enumerate(((q_gu, 0), (q_down, 2))):
+            nch = -(-q.cols // 4096)
+            y = torch.zeros((nch, q.rows), dtype=torch.int64, device=dev)  # tagged outputs, epoch 0
+            self.y.append(y)
+            _lib.check(lib.itq3_chain_write_desc(host, i, _lib.ptr(q.tiled()), _lib.ptr(y), None, q.rows, q.cols,
+                                                 int(not q.symmetric) | flag, 0))
+        self.desc = torch.frombuffer(bytearray(host.raw), dtype=torch.uint8).to(dev)
+        self.epoch = torch.zeros(2, dtype=torch.int32, device=dev)
+        self.out = torch.zeros(q_down.rows, dtype=torch.float32, device=dev)
+
+    def __call__(self, x: torch.Tensor, stream: int) -> torch.Tensor:
+        lib = self._lib
+        lib.call("itq3_chain_run_gated", lib.ptr(self.desc), 2, lib.ptr(x), 3, lib.ptr(self.epoch), lib.ptr(self.out),
+                 0, None, stream)
+        return self.out
 
 
 class DecoderStack:
@@ -62,13 +95,13 @@ class DecoderStack:
         self.xs = torch.zeros(self.h, device=self.dev)          # residual stream
         self.hbuf = torch.zeros(self.h, device=self.dev)        # normalised input of a projection
         self.att = torch.zeros(self.h, device=self.dev)         # attention output (nh * hd)
-        self.act = torch.zeros(self.inter, device=self.dev)     # SiLU(gate) * up
         from . import _lib
 
         self.attn_ws = torch.zeros(_lib.load().itq3_glue_attention_ws_nbytes(self.nh), dtype=torch.uint8,
                                    device=self.dev)  # split partials + per-head counters
         if self.hd != 128 or max_ctx > 1024 or self.nh * self.hd != self.h:
             raise ValueError("DecoderStack: the glue kernels need head_dim 128, max_ctx <= 1024, nh * hd = hidden")
+        self.pairs = [_GatedPair(row[2], row[3], self.dev) for row in self.q]
         self.graph = None
 
     def _rms(self, x, gain):
@@ -79,7 +112,7 @@ class DecoderStack:
         return torch.cat((a * cos - b * sin, a * sin + b * cos), dim=1)
 
     def _step(self) -> None:
-        """One token: 4 GEMV launches + 4 glue launches per layer (csrc/decoder_glue.cu)."""
+        """One token: 3 chain launches (qkv, o, gated gate_up+down) + 3 glue launches per layer."""
         from . import _lib
 
         st = _lib.stream_ptr(self.dev)
@@ -87,7 +120,7 @@ class DecoderStack:
         xs.copy_(self.x)
         prev = None
         for li in range(self.layers):
-            qkv_w, o_w, gu_w, down_w = self.q[li]
+            qkv_w, o_w = self.q[li][0], self.q[li][1]
             _lib.call("itq3_glue_residual_rmsnorm", _lib.ptr(xs), _lib.ptr(prev) if prev is not None else None,
                       _lib.ptr(self.gain[li][0]), _lib.ptr(h), self.h, self.eps, st)
             qkv = fused_matvec(qkv_w, h, check_finite=False)
@@ -97,9 +130,7 @@ class DecoderStack:
             o = fused_matvec(o_w, self.att, check_finite=False)
             _lib.call("itq3_glue_residual_rmsnorm", _lib.ptr(xs), _lib.ptr(o), _lib.ptr(self.gain[li][1]),
                       _lib.ptr(h), self.h, self.eps, st)
-            gu = fused_matvec(gu_w, h, check_finite=False)
-            _lib.call("itq3_glue_silu_mul", _lib.ptr(gu), _lib.ptr(self.act), self.inter, st)
-            prev = fused_matvec(down_w, self.act, check_finite=False)
+            prev = self.pairs[li](h, st)  # gate_up + SiLU gating + down: one chain launch
         _lib.call("itq3_glue_residual_rmsnorm", _lib.ptr(xs), _lib.ptr(prev), None, _lib.ptr(self.out), self.h,
                   self.eps, st)
         self.pos.add_(1)
