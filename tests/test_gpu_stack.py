@@ -88,3 +88,23 @@ def test_chain_replay_deterministic_and_matches_kernels():
         np.testing.assert_array_equal(a.forward(x), ya)  # graph replays are bitwise reproducible
     yb = b.forward(x)
     np.testing.assert_allclose(ya, yb, rtol=1e-3, atol=1e-4 * np.abs(yb).max())
+
+
+def test_chain_beyond_smem_descriptor_cache():
+    """170 stages: descriptors past the kernel's shared-memory cache (150) come from global memory
+    with the work split computed per stage; every stage still matches the oracle bound."""
+    shapes = [(512, 256), (256, 512)] * 85
+    qs = build(21, shapes=shapes)
+    pays = [q.payload().cpu().numpy() for q in qs]
+    st = LinearStack(qs, limbs=3, mode="chain")
+    x = np.random.default_rng(3).standard_normal(qs[0].cols).astype(np.float32)
+    out = st.forward(x)
+    xin = x.astype(np.float64)
+    for i, q in enumerate(qs):
+        y = st.stage_output(i).cpu().numpy().astype(np.float64)
+        if i >= 140 or i % 20 == 0:
+            exact, bound = chain_bound(pays[i], q.rows, q.cols, xin, 3)
+            assert np.all(np.abs(y - exact) <= bound), (i, np.max(np.abs(y - exact) / bound))
+        if i + 1 < len(qs):
+            xin = y[: qs[i + 1].cols]
+    np.testing.assert_array_equal(out, st.stage_output(len(qs) - 1).cpu().numpy())
