@@ -89,15 +89,13 @@ int itq3_ternary_dequantize(const int8_t* codes, int64_t n, double d, int z, dou
 int itq3_uniform_quantize(const double* x, int64_t n, double delta, double wmin, double wmax, double* out,
                           void* stream);
 
-/* ---- decoder-stack glue (decoder.py; not on the ITQ3_S path): x += r, out = RMSNorm(x) * gain
- * (r / gain may be NULL); RoPE + KV append + grouped-query decode attention (head_dim 128,
- * ctx <= 1024, position read from *pos); SiLU(gate) * up. */
-int itq3_glue_residual_rmsnorm(float* x, const float* r, const float* gain, float* out, int n, float eps, void* stream);
-int64_t itq3_glue_attention_ws_nbytes(int n_heads);  /* zero-initialise once */
+/* ---- decoder-stack glue (decoder.py; not on the ITQ3_S path): RoPE + KV append + grouped-query
+ * split decode attention (head_dim 128, ctx <= 1024, position read from *pos); ws from
+ * itq3_glue_attention_ws_nbytes, zero-initialised once. */
+int64_t itq3_glue_attention_ws_nbytes(int n_heads);
 int itq3_glue_rope_attention(const float* qkv, const float* cos_tab, const float* sin_tab, const int64_t* pos,
                              float* k_cache, float* v_cache, float* out, int n_heads, int n_kv, int head_dim, int ctx,
                              void* ws, void* stream);
-int itq3_glue_silu_mul(const float* gu, float* out, int inter, void* stream);
 
 /* ---- transform: fwht_forward / fwht_inverse (transform.py:61-96) on n_vec
  * contiguous vectors of length n (2..512, power of two), dtype F32 or F64,
@@ -224,7 +222,9 @@ int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* tiled, void
  * itq3_chain_run the same number of times; consumers and the final fold read the full yrows rows.
  * `asymmetric` (both write_desc calls) is a flag word: bit 0 = asymmetric zero-points, bit 1 = gated
  * input -- the stage reads SiLU(prev[i]) * prev[cols + i] from the previous stage's output (a
- * gate | up projection feeding a down projection). */
+ * gate | up projection feeding a down projection); bit 2 = RMSNorm input (stage 0, cols <= 4096:
+ * x0 * rsqrt(mean(x0^2) + 1e-5) * xin, `xin` carrying the gain); bit 3 = the final fold adds into
+ * `out` (residual stream) instead of overwriting it.  Bits 1-3 need itq3_chain_run_gated. */
 int itq3_chain_write_desc_tp(void* host_desc, int index, const uint8_t* tiled, void* y, int64_t rows, int64_t cols,
                              int asymmetric, int64_t row0, int64_t yrows, const void* d_peers, int npeer);
 int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch, float* out,

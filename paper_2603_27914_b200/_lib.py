@@ -36,10 +36,8 @@ SIGNATURES = {
     "itq3_ternary_quantize": (_i32, [_vp, _i64, _dbl, _i32, _vp, _vp]),
     "itq3_ternary_dequantize": (_i32, [_vp, _i64, _dbl, _i32, _vp, _vp]),
     "itq3_uniform_quantize": (_i32, [_vp, _i64, _dbl, _dbl, _dbl, _vp, _vp]),
-    "itq3_glue_residual_rmsnorm": (_i32, [_vp, _vp, _vp, _vp, _i32, ctypes.c_float, _vp]),
     "itq3_glue_attention_ws_nbytes": (_i64, [_i32]),
     "itq3_glue_rope_attention": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),
-    "itq3_glue_silu_mul": (_i32, [_vp, _vp, _i32, _vp]),
     "itq3_fwht": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp]),
     "itq3_eval_ws_nbytes": (ctypes.c_size_t, [_i64, _i32]),
     "itq3_eval_ws_offset": (_i64, [_i64, _i32, _i32]),

@@ -275,6 +275,7 @@ struct ChainSmem {
     alignas(128) uint8_t ring[kNumSlots][kSlotBytes];
     uint8_t rot[kChainConsumerWarps][kActSmemBlock];   // per-warp rotation scratch (own block only)
     float part[kNumSlots][kChainConsumerWarps][16];    // per-warp row partials of a unit
+    float normsq[kChainConsumerWarps];                 // per-warp sums of squares (RMSNorm input stages)
     uint64_t full[kNumSlots];
     uint64_t empty[kNumSlots];
     uint64_t parts[kNumSlots];  // 16 warps' partials of the unit in this slot are written
@@ -450,12 +451,38 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         const int b0 = sp.ch * kUnitBlocks;
         const int nb = min(kUnitBlocks, st.NB - b0);
         const bool has_block = warp < nb;
+        float nscale = 1.f;
+        if (GATED && (st.asym & 4)) {
+            // RMSNorm input stage (decoder; host-checked cols <= 4096, so this CTA's chunk is the whole
+            // input vector): every consumer warp adds its block's squares, one named barrier, and the
+            // scale multiplies the input as it is loaded below
+            float ss = 0.f;
+            if (has_block)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const float v = __ldg(x0 + 256 * (b0 + warp) + lane + 32 * e);
+                    ss += v * v;
+                }
+            for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
+            if (lane == 0) sm.normsq[warp] = ss;
+            consumer_sync();
+            float tot = 0.f;
+#pragma unroll
+            for (int w = 0; w < kChainConsumerWarps; ++w) tot += sm.normsq[w];
+            nscale = rsqrtf(tot / (float)st.cols + 1e-5f);
+        }
         uint2 bf[8];
         float fcx = 0.f, corr = 0.f;
         long long c0 = prof ? clock64() : 0;
         if (has_block) {
             float f[8];
-            if (s == 0 || st.xin) {
+            if (GATED && (st.asym & 4)) {
+                // RMSNorm input: x0 * rsqrt(mean(x0^2) + 1e-5) * gain (gain in st.xin)
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    f[e] = __ldg(x0 + 256 * (b0 + warp) + lane + 32 * e) * nscale *
+                           __ldg(st.xin + 256 * (b0 + warp) + lane + 32 * e);
+            } else if (s == 0 || st.xin) {
                 const float* xs = st.xin ? st.xin : x0;
 #pragma unroll
                 for (int e = 0; e < 8; ++e) f[e] = __ldg(xs + 256 * (b0 + warp) + lane + 32 * e);
@@ -588,7 +615,10 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             if (ok) break;
             __nanosleep(64);
         }
-        out[r] = v;
+        if (GATED && (last.asym & 8))
+            out[r] += v;  // residual accumulation (decoder): out is the residual stream
+        else
+            out[r] = v;
     }
     if (cta == 0 && tid == 0) {
         while (atomicAdd(epoch_ptr + 1, 0u) < (unsigned)G) __nanosleep(32);
@@ -630,6 +660,10 @@ extern "C" int itq3_chain_write_desc_tp(void* host_desc, int index, const uint8_
         set_error("chain: stage %d: bad tensor-parallel shard (row0 %lld, rows %lld, yrows %lld, npeer %d)", index,
                   (long long)row0, (long long)rows, (long long)yrows, npeer);
         return ITQ3_E_DOMAIN;
+    }
+    if ((asymmetric & 4) && cols > 4096) {
+        set_error("chain: stage %d: an RMSNorm input stage needs cols <= 4096 (got %lld)", index, (long long)cols);
+        return ITQ3_E_UNSUPPORTED;
     }
     st.tiled = tiled;
     st.y = (unsigned long long*)y;

@@ -1,52 +1,10 @@
-// Decoder-stack glue (decoder.py): the non-ITQ3 operations of a
-// Llama-style decode step fused into three small kernels so that a layer is 4 GEMV launches + 4
-// glue launches.  Not on the ITQ3_S hot path; fp32 throughout.
+// Decoder-stack glue (decoder.py): the one non-ITQ3 operation of a
+// Llama-style decode step that does not fold into the chain launches -- RoPE + KV-cache append +
+// grouped-query decode attention.  (RMSNorm, SiLU gating and the residual adds live in the chain
+// kernel's decoder flags.)  Not on the ITQ3_S hot path; fp32 throughout.
 #include "common.cuh"
 
 namespace itq3 {
-
-constexpr int kGlueThreads = 1024;
-
-__device__ __forceinline__ float block_sum(float v, float* red) {
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
-    if (l == 0) red[w] = v;
-    __syncthreads();
-    v = l < (int)(blockDim.x >> 5) ? red[l] : 0.f;
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-    return v;
-}
-
-// x += r (if r), then out = x * rsqrt(mean(x^2) + eps) * gain (if gain; else out = x).  One CTA;
-// each thread keeps its (up to 8) elements in registers across the reduction.
-__global__ void __launch_bounds__(kGlueThreads) glue_residual_rmsnorm(float* __restrict__ x,
-                                                                     const float* __restrict__ r,
-                                                                     const float* __restrict__ gain,
-                                                                     float* __restrict__ out, int n, float eps) {
-    __shared__ float red[32];
-    constexpr int kPer = 8;  // n <= 8 * 1024
-    float v[kPer];
-    float ss = 0.f;
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-        const int i = threadIdx.x + j * kGlueThreads;
-        v[j] = 0.f;
-        if (i < n) {
-            v[j] = x[i] + (r ? r[i] : 0.f);
-            if (r) x[i] = v[j];
-            ss += v[j] * v[j];
-        }
-    }
-    float s = 1.f;
-    if (gain) s = rsqrtf(block_sum(ss, red) / (float)n + eps);
-    if (!out) return;
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-        const int i = threadIdx.x + j * kGlueThreads;
-        if (i < n) out[i] = gain ? v[j] * s * gain[i] : v[j];
-    }
-}
 
 // Flash-decoding attention: CTA (h, sp) of a (query head, position split) grid handles positions
 // [lo, hi) of 0..pos.  Every CTA applies RoPE (rotate-half) to its query and to its kv head's key at
@@ -175,26 +133,9 @@ __global__ void __launch_bounds__(1024) glue_rope_attention(const float* __restr
     out[(int64_t)h * HD + t] = num / den;
 }
 
-__global__ void glue_silu_mul(const float* __restrict__ gu, float* __restrict__ out, int inter) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= inter) return;
-    const float g = gu[i];
-    out[i] = g / (1.f + __expf(-g)) * gu[inter + i];
-}
-
 }  // namespace itq3
 
 using namespace itq3;
-
-extern "C" int itq3_glue_residual_rmsnorm(float* x, const float* r, const float* gain, float* out, int n, float eps,
-                                          void* stream) {
-    if (n <= 0 || n > 8 * kGlueThreads) {
-        set_error("itq3_glue_residual_rmsnorm: 0 < n <= %d", 8 * kGlueThreads);
-        return ITQ3_E_SHAPE;
-    }
-    glue_residual_rmsnorm<<<1, kGlueThreads, 0, (cudaStream_t)stream>>>(x, r, gain, out, n, eps);
-    return check_launch("itq3_glue_residual_rmsnorm");
-}
 
 extern "C" int64_t itq3_glue_attention_ws_nbytes(int n_heads) {
     return (int64_t)n_heads * (kAttnSplits * (128 + 2) * 4 + 4);
@@ -213,9 +154,4 @@ extern "C" int itq3_glue_rope_attention(const float* qkv, const float* cos_tab, 
     glue_rope_attention<<<dim3(n_heads, kAttnSplits), 1024, 0, (cudaStream_t)stream>>>(
         qkv, cos_tab, sin_tab, pos, k_cache, v_cache, out, n_heads, n_kv, ctx, part, cnt);
     return check_launch("itq3_glue_rope_attention");
-}
-
-extern "C" int itq3_glue_silu_mul(const float* gu, float* out, int inter, void* stream) {
-    glue_silu_mul<<<(inter + 255) / 256, 256, 0, (cudaStream_t)stream>>>(gu, out, inter);
-    return check_launch("itq3_glue_silu_mul");
 }

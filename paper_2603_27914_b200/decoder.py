@@ -4,10 +4,11 @@ batch-1 decode tokens/s metric.  None of it exists in the reference; it only fra
 
 Per layer and token: [residual +] RMSNorm -> qkv GEMV -> RoPE + KV-cache append + grouped-query
 attention over the cache -> o GEMV -> residual + RMSNorm -> gate_up GEMV -> SiLU(gate) * up -> down
-GEMV.  qkv and o are one-stage chain launches (csrc/chain.cu, one cooperative kernel each); gate_up,
-the SiLU gating and down are ONE two-stage chain launch (the down stage applies the gating while
-loading its input); the rest of the glue is two small kernels (csrc/decoder_glue.cu), so a layer
-is 6 launches.  A whole token step is ONE CUDA
+GEMV.  Everything but the attention runs inside chain launches (csrc/chain.cu, decoder flags): the
+RMSNorm in the loads of the qkv / gate_up stages (every CTA of a 4096-column stage holds the whole
+input), the SiLU gating in the loads of the down stage, the residual adds in the final folds; the
+attention (RoPE + KV append + split decode attention) is one glue kernel (csrc/decoder_glue.cu).
+A layer is 4 launches: [RMSNorm -> qkv], attention, [o -> +=], [RMSNorm -> gate_up -> gate -> down -> +=].  A whole token step is ONE CUDA
 graph: the position lives in a device tensor that the graph itself advances, the attention reads
 the full cache under a position mask, so replays need no host work.
 """
@@ -24,35 +25,41 @@ from .compute import fused_matvec
 LLAMA3_8B = dict(hidden=4096, inter=14336, n_heads=32, n_kv=8, head_dim=128, rope_theta=500000.0)
 
 
-class _GatedPair:
-    """gate_up -> SiLU(gate) * up -> down as ONE two-stage chain launch (csrc/chain.cu, gated stage
-    flag): the down projection's consumers read both halves of the gate_up output and apply the
-    gating while loading, so neither the intermediate activation nor a second launch exists."""
+class _Chain:
+    """A short chain of ITQ3_S stages run as ONE cooperative launch (csrc/chain.cu, decoder flags):
+    stages = [(QuantizedTensor, flags, gain)], flags bit 1 = gated input (SiLU(gate) * up of the
+    previous stage), bit 2 = RMSNorm input with `gain` (first stage), bit 3 = the fold adds into `out`
+    (the residual stream) instead of overwriting it."""
 
-    def __init__(self, q_gu: QuantizedTensor, q_down: QuantizedTensor, dev):
+    def __init__(self, stages, out: torch.Tensor, dev):
         import ctypes
 
         from . import _lib
 
         self._lib = _lib
         lib = _lib.load()
-        host = ctypes.create_string_buffer(lib.itq3_chain_desc_nbytes() * 2)
-        self.y = []
-        for i, (q, flag) in enumerate(((q_gu, 0), (q_down, 2))):
-            nch = -(-q.cols // 4096)
-            y = torch.zeros((nch, q.rows), dtype=torch.int64, device=dev)  # tagged outputs, epoch 0
+        host = ctypes.create_string_buffer(lib.itq3_chain_desc_nbytes() * len(stages))
+        self.y, self.keep = [], []
+        for i, (q, flags, gain) in enumerate(stages):
+            y = torch.zeros((-(-q.cols // 4096), q.rows), dtype=torch.int64, device=dev)  # tagged outputs
             self.y.append(y)
-            _lib.check(lib.itq3_chain_write_desc(host, i, _lib.ptr(q.tiled()), _lib.ptr(y), None, q.rows, q.cols,
-                                                 int(not q.symmetric) | flag, 0))
+            self.keep.append(gain)
+            _lib.check(lib.itq3_chain_write_desc(host, i, _lib.ptr(q.tiled()), _lib.ptr(y),
+                                                 _lib.ptr(gain) if gain is not None else None, q.rows, q.cols,
+                                                 int(not q.symmetric) | flags, 0))
+        self.n = len(stages)
         self.desc = torch.frombuffer(bytearray(host.raw), dtype=torch.uint8).to(dev)
         self.epoch = torch.zeros(2, dtype=torch.int32, device=dev)
-        self.out = torch.zeros(q_down.rows, dtype=torch.float32, device=dev)
+        self.out = out
 
     def __call__(self, x: torch.Tensor, stream: int) -> torch.Tensor:
         lib = self._lib
-        lib.call("itq3_chain_run_gated", lib.ptr(self.desc), 2, lib.ptr(x), 3, lib.ptr(self.epoch), lib.ptr(self.out),
-                 0, None, stream)
+        lib.call("itq3_chain_run_gated", lib.ptr(self.desc), self.n, lib.ptr(x), 3, lib.ptr(self.epoch),
+                 lib.ptr(self.out), 0, None, stream)
         return self.out
+
+
+GATED, NORM_IN, ADD_OUT = 2, 4, 8
 
 
 class DecoderStack:
@@ -93,7 +100,6 @@ class DecoderStack:
         self.out = torch.zeros(self.h, device=self.dev)
         self.kpos = torch.arange(max_ctx, device=self.dev)
         self.xs = torch.zeros(self.h, device=self.dev)          # residual stream
-        self.hbuf = torch.zeros(self.h, device=self.dev)        # normalised input of a projection
         self.att = torch.zeros(self.h, device=self.dev)         # attention output (nh * hd)
         from . import _lib
 
@@ -101,7 +107,14 @@ class DecoderStack:
                                    device=self.dev)  # split partials + per-head counters
         if self.hd != 128 or max_ctx > 1024 or self.nh * self.hd != self.h:
             raise ValueError("DecoderStack: the glue kernels need head_dim 128, max_ctx <= 1024, nh * hd = hidden")
-        self.pairs = [_GatedPair(row[2], row[3], self.dev) for row in self.q]
+        # per layer: [RMSNorm -> qkv], [o -> += residual], [RMSNorm -> gate_up -> SiLU gating -> down -> += residual]
+        self.qkv_out = torch.zeros(self.h + 2 * kv, device=self.dev)
+        self.chains = []
+        for li, (qkv_w, o_w, gu_w, down_w) in enumerate(self.q):
+            g1, g2 = self.gain[li][0], self.gain[li][1]
+            self.chains.append((_Chain([(qkv_w, NORM_IN, g1)], self.qkv_out, self.dev),
+                                _Chain([(o_w, ADD_OUT, None)], self.xs, self.dev),
+                                _Chain([(gu_w, NORM_IN, g2), (down_w, GATED | ADD_OUT, None)], self.xs, self.dev)))
         self.graph = None
 
     def _rms(self, x, gain):
@@ -112,27 +125,22 @@ class DecoderStack:
         return torch.cat((a * cos - b * sin, a * sin + b * cos), dim=1)
 
     def _step(self) -> None:
-        """One token: 3 chain launches (qkv, o, gated gate_up+down) + 3 glue launches per layer."""
+        """One token: per layer 3 chain launches ([RMSNorm -> qkv], [o -> += x], [RMSNorm -> gate_up ->
+        SiLU gating -> down -> += x]) and one glue launch (RoPE + KV append + split attention)."""
         from . import _lib
 
         st = _lib.stream_ptr(self.dev)
-        xs, h = self.xs, self.hbuf
+        xs = self.xs
         xs.copy_(self.x)
-        prev = None
         for li in range(self.layers):
-            qkv_w, o_w = self.q[li][0], self.q[li][1]
-            _lib.call("itq3_glue_residual_rmsnorm", _lib.ptr(xs), _lib.ptr(prev) if prev is not None else None,
-                      _lib.ptr(self.gain[li][0]), _lib.ptr(h), self.h, self.eps, st)
-            qkv = fused_matvec(qkv_w, h, check_finite=False)
+            c_qkv, c_o, c_mlp = self.chains[li]
+            qkv = c_qkv(xs, st)
             _lib.call("itq3_glue_rope_attention", _lib.ptr(qkv), _lib.ptr(self.cos), _lib.ptr(self.sin),
                       _lib.ptr(self.pos), _lib.ptr(self.k_cache[li, 0]), _lib.ptr(self.v_cache[li, 0]),
                       _lib.ptr(self.att), self.nh, self.nkv, self.hd, self.max_ctx, _lib.ptr(self.attn_ws), st)
-            o = fused_matvec(o_w, self.att, check_finite=False)
-            _lib.call("itq3_glue_residual_rmsnorm", _lib.ptr(xs), _lib.ptr(o), _lib.ptr(self.gain[li][1]),
-                      _lib.ptr(h), self.h, self.eps, st)
-            prev = self.pairs[li](h, st)  # gate_up + SiLU gating + down: one chain launch
-        _lib.call("itq3_glue_residual_rmsnorm", _lib.ptr(xs), _lib.ptr(prev), None, _lib.ptr(self.out), self.h,
-                  self.eps, st)
+            c_o(self.att, st)   # xs += W_o att
+            c_mlp(xs, st)       # xs += W_down (SiLU(gate) * up)(RMSNorm(xs))
+        self.out.copy_(xs)
         self.pos.add_(1)
 
     def capture(self) -> None:
