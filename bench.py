@@ -264,7 +264,7 @@ def run_decoder(args):
     tiled = sum(int(t.numel()) for row in st.q for q in row for t in q._tiled.values())
     if rank == 0:
         print(json.dumps({
-            "metric": "decode tokens/sec (batch-1 ITQ3_S decoder: fused IFWHT-dequant GEMVs + fused RMSNorm/RoPE-attention/SiLU glue kernels)",
+            "metric": "decode tokens/sec (batch-1 ITQ3_S decoder: fused IFWHT-dequant GEMV chains with RMSNorm, gating and residuals folded in, + a RoPE/attention kernel)",
             "value": world * 1000.0 / ms, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8xs8->s32 mma + fp32",
