@@ -20,7 +20,6 @@ import math
 import torch
 
 from .codec import QuantizedTensor, quantize_tensor
-from .compute import fused_matvec
 
 LLAMA3_8B = dict(hidden=4096, inter=14336, n_heads=32, n_kv=8, head_dim=128, rope_theta=500000.0)
 

@@ -1,4 +1,4 @@
-import os, sys, json, math, torch
+import os, sys, json, torch
 sys.path.insert(0, os.getcwd())
 import bench
 from paper_2603_27914_b200.stack import LinearStack
