@@ -1,4 +1,15 @@
-import os, sys, json, torch
+"""Chain-kernel decomposition: ms per token of the Llama-2-7B linear stack as a dependent chain and with
+the dependency removed (streaming), for whichever libitq3.so is loaded (ITQ3_LIB=... points at a
+knock-out build, e.g. -DCHAIN_EXP_NOROT / -DCHAIN_EXP_NOTILE).  Run from the repo root:
+
+    python tools/chain_decomp.py
+"""
+import json
+import os
+import sys
+
+import torch
+
 sys.path.insert(0, os.getcwd())
 import bench
 from paper_2603_27914_b200.stack import LinearStack
