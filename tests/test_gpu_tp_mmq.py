@@ -56,3 +56,30 @@ def test_tp_mmq_peer_stores(world, m):
         torch.testing.assert_close(bufs[r][: rows * m].view(rows, m), y0, rtol=0, atol=0)
     exact, bound = mmq_bound(q.payload().cpu().numpy(), rows, cols, X.cpu().numpy())
     assert np.all(np.abs(y0.cpu().numpy() - exact) <= bound)  # also: no NaN left from the fill
+
+
+@pytest.mark.parametrize("m", [40, 300])
+def test_tp_mmq_peer_stores_bf16(m):
+    """bf16 outputs through the peer-store epilogue (two simulated ranks, each computing half the rows
+    and writing both buffers): every copy equals the plain K5 call's bf16 output of the same rows."""
+    rows, cols, world = 768, 1024, 2
+    rng = np.random.default_rng(m)
+    q = P.quantize_tensor(rng.standard_normal((rows, cols)) * 0.05)
+    X = torch.from_numpy(rng.standard_normal((cols, m)).astype(np.float32)).cuda()
+    lib = _lib.load()
+    act = torch.empty(lib.itq3_mmq_act_nbytes(cols, m), dtype=torch.uint8, device="cuda")
+    _lib.call("itq3_rotate_act_f16", _lib.ptr(X), _lib.F32, cols, m, X.stride(0), X.stride(1), _lib.ptr(act), None,
+              _lib.stream_ptr(X.device))
+    bufs = [torch.full((rows, m), float("nan"), dtype=torch.bfloat16, device="cuda") for _ in range(world)]
+    peers = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    for r in range(world):
+        shard = shard_quantized(q, world, r)
+        r0 = r * (rows // world)
+        _lib.call("itq3_mmq_peers", _lib.ptr(shard.mmq_layout()), shard.rows, cols, 0, _lib.ptr(act), m,
+                  _lib.ptr(peers), world, r0, _lib.BF16, m, 1, None, _lib.stream_ptr(X.device))
+    ref = torch.empty((rows, m), dtype=torch.bfloat16, device="cuda")
+    _lib.call("itq3_mmq", _lib.ptr(q.mmq_layout()), rows, cols, 0, _lib.ptr(act), m, _lib.ptr(ref), _lib.BF16, m, 1,
+              None, _lib.stream_ptr(X.device))
+    torch.cuda.synchronize()
+    for b in bufs:
+        torch.testing.assert_close(b, ref, rtol=0, atol=0)
