@@ -39,6 +39,23 @@ def _nonfinite_flag(dev: torch.device) -> torch.Tensor:
     return f
 
 
+_SCRATCH: dict = {}
+
+
+def _scratch(dev: torch.device, stream: int, slot: str, nbytes: int) -> torch.Tensor | None:
+    """Reusable device scratch (rotated activations, split-K workspace) per (device, stream, slot):
+    calls on one stream are ordered, so a buffer can be reused by the next call without a fresh
+    allocation; it only grows."""
+    if nbytes <= 0:
+        return None
+    key = (dev, stream, slot)
+    buf = _SCRATCH.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+        _SCRATCH[key] = buf
+    return buf
+
+
 def _raise_if_nonfinite(flag: torch.Tensor) -> None:
     if int(flag.item()):
         flag.zero_()
@@ -103,13 +120,12 @@ def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, 
             and X.dtype != torch.float64:
         lib = _lib.load()
         s = _lib.stream_ptr(dev)
-        act = torch.empty(lib.itq3_mmq8_act_nbytes(cols, k), dtype=torch.uint8, device=dev)
+        act = _scratch(dev, s, "act8", lib.itq3_mmq8_act_nbytes(cols, k))
         flag = _nonfinite_flag(dev) if check_finite else None
         _lib.call("itq3_rotate_act_i8", _lib.ptr(X), _lib.TORCH_DTYPE_CODE[X.dtype], cols, k, X.stride(0),
                   X.stride(1), _lib.ptr(act), _lib.ptr(flag) if flag is not None else None, s)
         Y = torch.empty((rows, k), dtype=out_dtype, device=dev)
-        wsn = lib.itq3_mmq8_ws_nbytes(rows, cols, k)
-        ws = torch.empty(wsn, dtype=torch.uint8, device=dev) if wsn else None
+        ws = _scratch(dev, s, "ws8", lib.itq3_mmq8_ws_nbytes(rows, cols, k))
         _lib.call("itq3_mmq8", _lib.ptr(q.mmq8_layout()), rows, cols, _lib.ptr(act), k, _lib.ptr(Y),
                   _lib.TORCH_DTYPE_CODE[out_dtype], Y.stride(0), Y.stride(1), _lib.ptr(ws) if ws is not None else None,
                   s)
@@ -120,13 +136,12 @@ def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, 
         # K5: block_n 256 variant s for k > MMQ8_MAX_TOKENS; variant ss and block_n != 256 for every k >= MMQ_MIN_TOKENS
         mmq = q.mmq_layout()
         s = _lib.stream_ptr(dev)
-        act = torch.empty(_lib.load().itq3_mmq_act_nbytes(cols, k), dtype=torch.uint8, device=dev)
+        act = _scratch(dev, s, "act", _lib.load().itq3_mmq_act_nbytes(cols, k))
         flag = _nonfinite_flag(dev) if check_finite else None
         _lib.call("itq3_rotate_act_f16_n", _lib.ptr(X), _lib.TORCH_DTYPE_CODE[X.dtype], cols, k, X.stride(0),
                   X.stride(1), q.block_n, _lib.ptr(act), _lib.ptr(flag) if flag is not None else None, s)
         Y = torch.empty((rows, k), dtype=out_dtype, device=dev)
-        wsn = _lib.load().itq3_mmq_ws_nbytes(rows, cols, k)
-        ws = torch.empty(wsn, dtype=torch.uint8, device=dev) if wsn else None
+        ws = _scratch(dev, s, "ws", _lib.load().itq3_mmq_ws_nbytes(rows, cols, k))
         _lib.call("itq3_mmq", _lib.ptr(mmq), rows, cols, q.mmq_flags(), _lib.ptr(act), k, _lib.ptr(Y),
                   _lib.TORCH_DTYPE_CODE[out_dtype], Y.stride(0), Y.stride(1), _lib.ptr(ws) if ws is not None else None,
                   s)
