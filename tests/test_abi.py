@@ -76,3 +76,22 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(P.ItqError, match="no CPU fallback"):
         P.quantize_tensor(np.ones((2, 256)))
+
+
+def test_host_side_layout_functions():
+    """Host-only entry points (no GPU): record sizes by format flag, chain descriptor flag checks."""
+    import ctypes
+
+    from paper_2603_27914_b200 import _lib
+
+    lib = _lib.load()
+    plain = lib.itq3_mmq_nbytes(1000, 4096, 0)
+    per32 = lib.itq3_mmq_nbytes(1000, 4096, 2)
+    assert plain == (1024 // 128) * (4096 // 128) * (4096 + 256 + 128)
+    assert per32 == (1024 // 128) * (4096 // 128) * (4096 + 1024 + 512)
+    assert lib.itq3_glue_attention_ws_nbytes(32) == 32 * (4 * 130 * 4 + 4)
+    host = ctypes.create_string_buffer(lib.itq3_chain_desc_nbytes() * 2)
+    # RMSNorm-input stages need the whole input in one CTA chunk (cols <= 4096)
+    assert lib.itq3_chain_write_desc(host, 0, None, None, None, 1024, 4096, 4, 0) == 0
+    assert lib.itq3_chain_write_desc(host, 0, None, None, None, 1024, 8192, 4, 0) != 0
+    assert lib.itq3_chain_write_desc(host, 1, None, None, None, 4096, 14336, 2 | 8, 0) == 0
