@@ -61,7 +61,11 @@ def test_api_surface_mirrors_reference_names():
                  "pack_ternary", "unpack_ternary", "serialize_block", "deserialize_block", "write_container",
                  "read_container", "encode_f16", "decode_f16", "fwht_forward", "fwht_inverse", "ItqError",
                  "LengthError", "DomainError", "ShapeError", "CorruptionError", "ContainerError", "BadMagicError",
-                 "UnsupportedVersionError", "TruncatedStreamError", "SizeMismatchError"]:
+                 "UnsupportedVersionError", "TruncatedStreamError", "SizeMismatchError", "BlockStats", "block_stats",
+                 "optimal_scale", "ternary_quantize", "ternary_dequantize", "ternary_mse", "uniform_quantize",
+                 "hadamard_matrix", "hadamard_oracle", "StageTrace", "fwht_staged", "fwht32_warp", "CheckResult",
+                 "run_selfcheck", "AblationRow", "ErrorReport", "eval_error", "eval_container", "rotation_benefit",
+                 "ablate_block_size", "generate_weights", "report_json", "report_csv", "argmin_scale_coeff"]:
         assert hasattr(P, name), name
     assert P.CorruptionError.ident == "corrupt-data" and issubclass(P.CorruptionError, ValueError)
     assert issubclass(P.BadMagicError, P.ContainerError) and P.SizeMismatchError.ident == "size-mismatch"
