@@ -50,6 +50,8 @@ def _scratch(dev: torch.device, stream: int, slot: str, nbytes: int) -> torch.Te
         return None
     key = (dev, stream, slot)
     buf = _SCRATCH.get(key)
+    if buf is None and len(_SCRATCH) >= 64:  # many short-lived streams: drop the cache (stream-ordered frees)
+        _SCRATCH.clear()
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
         _SCRATCH[key] = buf
