@@ -37,12 +37,28 @@ MODELS = {
     "llama3-8b": (32, [("qkv", 6144, 4096), ("o", 4096, 4096), ("gate_up", 28672, 4096), ("down", 4096, 14336)]),
     "llama3-70b": (80, [("qkv", 10240, 8192), ("o", 8192, 8192), ("gate_up", 57344, 8192), ("down", 8192, 28672)]),
 }
-MODEL = os.environ.get("ITQ3_BENCH_MODEL", "llama2-7b")
-for _i, _a in enumerate(sys.argv):  # resolved before argparse so module constants follow --model
-    if _a == "--model" and _i + 1 < len(sys.argv):
-        MODEL = sys.argv[_i + 1]
-    elif _a.startswith("--model="):
-        MODEL = _a.split("=", 1)[1]
+
+
+def _argv_value(flag: str):
+    for i, a in enumerate(sys.argv):
+        if a == flag and i + 1 < len(sys.argv):
+            return sys.argv[i + 1]
+        if a.startswith(flag + "="):
+            return a.split("=", 1)[1]
+    return None
+
+
+def _default_model() -> str:
+    """--model, else ITQ3_BENCH_MODEL, else: N = 1 -> llama2-7b (configs[1], the headline); N > 1 ->
+    llama3-70b row-sharded over the ranks (configs[4], C5) unless --replicas is given."""
+    m = _argv_value("--model") or os.environ.get("ITQ3_BENCH_MODEL")
+    if m:
+        return m
+    n = int(_argv_value("--gpus") or os.environ.get("WORLD_SIZE", "1"))
+    return "llama3-70b" if n > 1 and "--replicas" not in sys.argv else "llama2-7b"
+
+
+MODEL = _default_model()  # resolved before argparse so module constants follow --model / --gpus
 N_LAYERS, LAYER_SHAPES = MODELS[MODEL]
 WEIGHTS_PER_TOKEN = N_LAYERS * sum(r * c for _, r, c in LAYER_SHAPES)  # llama2-7b: 6,476,005,376
 METRIC = "decode tokens/sec (batch-1 fused IFWHT-dequant GEMV chain, %s linear shapes)" % MODEL
@@ -246,14 +262,14 @@ def run_decoder(args):
     g.manual_seed(rank)
     st.x.copy_(torch.randn(st.h, generator=g, device=dev))
     for _ in range(args.warmup):
-        st.graph.replay()
+        st.replay()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        st.graph.replay()
+        st.replay()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
@@ -320,19 +336,51 @@ def run_tp(args):
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
         st.replay()
     e1.record()
     torch.cuda.synchronize()
+    clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+        return float(t.item())
+
+    ms = max_over_ranks(ms)
+    e2e = None
+    if hasattr(st, "forward"):  # public API, host buffers: H2D x + graphed step + D2H of the gathered y
+        import numpy as np
+
+        x0 = np.random.default_rng(7).standard_normal(cols[0]).astype(np.float32)
+        for _ in range(args.warmup):
+            st.forward(x0)
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            st.forward(x0)
+        e2e_ms = max_over_ranks(1000.0 * (time.perf_counter() - t0) / args.steps)
+        e2e = {"value": 1000.0 / e2e_ms, "unit": "tokens/s", "h2d_bytes_per_step": 4 * cols[0],
+               "d2h_bytes_per_step": 4 * rows[-1], "api": "TPChainStack.forward(host np.float32) on every rank"}
+    local_bytes = sum(int(t.numel()) for t in st.tiled)
+    tot_bytes = local_bytes
+    if world > 1:
+        t = torch.tensor([float(local_bytes)], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t)
+        tot_bytes = int(t.item())
+    peak, peak_src = measured_peak()
+    nvl = st.nvlink_bytes_per_step() * world if hasattr(st, "nvlink_bytes_per_step") else None
     if rank == 0:
-        tiled_bytes = sum(int(t.numel()) for t in st.tiled) * world
+        per_gpu = tot_bytes / world / (ms / 1000.0) / 1e9
         print(json.dumps({
             "metric": METRIC.replace("GEMV chain", "GEMV chain, tensor-parallel"), "value": 1000.0 / ms,
             "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -341,11 +389,156 @@ def run_tp(args):
             "config": {"workload": WORKLOAD, "model": f"{MODEL} (linear layers)", "global_batch": 1, "seq_len": 1,
                        "parallelism": f"tp{world} (row-sharded stages; " + (
                            "all-gather fused into the chain kernel's peer stores)" if args.tp_impl == "fused"
-                           else "NCCL all-gather per stage)")},
-            "packed_weight_gbps": tiled_bytes / (ms / 1000.0) / 1e9,
-            "gpu_launches": (1 if args.tp_impl == "fused" else 2 * len(qs)) * args.steps}), flush=True)
+                           else "NCCL all-gather per stage)"),
+                       "l2": f"{tot_bytes / world / 1e9:.2f} GB of tiled weights per GPU per step > 126 MB L2"},
+            "packed_weight_gbps": tot_bytes / (ms / 1000.0) / 1e9,
+            "packed_weight_gbps_per_gpu": per_gpu,
+            "nvlink_bytes_per_token": nvl,
+            "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s", "frac": per_gpu / peak,
+                         "traffic": None, "kernel": "itq3::chain_kernel per rank (whole step, 1 launch)",
+                         "peak_source": peak_src},
+            "e2e": e2e,
+            "gpu_launches": (1 if args.tp_impl == "fused" else 2 * len(qs)) * args.steps,
+            "clocks": clk}), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------------------------
+# extra keys of the N = 1 line: C3 MMQ (configs[2]) and C4 decoder (configs[3]), device-timed
+# ------------------------------------------------------------------------------------------------
+def graph_time(fn, reps):
+    """Device time per call of fn(i): reps calls captured in one CUDA graph, CUDA events around a replay."""
+    import torch
+
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for i in range(3):
+            fn(i)
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(reps):
+            fn(i)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+INT8_NOMINAL_TOPS = 4500.0  # B200 dense int8 (datasheet; no measured int8 peak in MEASURED_PEAKS.json)
+
+
+def measure_c3(dev, reps: int = 20) -> dict:
+    """BASELINE configs[2] at the Llama-3-8B gate/up shape 14336 x 4096: K5 (tcgen05 kind::f16 CTA pairs)
+    at M = 2048 in TFLOPS, K5b (kind::i8) at M = 16 / 64 in packed GB/s.  Calls rotate over 11 distinct
+    weight copies (> 160 MB > L2), so every call streams its weights from HBM."""
+    import torch
+
+    import paper_2603_27914_b200 as P
+    from paper_2603_27914_b200 import _lib
+
+    rows, K = 14336, 4096
+    lib = _lib.load()
+    g = torch.Generator(device=dev)
+    g.manual_seed(33)
+    copies = []
+    for _ in range(11):
+        q = P.quantize_tensor(torch.randn((rows, K), generator=g, device=dev).mul_(K ** -0.5))
+        copies.append((q.mmq_layout(), q.mmq8_layout()))
+        del q
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except (OSError, ValueError):
+        pass
+    bf16 = float(peaks.get("bf16_tflops", 0) or 0) or None
+    hbm, _ = measured_peak()
+    out = {"shape": f"{rows}x{K}", "weight_copies": len(copies)}
+    for M in (16, 64, 2048):
+        small = P.compute.MMQ_MIN_TOKENS <= M <= P.compute.MMQ8_MAX_TOKENS
+        X = torch.randn((K, M), generator=g, device=dev)
+        act = torch.empty(lib.itq3_mmq8_act_nbytes(K, M) if small else lib.itq3_mmq_act_nbytes(K, M),
+                          dtype=torch.uint8, device=dev)
+        Y = torch.empty((rows, M), dtype=torch.float32, device=dev)
+        wsn = lib.itq3_mmq8_ws_nbytes(rows, K, M) if small else lib.itq3_mmq_ws_nbytes(rows, K, M)
+        ws = torch.empty(max(wsn, 1), dtype=torch.uint8, device=dev)
+
+        def rot(i):
+            s = _lib.stream_ptr(dev)
+            name = "itq3_rotate_act_i8" if small else "itq3_rotate_act_f16"
+            _lib.call(name, _lib.ptr(X), _lib.F32, K, M, X.stride(0), X.stride(1), _lib.ptr(act), None, s)
+
+        def mm(i):
+            s = _lib.stream_ptr(dev)
+            w = copies[i % len(copies)][1 if small else 0]
+            if small:
+                _lib.call("itq3_mmq8", _lib.ptr(w), rows, K, _lib.ptr(act), M, _lib.ptr(Y), _lib.F32, Y.stride(0),
+                          Y.stride(1), _lib.ptr(ws) if wsn else None, s)
+            else:
+                _lib.call("itq3_mmq", _lib.ptr(w), rows, K, 0, _lib.ptr(act), M, _lib.ptr(Y), _lib.F32, Y.stride(0),
+                          Y.stride(1), _lib.ptr(ws) if wsn else None, s)
+
+        def both(i):
+            rot(i)
+            mm(i)
+
+        ms = graph_time(both, reps)
+        ms_k = graph_time(mm, reps)
+        flops = 2.0 * rows * K * M
+        wbytes = int(copies[0][1 if small else 0].numel())
+        r = {"kernel": "K5b tcgen05 kind::i8" if small else "K5 tcgen05 kind::f16 cta_group::2",
+             "us": ms * 1e3, "kernel_us": ms_k * 1e3, "tflops": flops / ms / 1e9, "kernel_tflops": flops / ms_k / 1e9,
+             "weight_bytes": wbytes, "kernel_weight_gbps": wbytes / ms_k / 1e6,
+             "kernel_frac_hbm": wbytes / ms_k / 1e6 / hbm}
+        if bf16:
+            r["kernel_frac_bf16_measured"] = r["kernel_tflops"] / bf16
+        r["kernel_frac_int8_nominal"] = r["kernel_tflops"] / INT8_NOMINAL_TOPS
+        out[f"m{M}"] = r
+    del copies
+    torch.cuda.empty_cache()
+    return out
+
+
+def measure_c4(dev, steps: int, warmup: int) -> dict:
+    """BASELINE configs[3]: the Llama-3-8B-shaped decoder (32 layers, random-init weights quantized to
+    ITQ3_S on the GPU), one CUDA graph per token, positions 512+ of a 1024-position KV cache."""
+    import torch
+
+    from paper_2603_27914_b200.decoder import DecoderStack
+
+    st = DecoderStack(layers=32, max_ctx=1024, seed=3000, dev=dev)
+    st.capture()
+    st.reset(512)
+    st.x.copy_(torch.randn(st.h, device=dev))
+    for _ in range(warmup):
+        st.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        st.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    wbytes = st.weight_bytes()
+    hbm, _ = measured_peak()
+    r = {"tokens_per_s": 1000.0 / ms, "ms_per_token": ms, "packed_weight_bytes_per_token": wbytes,
+         "packed_weight_gbps": wbytes / ms / 1e6, "frac_hbm": wbytes / ms / 1e6 / hbm,
+         "launches_per_token": st.launches_per_step(), "lm_head": st.lm_head is not None,
+         "workload": "llama3-8b decoder decode, 32 layers (hidden 4096, ffn 14336, 32/8 heads, head_dim 128)"
+                     + (" + 128256x4096 ITQ3_S lm_head" if st.lm_head is not None else "")
+                     + ", positions 512+ of a 1024 KV cache, batch 1"}
+    del st
+    torch.cuda.empty_cache()
+    return r
 
 
 def run_ours(args):
@@ -448,6 +641,10 @@ def run_ours(args):
         if world > 1:
             torch.distributed.destroy_process_group()
         return
+    extra = {}
+    if world == 1 and not args.no_extra:
+        extra["c3_mmq"] = measure_c3(dev)
+        extra["c4_decoder"] = measure_c4(dev, args.steps, args.warmup)
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         arm = CpuArm(rows_per_stage=args.cpu_rows)
@@ -483,9 +680,51 @@ def run_ours(args):
         "gpu_launches": stack.launches_per_step * args.steps,
         "clocks": clk,
     }
+    line.update(extra)
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N > 1` without a torchrun environment: re-launch this script under torch.distributed.run
+    with one rank per GPU on 127.0.0.1 (rank 0 prints the JSON line); returns the launcher's exit code."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.run(cmd, env=env).returncode
+
+
+def run_dry(args):
+    """--dry-run (CPU, gloo): exercises the multi-rank plumbing of the GPU arms -- rank discovery,
+    barrier, max-over-ranks of the step time, one JSON line from rank 0 -- without a GPU."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    t0 = time.perf_counter()
+    for _ in range(args.warmup + args.steps):
+        sum(range(10000))
+    ms = 1000.0 * (time.perf_counter() - t0) / (args.warmup + args.steps) * (1 + rank)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": 1000.0 / ms, "unit": "tokens/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "dry_run": True,
+                          "config": {"workload": WORKLOAD, "model": MODEL,
+                                     "parallelism": f"tp{world}" if world > 1 and not args.replicas else
+                                     f"replicas{world}"}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():
@@ -499,20 +738,29 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compare", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C3 MMQ and C4 decoder keys of the N=1 line")
     ap.add_argument("--mode", choices=["chain", "kernels"], default="chain")
     ap.add_argument("--model", choices=sorted(MODELS), default=MODEL)
-    ap.add_argument("--tp", action="store_true", help="row-shard one token stream over the ranks (C5)")
+    ap.add_argument("--tp", action="store_true", help="row-shard one token stream over the ranks (C5); "
+                                                      "the default for --gpus > 1")
+    ap.add_argument("--replicas", action="store_true", help="--gpus > 1: N independent replicas of the N=1 step")
     ap.add_argument("--decoder", action="store_true", help="configs[3]: full Llama-3-8B-shaped decoder decode step")
     ap.add_argument("--tp-impl", choices=["fused", "nccl"], default="fused",
                     help="--tp: fused chain kernel with NVLink peer stores, or per-stage kernels + NCCL all_gather")
+    ap.add_argument("--dry-run", action="store_true", help="CPU/gloo check of the multi-rank plumbing (tests)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.layers is None:
         args.layers = N_LAYERS
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    world = dist_env()[1]
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
-    elif args.tp:
+    elif args.tp or (world > 1 and not args.replicas and not args.decoder):
         run_tp(args)
     elif args.decoder:
         run_decoder(args)

@@ -30,12 +30,16 @@ MMQ8_MAX_TOKENS = 64  # ... 8 <= k <= 64 to the kind::i8 one (K5b), larger k to 
 _NONFINITE: dict = {}
 
 
-def _nonfinite_flag(dev: torch.device) -> torch.Tensor:
-    """Per-device u32 flag the MMQ activation rotations OR with 1 on a non-finite input (kept zero)."""
-    f = _NONFINITE.get(dev)
+def _nonfinite_flag(dev: torch.device, stream: int) -> torch.Tensor:
+    """Per-(device, stream) u32 flag the MMQ activation rotations OR with 1 on a non-finite input
+    (kept zero): calls on different streams never see each other's error."""
+    key = (dev, stream)
+    f = _NONFINITE.get(key)
     if f is None:
+        if len(_NONFINITE) >= 64:
+            _NONFINITE.clear()
         f = torch.zeros(1, dtype=torch.int32, device=dev)
-        _NONFINITE[dev] = f
+        _NONFINITE[key] = f
     return f
 
 
@@ -45,9 +49,13 @@ _SCRATCH: dict = {}
 def _scratch(dev: torch.device, stream: int, slot: str, nbytes: int) -> torch.Tensor | None:
     """Reusable device scratch (rotated activations, split-K workspace) per (device, stream, slot):
     calls on one stream are ordered, so a buffer can be reused by the next call without a fresh
-    allocation; it only grows."""
+    allocation; it only grows.  Under CUDA-graph capture a fresh buffer from the graph's private
+    pool is used instead: a captured graph keeps raw pointers, so it must never share (or outlive)
+    a cached buffer that a later eager call could grow, free or race with on replay."""
     if nbytes <= 0:
         return None
+    if torch.cuda.is_current_stream_capturing():
+        return torch.empty(nbytes, dtype=torch.uint8, device=dev)
     key = (dev, stream, slot)
     buf = _SCRATCH.get(key)
     if buf is None and len(_SCRATCH) >= 64:  # many short-lived streams: drop the cache (stream-ordered frees)
@@ -112,7 +120,14 @@ def _matvec_chain(q: QuantizedTensor, x: torch.Tensor) -> torch.Tensor:
 
 def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, limbs: int,
                    check_finite: bool = True) -> torch.Tensor:
-    """Y (rows x k) = w_hat @ X for a CUDA X (cols x k, any strides)."""
+    """Y (rows x k) = w_hat @ X for a CUDA X (cols x k, any strides), computed on X's device (its
+    weight layouts are built there, the launches go to that device's current stream)."""
+    with torch.cuda.device(X.device):
+        return _matmul_on_device(q, X, out_dtype, limbs, check_finite)
+
+
+def _matmul_on_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, limbs: int,
+                      check_finite: bool) -> torch.Tensor:
     dev = X.device
     rows, cols = q.rows, q.cols
     k = X.shape[1]
@@ -123,7 +138,7 @@ def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, 
         lib = _lib.load()
         s = _lib.stream_ptr(dev)
         act = _scratch(dev, s, "act8", lib.itq3_mmq8_act_nbytes(cols, k))
-        flag = _nonfinite_flag(dev) if check_finite else None
+        flag = _nonfinite_flag(dev, s) if check_finite else None
         _lib.call("itq3_rotate_act_i8", _lib.ptr(X), _lib.TORCH_DTYPE_CODE[X.dtype], cols, k, X.stride(0),
                   X.stride(1), _lib.ptr(act), _lib.ptr(flag) if flag is not None else None, s)
         Y = torch.empty((rows, k), dtype=out_dtype, device=dev)
@@ -139,7 +154,7 @@ def _matmul_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtype, 
         mmq = q.mmq_layout()
         s = _lib.stream_ptr(dev)
         act = _scratch(dev, s, "act", _lib.load().itq3_mmq_act_nbytes(cols, k))
-        flag = _nonfinite_flag(dev) if check_finite else None
+        flag = _nonfinite_flag(dev, s) if check_finite else None
         _lib.call("itq3_rotate_act_f16_n", _lib.ptr(X), _lib.TORCH_DTYPE_CODE[X.dtype], cols, k, X.stride(0),
                   X.stride(1), q.block_n, _lib.ptr(act), _lib.ptr(flag) if flag is not None else None, s)
         Y = torch.empty((rows, k), dtype=out_dtype, device=dev)

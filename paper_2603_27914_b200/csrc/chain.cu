@@ -687,19 +687,10 @@ static int chain_run(const void* d_desc, int n_stages, const float* x0, int limb
         set_error("chain: limbs must be in [1, %d]", kMaxLimbs);
         return ITQ3_E_DOMAIN;
     }
-    static bool attr_set = false;
+    static std::atomic<unsigned long long> smem_attr{0};
     const int smem = (int)sizeof(ChainSmem);
-    if (!attr_set) {
-        if (cudaFuncSetAttribute(chain_kernel<GATED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-            return check_launch("chain: smem attribute");
-        attr_set = true;
-    }
-    if (grid <= 0) {
-        int dev = 0, sms = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        grid = sms;
-    }
+    if (int rc = ensure_smem_attr(chain_kernel<GATED>, smem, smem_attr, "chain: smem attribute")) return rc;
+    if (grid <= 0) grid = device_sms();
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kChainThreads);

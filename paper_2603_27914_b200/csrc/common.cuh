@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -21,6 +22,26 @@ constexpr int kSubBlocks = 8;  // packing.py:31
 // ---- error plumbing (host) ------------------------------------------------------------
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute belongs to
+// the device context, so a process driving several GPUs sets it on each (bit d of `done` = device d).
+template <typename K>
+inline int ensure_smem_attr(K* kernel, int smem, std::atomic<unsigned long long>& done, const char* what) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return ITQ3_OK;
+    if (cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return check_launch(what);
+    done.fetch_or(bit, std::memory_order_acq_rel);
+    return ITQ3_OK;
+}
+inline int device_sms() {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
 
 __host__ __device__ inline int block_nbytes(int n, int ss) { return 3 * n / 8 + 4 + (ss ? 16 : 0); }
 inline bool valid_block_n(int n) { return n == 32 || n == 64 || n == 128 || n == 256 || n == 512; }

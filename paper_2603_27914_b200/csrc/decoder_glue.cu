@@ -27,7 +27,13 @@ __global__ void __launch_bounds__(1024) glue_rope_attention(const float* __restr
     __shared__ float part[8][HD];
     __shared__ bool last;
     const int h = blockIdx.x, sp = blockIdx.y, t = threadIdx.x, w = t >> 5, l = t & 31, kvh = h / (nh / nkv);
-    const int pos = (int)*pos_p;
+    const int64_t pos64 = *pos_p;
+    if (pos64 < 0 || pos64 >= ctx) {  // beyond the KV cache: no cache write, zero output, error word set
+        if (t < HD && sp == 0) out[(int64_t)h * HD + t] = 0.f;
+        if (t == 0 && h == 0 && sp == 0) atomicOr(counters + nh, 1u);
+        return;
+    }
+    const int pos = (int)pos64;
     const int chunk = (pos + kAttnSplits) / kAttnSplits;  // ceil((pos + 1) / splits)
     const int lo = sp * chunk, hi = min(pos + 1, lo + chunk);
     float* kch = kc + (int64_t)kvh * ctx * HD;
@@ -138,7 +144,7 @@ __global__ void __launch_bounds__(1024) glue_rope_attention(const float* __restr
 using namespace itq3;
 
 extern "C" int64_t itq3_glue_attention_ws_nbytes(int n_heads) {
-    return (int64_t)n_heads * (kAttnSplits * (128 + 2) * 4 + 4);
+    return (int64_t)n_heads * (kAttnSplits * (128 + 2) * 4 + 4) + 4;  // + the out-of-cache error word
 }
 
 extern "C" int itq3_glue_rope_attention(const float* qkv, const float* cos_tab, const float* sin_tab,
@@ -148,7 +154,8 @@ extern "C" int itq3_glue_rope_attention(const float* qkv, const float* cos_tab, 
         set_error("itq3_glue_rope_attention: head_dim 128, ctx <= 1024, n_heads a multiple of n_kv");
         return ITQ3_E_UNSUPPORTED;
     }
-    // ws: [n_heads][splits][2 + 128] fp32 partials, then n_heads u32 counters (zero before first use)
+    // ws: [n_heads][splits][2 + 128] fp32 partials, then n_heads u32 counters (zero before first use),
+    // then one u32 error word (bit 0: a launch saw a position outside [0, ctx))
     float* part = (float*)ws;
     unsigned* cnt = (unsigned*)(part + (int64_t)n_heads * kAttnSplits * (128 + 2));
     glue_rope_attention<<<dim3(n_heads, kAttnSplits), 1024, 0, (cudaStream_t)stream>>>(

@@ -339,15 +339,9 @@ template <typename TOut>
 int itq3_dequant_tc(const uint8_t* payload, int64_t n_blocks, int64_t numel, TOut* out, cudaStream_t s) {
     using namespace itq3dq;
     const int smem = (int)sizeof(Smem) + 1024;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(dequant_tc_kernel<TOut>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-            cudaSuccess)
-            return itq3::check_launch("itq3_dequant: smem attribute");
-        attr = true;
-    }
-    static int sms = 0;
-    if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    static std::atomic<unsigned long long> attr{0};
+    if (int rc = itq3::ensure_smem_attr(dequant_tc_kernel<TOut>, smem, attr, "itq3_dequant: smem attribute")) return rc;
+    const int sms = itq3::device_sms();
     const int64_t ntiles = (n_blocks + 127) / 128;
     const unsigned grid = (unsigned)(ntiles < sms ? ntiles : sms);
     dequant_tc_kernel<TOut><<<grid, kThreads, smem, s>>>(payload, n_blocks, numel, out);

@@ -580,11 +580,8 @@ extern "C" int itq3_eval(const void* w, int w_dtype, int64_t numel, int block_n,
     rc = check_launch("itq3_eval(pairwise)");
     if (rc) return rc;
     const size_t smem = (size_t)(1 << kPwMaxDepth) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(eval_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    static std::atomic<unsigned long long> attr{0};
+    if (int rc2 = ensure_smem_attr(eval_finish_kernel, (int)smem, attr, "itq3_eval: smem attribute")) return rc2;
     eval_finish_kernel<<<1, kFinThreads, smem, s>>>(jobs, numel, nb, block_n, o.slack, o.clamp_cnt, o.zero_cnt,
                                                     o.nonfinite, d_report);
     return check_launch("itq3_eval(finish)");

@@ -989,20 +989,10 @@ static int launch_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym, 
                       int64_t sr, int64_t sm_, float* ws, cudaStream_t s,
                       const unsigned long long* ypeer = nullptr, int npeer = 0, int64_t row0 = 0) {
     const int smem = (int)sizeof(PairSmem) + 1024;
-    static bool attr = false, attr32 = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(mmq_pair_kernel<BN, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
-            cudaFuncSetAttribute(mmq_pair_kernel<BN, TY, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-                cudaSuccess)
-            return check_launch("itq3_mmq: smem attribute");
-        attr = true;
-    }
-    if (!attr32) {
-        if (cudaFuncSetAttribute(mmq_pair_kernel<BN, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-            cudaSuccess)
-            return check_launch("itq3_mmq: smem attribute");
-        attr32 = true;
-    }
+    static std::atomic<unsigned long long> attr{0}, attr_peer{0}, attr32{0};
+    if (int rc = ensure_smem_attr(mmq_pair_kernel<BN, TY>, smem, attr, "itq3_mmq: smem attribute")) return rc;
+    if (int rc = ensure_smem_attr(mmq_pair_kernel<BN, TY, true>, smem, attr_peer, "itq3_mmq: smem attribute")) return rc;
+    if (int rc = ensure_smem_attr(mmq_pair_kernel<BN, float>, smem, attr32, "itq3_mmq: smem attribute")) return rc;
     PairWork wk;
     wk.tiles_r = mmq_rows_pad(rows) / 256;
     wk.tiles_n = (int)((m + BN - 1) / BN);
@@ -1553,12 +1543,8 @@ template <int BN, typename TY>
 static int launch_mmq8(const uint8_t* w, int64_t rows, int64_t cols, const uint8_t* act, int64_t m, TY* y,
                        int64_t sr, int64_t sm_, float* ws, cudaStream_t s) {
     const int smem = (int)sizeof(Q8Smem<BN>) + 1024;
-    static bool attr = false, attr32 = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(mmq8_kernel<BN, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-            return check_launch("itq3_mmq8: smem attribute");
-        attr = true;
-    }
+    static std::atomic<unsigned long long> attr{0}, attr32{0};
+    if (int rc = ensure_smem_attr(mmq8_kernel<BN, TY>, smem, attr, "itq3_mmq8: smem attribute")) return rc;
     const int NB = (int)(cols / 256);
     const int ks = ws ? mmq8_splits(rows, cols, m) : 1;
     const dim3 grid((unsigned)((rows + 127) / 128), (unsigned)((m + BN - 1) / BN), (unsigned)ks);
@@ -1566,12 +1552,7 @@ static int launch_mmq8(const uint8_t* w, int64_t rows, int64_t cols, const uint8
         launch_pdl(mmq8_kernel<BN, TY>, grid, dim3(kQ8Threads), smem, s, w, NB, act, rows, m, y, sr, sm_, (int64_t)0);
         return check_launch("itq3_mmq8");
     }
-    if (!attr32) {
-        if (cudaFuncSetAttribute(mmq8_kernel<BN, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-            cudaSuccess)
-            return check_launch("itq3_mmq8: smem attribute");
-        attr32 = true;
-    }
+    if (int rc = ensure_smem_attr(mmq8_kernel<BN, float>, smem, attr32, "itq3_mmq8: smem attribute")) return rc;
     launch_pdl(mmq8_kernel<BN, float>, grid, dim3(kQ8Threads), smem, s, w, NB, act, rows, m, ws, m, (int64_t)1,
                rows * m);
     int rc = check_launch("itq3_mmq8 (split-K)");

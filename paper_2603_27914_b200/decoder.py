@@ -21,7 +21,7 @@ import torch
 
 from .codec import QuantizedTensor, quantize_tensor
 
-LLAMA3_8B = dict(hidden=4096, inter=14336, n_heads=32, n_kv=8, head_dim=128, rope_theta=500000.0)
+LLAMA3_8B = dict(hidden=4096, inter=14336, n_heads=32, n_kv=8, head_dim=128, rope_theta=500000.0, vocab=128256)
 
 
 class _Chain:
@@ -66,7 +66,7 @@ class DecoderStack:
     on the GPU by K1), RMSNorm gains near 1, a KV cache of `max_ctx` positions (fp32)."""
 
     def __init__(self, layers: int = 32, max_ctx: int = 1024, seed: int = 0, dev=None, shapes: dict | None = None,
-                 eps: float = 1e-5, serving: bool = True):
+                 eps: float = 1e-5, serving: bool = True, lm_head: bool = True):
         cfg = dict(LLAMA3_8B, **(shapes or {}))
         self.dev = dev or torch.device("cuda", torch.cuda.current_device())
         self.layers, self.max_ctx, self.eps = layers, max_ctx, eps
@@ -89,12 +89,25 @@ class DecoderStack:
                 del w
             self.q.append(row)
         self.gain = [(1.0 + 0.1 * torch.randn((2, self.h), generator=g, device=self.dev)) for _ in range(layers)]
+        # final RMSNorm + ITQ3_S lm_head (vocab x hidden): logits of the token, one more chain launch
+        self.vocab = cfg["vocab"]
+        self.lm_head = None
+        if lm_head:
+            w = torch.randn((self.vocab, self.h), generator=g, device=self.dev).mul_(0.02)
+            self.lm_head = quantize_tensor(w)
+            self.lm_head.tiled()
+            if serving:
+                self.lm_head.drop_payload()
+            del w
+            self.final_gain = 1.0 + 0.1 * torch.randn(self.h, generator=g, device=self.dev)
+            self.logits = torch.zeros(self.vocab, device=self.dev)
         inv = 1.0 / (cfg["rope_theta"] ** (torch.arange(0, self.hd, 2, device=self.dev, dtype=torch.float64) / self.hd))
         ang = torch.arange(max_ctx, device=self.dev, dtype=torch.float64)[:, None] * inv[None, :]
         self.cos, self.sin = ang.cos().float(), ang.sin().float()
         self.k_cache = torch.zeros((layers, 1, self.nkv, max_ctx, self.hd), device=self.dev)
         self.v_cache = torch.zeros_like(self.k_cache)
         self.pos = torch.zeros(1, dtype=torch.long, device=self.dev)
+        self.host_pos = 0
         self.x = torch.zeros(self.h, device=self.dev)
         self.out = torch.zeros(self.h, device=self.dev)
         self.kpos = torch.arange(max_ctx, device=self.dev)
@@ -114,7 +127,19 @@ class DecoderStack:
             self.chains.append((_Chain([(qkv_w, NORM_IN, g1)], self.qkv_out, self.dev),
                                 _Chain([(o_w, ADD_OUT, None)], self.xs, self.dev),
                                 _Chain([(gu_w, NORM_IN, g2), (down_w, GATED | ADD_OUT, None)], self.xs, self.dev)))
+        self.head_chain = (_Chain([(self.lm_head, NORM_IN, self.final_gain)], self.logits, self.dev)
+                           if self.lm_head is not None else None)
         self.graph = None
+
+    def weight_bytes(self) -> int:
+        """Packed (tiled) ITQ3_S weight bytes one token streams: every layer's linears + the lm_head."""
+        n = sum(int(t.numel()) for row in self.q for q in row for t in q._tiled.values())
+        if self.lm_head is not None:
+            n += sum(int(t.numel()) for t in self.lm_head._tiled.values())
+        return n
+
+    def launches_per_step(self) -> int:
+        return 4 * self.layers + (1 if self.lm_head is not None else 0)
 
     def _rms(self, x, gain):
         return torch.nn.functional.rms_norm(x, (self.h,), weight=gain, eps=self.eps)
@@ -139,6 +164,8 @@ class DecoderStack:
                       _lib.ptr(self.att), self.nh, self.nkv, self.hd, self.max_ctx, _lib.ptr(self.attn_ws), st)
             c_o(self.att, st)   # xs += W_o att
             c_mlp(xs, st)       # xs += W_down (SiLU(gate) * up)(RMSNorm(xs))
+        if self.head_chain is not None:
+            self.head_chain(xs, st)  # logits = W_head RMSNorm(xs)
         self.out.copy_(xs)
         self.pos.add_(1)
 
@@ -156,18 +183,34 @@ class DecoderStack:
         self.graph = g
 
     def reset(self, pos: int = 0) -> None:
+        if not 0 <= pos < self.max_ctx:
+            raise ValueError(f"DecoderStack: position {pos} outside the KV cache (max_ctx {self.max_ctx})")
         self.pos.fill_(pos)
+        self.host_pos = pos
         self.k_cache.zero_()
         self.v_cache.zero_()
 
+    def replay(self) -> None:
+        """One graphed token step (bench loop); the host-side position guards the KV cache bound."""
+        if self.host_pos >= self.max_ctx:
+            raise ValueError(f"DecoderStack: KV cache full ({self.max_ctx} positions); reset() first")
+        self.graph.replay()
+        self.host_pos += 1
+
     def step(self, x: torch.Tensor | None = None) -> torch.Tensor:
-        """Decode one token: hidden state in (device, len hidden), hidden state out; advances the position."""
+        """Decode one token: hidden state in (device, len hidden), hidden state out; advances the position.
+        Raises once the KV cache is full (the glue kernel also refuses positions >= max_ctx on the
+        device and writes no cache entry: its error word, attn_ws's last u32, is set)."""
         if x is not None:
             self.x.copy_(x)
         if self.graph is None:
             self.capture()
-        self.graph.replay()
+        self.replay()
         return self.out
+
+    def device_error(self) -> int:
+        """The glue kernel's out-of-cache flag (non-zero after a replay at a position >= max_ctx)."""
+        return int(self.attn_ws.view(torch.int32)[-1].item())
 
     def reference_step(self, x: torch.Tensor, pos: int, k_hist: list, v_hist: list) -> torch.Tensor:  # noqa: C901
         """The same token step in plain torch fp32 with dequantised weights (numerics test only)."""
@@ -196,4 +239,8 @@ class DecoderStack:
             h = h + W[1] @ att.reshape(self.h)
             gu = W[2] @ self._rms(h, g2)
             h = h + W[3] @ (torch.nn.functional.silu(gu[: self.inter]) * gu[self.inter:])
+        if self.lm_head is not None:
+            if not hasattr(self, "_ref_head"):
+                self._ref_head = torch.as_tensor(dequantize_tensor(self.lm_head), device=self.dev).float()
+            self.ref_logits = self._ref_head @ self._rms(h, self.final_gain)
         return h

@@ -279,6 +279,30 @@ class TPChainStack:
         """The full last-stage output (all ranks' rows), identical on every rank."""
         return self.out
 
+    def forward(self, x) -> "np.ndarray":
+        """Host in -> host out on this rank: H2D of x (pinned), the graphed chain step, D2H of the
+        gathered last-stage output.  Every rank must call it for the same step (the chain's peer
+        stores pair the ranks' launches)."""
+        import numpy as np
+
+        if getattr(self, "host_in", None) is None:
+            self.host_in = torch.empty(self.x.numel(), dtype=torch.float32).pin_memory()
+            self.host_out = torch.empty(self.out.numel(), dtype=torch.float32).pin_memory()
+        self.host_in.copy_(torch.as_tensor(np.asarray(x, dtype=np.float32)).reshape(-1))
+        self.x.copy_(self.host_in, non_blocking=True)
+        self.replay()
+        self.host_out.copy_(self.out, non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        return self.host_out.numpy()
+
+    def nvlink_bytes_per_step(self) -> int:
+        """Bytes this rank stores into its peers' copies per step: every tagged output word (8 B per
+        row and K-chunk partial) of its row shards, once per remote rank."""
+        tot = 0
+        for q in self.qs:
+            tot += q.rows * -(-q.cols // 4096) * 8 * (self.world - 1)
+        return tot
+
 
 class TPMatmul:
     """Row-sharded batched product (fused_matmul, k >= 16) with the all-gather fused into the K5 MMQ
@@ -287,7 +311,14 @@ class TPMatmul:
     unfused equivalent is ShardedLinear (local fused_matmul + NCCL all_gather_into_tensor).
 
     `local_q`: this rank's rows shard_bounds(rows, world, rank); Y is rows x max_tokens (fp32) on every
-    rank.  `peer_bases` / `ybuf` (testing): explicit per-rank output buffers instead of a rendezvous.
+    rank.  `peer_bases` / `ybuf` (testing): explicit per-rank output buffers (2 * rows * max_tokens
+    floats each) instead of a rendezvous.
+
+    Y is double-buffered by call parity: call t writes half t % 2 of every rank's buffer, so a fast
+    rank's call t + 1 never overwrites the words a slower rank is still reading from call t (it
+    cannot start call t + 2 before every rank has passed call t + 1's barrier, which is stream-ordered
+    behind that rank's reads of call t's Y).  The returned Y is a view of that half: valid until the
+    second-next call on this object (clone it to keep it longer).
     """
 
     def __init__(self, local_q: QuantizedTensor, rows: int, max_tokens: int, group=None, world: int | None = None,
@@ -313,18 +344,23 @@ class TPMatmul:
             if world > 1:
                 from torch.distributed import _symmetric_memory as symm
 
-                ybuf = symm.empty(rows * max_tokens, dtype=torch.float32, device=self.dev)
+                ybuf = symm.empty(2 * rows * max_tokens, dtype=torch.float32, device=self.dev)
                 self.hdl = symm.rendezvous(ybuf, group if group is not None else dist.group.WORLD)
                 delta = ybuf.data_ptr() - self.hdl.buffer_ptrs[rank]
                 peer_bases = [b + delta for b in self.hdl.buffer_ptrs]
             else:
-                ybuf = torch.empty(rows * max_tokens, dtype=torch.float32, device=self.dev)
+                ybuf = torch.empty(2 * rows * max_tokens, dtype=torch.float32, device=self.dev)
         if peer_bases is None:
             peer_bases = [ybuf.data_ptr()]
         if len(peer_bases) != world or peer_bases[rank] != ybuf.data_ptr():
             raise ShapeError("TPMatmul: peer_bases must list every rank's buffer, this rank's at index rank")
+        if ybuf.numel() < 2 * rows * max_tokens:
+            raise ShapeError("TPMatmul: ybuf must hold 2 * rows * max_tokens floats (double-buffered Y)")
         self.ybuf = ybuf
-        self.peers = torch.tensor(peer_bases, dtype=torch.int64, device=self.dev)
+        half = 4 * rows * max_tokens  # bytes per parity half
+        self.peers = torch.tensor([[b + p * half for b in peer_bases] for p in (0, 1)], dtype=torch.int64,
+                                  device=self.dev)
+        self.calls = 0
 
     def launch(self, X: torch.Tensor, stream: int | None = None) -> None:
         """Rotate X (cols x k, this rank's device) and run the peer-store MMQ; no synchronisation."""
@@ -337,8 +373,10 @@ class TPMatmul:
                  X.stride(1), self.q.block_n, lib.ptr(self._act), None, s)
         wsn = lib.load().itq3_mmq_ws_nbytes(self.q.rows, self.cols, k)
         self._ws = torch.empty(wsn, dtype=torch.uint8, device=self.dev) if wsn else None
+        self.parity = self.calls & 1
+        self.calls += 1
         lib.call("itq3_mmq_peers", lib.ptr(self.q.mmq_layout()), self.q.rows, self.cols, self.q.mmq_flags(),
-                 lib.ptr(self._act), k, lib.ptr(self.peers), self.world, self.r0, lib.F32, k, 1,
+                 lib.ptr(self._act), k, lib.ptr(self.peers[self.parity]), self.world, self.r0, lib.F32, k, 1,
                  lib.ptr(self._ws) if self._ws is not None else None, s)
 
     def __call__(self, X: torch.Tensor) -> torch.Tensor:
@@ -347,4 +385,5 @@ class TPMatmul:
         if self.hdl is not None:
             self.hdl.barrier()  # every rank's peer stores have landed before anyone reads Y
         k = X.shape[1]
-        return self.ybuf[: self.rows * k].view(self.rows, k)
+        base = self.parity * self.rows * self.max_tokens
+        return self.ybuf[base: base + self.rows * k].view(self.rows, k)

@@ -119,18 +119,52 @@ def full(itq3):
         json.dump(digests, f, indent=1)
 
 
+# Extra C3 row samples (rows x K, M, weight seed): embedded by tests/test_gpu_c3_shapes.py into the
+# LAST rows of a full Llama-3-8B-shaped layer, so the reference's outputs pin the kernels at the
+# shapes the sweep times (K5 for M = 128 / 1024 / 2048, K5b for M = 64).
+C3_EXTRA = [(256, 4096, 128, 4), (128, 4096, 2048, 5), (128, 14336, 64, 6), (128, 14336, 1024, 7)]
+
+
+def c3_extra(itq3):
+    from itq3.codec import QuantConfig
+    from itq3.compute import generate_weights
+
+    path = os.path.join(HERE, "full_digests.json")
+    with open(path) as f:
+        digests = json.load(f)
+    digests["c3"] = digests["c3"][:1]
+    for rows, cols, m, seed in C3_EXTRA:
+        t = time.time()
+        w = generate_weights("gaussian", rows, cols, seed=seed).astype(np.float32)
+        X = np.random.default_rng(seed + 100).standard_normal((cols, m)).astype(np.float32)
+        q = itq3.quantize_tensor(w, QuantConfig())
+        Y = itq3.fused_matmul(q, X)
+        name = f"mmq_c3_{rows}x{cols}_m{m}.npy"
+        np.save(os.path.join(HERE, name), Y)
+        digests["c3"].append(dict(rows=rows, cols=cols, m=m, seed=seed, x_seed=seed + 100, input_sha256=sha(w),
+                                  x_sha256=sha(X), container_sha256=sha(container(itq3, q)), y_file=name))
+        print("mmq sample", rows, cols, m, f"{time.time() - t:.1f}s")
+    with open(path, "w") as f:
+        json.dump(digests, f, indent=1)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--full-only", action="store_true")
+    ap.add_argument("--c3-extra", action="store_true", help="only (re)generate the extra C3 row samples")
     args = ap.parse_args()
     sys.path.insert(0, REF)
     import itq3  # noqa: E402  (the reference, read-only)
 
+    if args.c3_extra:
+        c3_extra(itq3)
+        return
     if not args.full_only:
         small_cases(itq3)
     if args.full or args.full_only:
         full(itq3)
+        c3_extra(itq3)
 
 
 if __name__ == "__main__":

@@ -10,7 +10,7 @@ pytestmark = pytest.mark.gpu
 P = pytest.importorskip("paper_2603_27914_b200")
 from paper_2603_27914_b200.decoder import DecoderStack  # noqa: E402
 
-SMALL = dict(hidden=512, inter=1024, n_heads=4, n_kv=2, head_dim=128, rope_theta=10000.0)
+SMALL = dict(hidden=512, inter=1024, n_heads=4, n_kv=2, head_dim=128, rope_theta=10000.0, vocab=2000)
 
 
 def test_decoder_steps_match_fp32_reference():
@@ -25,4 +25,29 @@ def test_decoder_steps_match_fp32_reference():
         want = st.reference_step(x, pos, k_hist, v_hist)
         err = float((got - want).norm() / want.norm())
         assert err < 1e-4, (pos, err)
+        lerr = float((st.logits - st.ref_logits).norm() / st.ref_logits.norm())  # RMSNorm -> lm_head chain
+        assert lerr < 1e-4, (pos, lerr)
     assert int(st.pos) == 300
+
+
+def test_decoder_kv_cache_bound():
+    """the graphed step advances the device position with no host work, so the host keeps
+    its own counter and refuses a step once the cache is full; the glue kernel also refuses a
+    position >= max_ctx on the device (no cache write, error word set)."""
+    dev = torch.device("cuda", 0)
+    st = DecoderStack(layers=1, max_ctx=8, seed=5, dev=dev, shapes=SMALL, serving=False)
+    st.capture()
+    st.reset(6)
+    x = torch.randn(512, device=dev)
+    st.step(x)
+    st.step(x)
+    with pytest.raises(ValueError, match="KV cache full"):
+        st.step(x)
+    assert st.device_error() == 0
+    kc = st.k_cache.clone()
+    st.graph.replay()  # bypass the host guard: the device position is now 8 == max_ctx
+    torch.cuda.synchronize()
+    assert st.device_error() == 1
+    assert torch.equal(st.k_cache, kc)
+    with pytest.raises(ValueError):
+        st.reset(8)

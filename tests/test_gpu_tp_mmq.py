@@ -38,13 +38,20 @@ def test_tp_mmq_peer_stores(world, m):
     X = torch.from_numpy(rng.standard_normal((cols, m)).astype(np.float32)).cuda()
     ref = unsharded(q, X)
     if world == 1:
-        Y = TPMatmul(q, rows, 512)(X)
+        tp = TPMatmul(q, rows, 512)
+        Y = tp(X)
         torch.cuda.synchronize()
         torch.testing.assert_close(Y, ref, rtol=0, atol=0)
         exact, bound = mmq_bound(q.payload().cpu().numpy(), rows, cols, X.cpu().numpy())
         assert np.all(np.abs(Y.cpu().numpy() - exact) <= bound)
+        # double-buffered by call parity: the next call writes the other half, Y stays intact
+        Y2 = tp(2 * X)
+        torch.cuda.synchronize()
+        assert Y2.data_ptr() != Y.data_ptr()
+        torch.testing.assert_close(Y, ref, rtol=0, atol=0)
+        assert tp(X).data_ptr() == Y.data_ptr()
         return
-    bufs = [torch.full((rows * 512,), float("nan"), dtype=torch.float32, device="cuda") for _ in range(world)]
+    bufs = [torch.full((2 * rows * 512,), float("nan"), dtype=torch.float32, device="cuda") for _ in range(world)]
     bases = [b.data_ptr() for b in bufs]
     tps = [TPMatmul(shard_quantized(q, world, r), rows, 512, world=world, rank=r, ybuf=bufs[r], peer_bases=bases)
            for r in range(world)]

@@ -147,3 +147,19 @@ def test_scalar_rules_vs_reference_fixtures():
     st = P.BlockStats(n=int(s[0]), mean=s[1], sigma=s[2], l1=s[3], linf=s[4], excess_kurtosis=s[5])
     got = [P.optimal_scale(st, P.ScalePolicy(kind=k)) for k in ("constant", "argmin", "mean-abs")]
     np.testing.assert_array_equal(got, G["os_out"])
+
+
+@pytest.mark.slow
+def test_c3_samples_oracle(golden):
+    """The oracle's fused_matmul reproduces the reference's C3 row samples (make_golden.py C3_EXTRA)."""
+    _, _, full = golden
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    for c in full["c3"][1:]:
+        w = O.generate_weights("gaussian", c["rows"], c["cols"], seed=c["seed"]).astype(np.float32)
+        X = np.random.default_rng(c["x_seed"]).standard_normal((c["cols"], c["m"])).astype(np.float32)
+        assert sha(w) == c["input_sha256"] and sha(X) == c["x_sha256"]
+        pay, pad = O.quantize_payload(w)
+        data = O.container_bytes(pay, c["rows"], c["cols"], 256, "s", True, pad)
+        assert hashlib.sha256(data).hexdigest() == c["container_sha256"]
+        Y = O.fused_matmul(pay, c["rows"], c["cols"], 256, False, X)
+        np.testing.assert_allclose(Y, np.load(os.path.join(here, c["y_file"])), rtol=1e-9, atol=1e-12)
