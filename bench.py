@@ -290,7 +290,7 @@ def run_decoder(args):
                        "model": "llama3-8b (decoder, random init)", "global_batch": world, "seq_len": 1,
                        "parallelism": "single" if world == 1 else f"replicas{world}"},
             "packed_weight_gbps": tiled / (ms / 1000.0) / 1e9,
-            "gpu_launches": 4 * args.layers * args.steps}), flush=True)  # 3 chains + 1 attention kernel per layer
+            "gpu_launches": st.launches_per_step() * args.steps}), flush=True)  # 2 chains + 1 attention per layer
     if world > 1:
         torch.distributed.destroy_process_group()
 

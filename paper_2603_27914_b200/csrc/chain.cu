@@ -452,17 +452,28 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         const int nb = min(kUnitBlocks, st.NB - b0);
         const bool has_block = warp < nb;
         float nscale = 1.f;
+        float xv[8];  // RMSNorm input stages: this warp's block of the (residual) input before the norm
         if (GATED && (st.asym & 4)) {
             // RMSNorm input stage (decoder; host-checked cols <= 4096, so this CTA's chunk is the whole
             // input vector): every consumer warp adds its block's squares, one named barrier, and the
-            // scale multiplies the input as it is loaded below
+            // scale multiplies the input as it is loaded below.  Flag 16 (residual input, s >= 1): the
+            // input is x0 + the previous stage's output -- the residual stream after an o projection
+            // folded into the same launch (h + W_o att, then RMSNorm, as the reference step orders it).
             float ss = 0.f;
-            if (has_block)
+            if (has_block) {
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const float v = __ldg(x0 + 256 * (b0 + warp) + lane + 32 * e);
-                    ss += v * v;
+                for (int e = 0; e < 8; ++e) xv[e] = __ldg(x0 + 256 * (b0 + warp) + lane + 32 * e);
+                if ((st.asym & 16) && s > 0) {
+                    const ChainStage pv = s - 1 < kSmemStages ? sm.desc[s - 1] : stages[s - 1];
+                    const int pn = (pv.NB + kUnitBlocks - 1) / kUnitBlocks;
+                    float pf[8];
+                    load_tagged_block<false>(pv.y + 256 * (b0 + warp), pn, pv.yrows, epoch, lane, pf);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) xv[e] += pf[e];
                 }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) ss += xv[e] * xv[e];
+            }
             for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
             if (lane == 0) sm.normsq[warp] = ss;
             consumer_sync();
@@ -477,11 +488,9 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         if (has_block) {
             float f[8];
             if (GATED && (st.asym & 4)) {
-                // RMSNorm input: x0 * rsqrt(mean(x0^2) + 1e-5) * gain (gain in st.xin)
+                // RMSNorm input: x * rsqrt(mean(x^2) + 1e-5) * gain (gain in st.xin)
 #pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    f[e] = __ldg(x0 + 256 * (b0 + warp) + lane + 32 * e) * nscale *
-                           __ldg(st.xin + 256 * (b0 + warp) + lane + 32 * e);
+                for (int e = 0; e < 8; ++e) f[e] = xv[e] * nscale * __ldg(st.xin + 256 * (b0 + warp) + lane + 32 * e);
             } else if (s == 0 || st.xin) {
                 const float* xs = st.xin ? st.xin : x0;
 #pragma unroll
@@ -615,10 +624,33 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             if (ok) break;
             __nanosleep(64);
         }
-        if (GATED && (last.asym & 8))
-            out[r] += v;  // residual accumulation (decoder): out is the residual stream
-        else
+        if (GATED && (last.asym & 8)) {
+            // residual accumulation (decoder): out is the residual stream.  Flag 32: stage 0's output
+            // (an o projection in the same launch) is added first: out = (out + y_0) + y_last.
+            float base = out[r];
+            if (last.asym & 32) {
+                const ChainStage s0 = sm.desc[0];
+                const int n0 = (s0.NB + kUnitBlocks - 1) / kUnitBlocks;
+                float v0;
+                for (;;) {
+                    bool ok = true;
+                    unsigned long long w = ld_u64_relaxed(s0.y + r);
+                    ok &= (unsigned)(w >> 32) == epoch;
+                    v0 = __uint_as_float((unsigned)w);
+                    for (int c = 1; c < n0; ++c) {
+                        w = ld_u64_relaxed(s0.y + c * s0.yrows + r);
+                        ok &= (unsigned)(w >> 32) == epoch;
+                        v0 += __uint_as_float((unsigned)w);
+                    }
+                    if (ok) break;
+                    __nanosleep(64);
+                }
+                base += v0;
+            }
+            out[r] = base + v;
+        } else {
             out[r] = v;
+        }
     }
     if (cta == 0 && tid == 0) {
         while (atomicAdd(epoch_ptr + 1, 0u) < (unsigned)G) __nanosleep(32);
@@ -664,6 +696,11 @@ extern "C" int itq3_chain_write_desc_tp(void* host_desc, int index, const uint8_
     if ((asymmetric & 4) && cols > 4096) {
         set_error("chain: stage %d: an RMSNorm input stage needs cols <= 4096 (got %lld)", index, (long long)cols);
         return ITQ3_E_UNSUPPORTED;
+    }
+    if (((asymmetric & 16) && (!(asymmetric & 4) || index < 1 || npeer)) || ((asymmetric & 32) && !(asymmetric & 8))) {
+        set_error("chain: stage %d: flag 16 (residual input) needs flag 4 on a stage >= 1 (single GPU); flag 32 needs "
+                  "flag 8", index);
+        return ITQ3_E_DOMAIN;
     }
     st.tiled = tiled;
     st.y = (unsigned long long*)y;

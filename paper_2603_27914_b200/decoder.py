@@ -8,7 +8,9 @@ GEMV.  Everything but the attention runs inside chain launches (csrc/chain.cu, d
 RMSNorm in the loads of the qkv / gate_up stages (every CTA of a 4096-column stage holds the whole
 input), the SiLU gating in the loads of the down stage, the residual adds in the final folds; the
 attention (RoPE + KV append + split decode attention) is one glue kernel (csrc/decoder_glue.cu).
-A layer is 4 launches: [RMSNorm -> qkv], attention, [o -> +=], [RMSNorm -> gate_up -> gate -> down -> +=].  A whole token step is ONE CUDA
+A layer is 3 launches: [RMSNorm -> qkv], attention, [o -> (+= residual) -> RMSNorm -> gate_up -> gate ->
+down -> += residual] (the o projection and the MLP share one launch: the gate_up stage's input is
+RMSNorm(x + W_o att) and the final fold adds W_o att before W_down(...)).  A whole token step is ONE CUDA
 graph: the position lives in a device tensor that the graph itself advances, the attention reads
 the full cache under a position mask, so replays need no host work.
 """
@@ -26,9 +28,11 @@ LLAMA3_8B = dict(hidden=4096, inter=14336, n_heads=32, n_kv=8, head_dim=128, rop
 
 class _Chain:
     """A short chain of ITQ3_S stages run as ONE cooperative launch (csrc/chain.cu, decoder flags):
-    stages = [(QuantizedTensor, flags, gain)], flags bit 1 = gated input (SiLU(gate) * up of the
-    previous stage), bit 2 = RMSNorm input with `gain` (first stage), bit 3 = the fold adds into `out`
-    (the residual stream) instead of overwriting it."""
+    stages = [(QuantizedTensor, flags, xin)], flags bit 1 = gated input (SiLU(gate) * up of the
+    previous stage), bit 2 = RMSNorm input with gain `xin`, bit 3 = the fold adds into `out` (the
+    residual stream) instead of overwriting it, bit 4 = the RMSNorm input is x0 + the previous
+    stage's output (residual after an o projection in the same launch), bit 5 = the fold adds stage
+    0's output first.  A stage-0 `xin` without flag 2 is that stage's input vector."""
 
     def __init__(self, stages, out: torch.Tensor, dev):
         import ctypes
@@ -58,7 +62,7 @@ class _Chain:
         return self.out
 
 
-GATED, NORM_IN, ADD_OUT = 2, 4, 8
+GATED, NORM_IN, ADD_OUT, RESID_IN, ADD_OUT0 = 2, 4, 8, 16, 32
 
 
 class DecoderStack:
@@ -119,14 +123,15 @@ class DecoderStack:
                                    device=self.dev)  # split partials + per-head counters
         if self.hd != 128 or max_ctx > 1024 or self.nh * self.hd != self.h:
             raise ValueError("DecoderStack: the glue kernels need head_dim 128, max_ctx <= 1024, nh * hd = hidden")
-        # per layer: [RMSNorm -> qkv], [o -> += residual], [RMSNorm -> gate_up -> SiLU gating -> down -> += residual]
+        # per layer: [RMSNorm -> qkv], attention, [o -> RMSNorm(x + o) -> gate_up -> SiLU gating -> down ->
+        # x += o + down]
         self.qkv_out = torch.zeros(self.h + 2 * kv, device=self.dev)
         self.chains = []
         for li, (qkv_w, o_w, gu_w, down_w) in enumerate(self.q):
             g1, g2 = self.gain[li][0], self.gain[li][1]
             self.chains.append((_Chain([(qkv_w, NORM_IN, g1)], self.qkv_out, self.dev),
-                                _Chain([(o_w, ADD_OUT, None)], self.xs, self.dev),
-                                _Chain([(gu_w, NORM_IN, g2), (down_w, GATED | ADD_OUT, None)], self.xs, self.dev)))
+                                _Chain([(o_w, 0, self.att), (gu_w, NORM_IN | RESID_IN, g2),
+                                        (down_w, GATED | ADD_OUT | ADD_OUT0, None)], self.xs, self.dev)))
         self.head_chain = (_Chain([(self.lm_head, NORM_IN, self.final_gain)], self.logits, self.dev)
                            if self.lm_head is not None else None)
         self.graph = None
@@ -139,7 +144,7 @@ class DecoderStack:
         return n
 
     def launches_per_step(self) -> int:
-        return 4 * self.layers + (1 if self.lm_head is not None else 0)
+        return 3 * self.layers + (1 if self.lm_head is not None else 0)
 
     def _rms(self, x, gain):
         return torch.nn.functional.rms_norm(x, (self.h,), weight=gain, eps=self.eps)
@@ -149,21 +154,20 @@ class DecoderStack:
         return torch.cat((a * cos - b * sin, a * sin + b * cos), dim=1)
 
     def _step(self) -> None:
-        """One token: per layer 3 chain launches ([RMSNorm -> qkv], [o -> += x], [RMSNorm -> gate_up ->
-        SiLU gating -> down -> += x]) and one glue launch (RoPE + KV append + split attention)."""
+        """One token: per layer 2 chain launches ([RMSNorm -> qkv], [o -> RMSNorm(x + o) -> gate_up -> SiLU
+        gating -> down -> x += o + down]) and one glue launch (RoPE + KV append + split attention)."""
         from . import _lib
 
         st = _lib.stream_ptr(self.dev)
         xs = self.xs
         xs.copy_(self.x)
         for li in range(self.layers):
-            c_qkv, c_o, c_mlp = self.chains[li]
+            c_qkv, c_mlp = self.chains[li]
             qkv = c_qkv(xs, st)
             _lib.call("itq3_glue_rope_attention", _lib.ptr(qkv), _lib.ptr(self.cos), _lib.ptr(self.sin),
                       _lib.ptr(self.pos), _lib.ptr(self.k_cache[li, 0]), _lib.ptr(self.v_cache[li, 0]),
                       _lib.ptr(self.att), self.nh, self.nkv, self.hd, self.max_ctx, _lib.ptr(self.attn_ws), st)
-            c_o(self.att, st)   # xs += W_o att
-            c_mlp(xs, st)       # xs += W_down (SiLU(gate) * up)(RMSNorm(xs))
+            c_mlp(xs, st)  # h = xs + W_o att; xs = h + W_down (SiLU(gate) * up)(RMSNorm(h))
         if self.head_chain is not None:
             self.head_chain(xs, st)  # logits = W_head RMSNorm(xs)
         self.out.copy_(xs)
