@@ -227,6 +227,11 @@ int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* tiled, void
  * `out` (residual stream) instead of overwriting it.  Bits 1-3 need itq3_chain_run_gated. */
 int itq3_chain_write_desc_tp(void* host_desc, int index, const uint8_t* tiled, void* y, int64_t rows, int64_t cols,
                              int asymmetric, int64_t row0, int64_t yrows, const void* d_peers, int npeer);
+/* Decoder flags (itq3_chain_run_gated): bit 4 = an RMSNorm stage's input is x0 + the previous stage's
+ * output; bit 5 (with bit 3) = the final fold adds stage 0's output first; bit 6 = the RMSNorm input
+ * is (x0 + stage 0's output) + the previous stage's output; bit 7 = that stage also writes the input
+ * it formed (the new residual stream) to the buffer set here. */
+int itq3_chain_set_xout(void* host_desc, int index, float* xout);
 int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch, float* out,
                    int grid, void* d_trace, void* stream);
 /* the same, for chains with gated stages (descriptor flag bit 1) */

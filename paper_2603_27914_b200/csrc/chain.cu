@@ -45,6 +45,7 @@ struct ChainStage {
     // y is then double-buffered by epoch parity ([2][nch][yrows]) so a rank already in step t+1
     // never overwrites words a slower peer still reads in step t.
     unsigned long long* const* ypeer;
+    float* xout;  // flag 128: the residual input this RMSNorm stage computed, written once (decoder)
     int64_t rows, cols;
     int32_t NB, RT, asym, npeer;
     int32_t row0, yrows;
@@ -261,7 +262,7 @@ __device__ __forceinline__ float2 chain_tile(const uint8_t* ring, int warp, int 
     return make_float2(d0 * (fcx * v0 - zf0 * corr), d1 * (fcx * v1 - zf1 * corr));
 }
 
-constexpr int kSmemStages = 150;  // stage descriptors + this CTA's split cached in smem (global beyond)
+constexpr int kSmemStages = 136;  // stage descriptors + this CTA's split cached in smem (global beyond)
 
 // Work split of stage st for CTA cta: K-chunk ch (CTAs c with c % nch == ch), and the row
 // tiles rt = rt0, rt0 + Gc, ... (Gc CTAs per chunk); active = 0 if the CTA is idle.
@@ -463,7 +464,15 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             if (has_block) {
 #pragma unroll
                 for (int e = 0; e < 8; ++e) xv[e] = __ldg(x0 + 256 * (b0 + warp) + lane + 32 * e);
-                if ((st.asym & 16) && s > 0) {
+                if ((st.asym & 64) && s > 1) {  // flag 64: x0 + stage 0's output first, then the previous stage's
+                    const ChainStage s0 = sm.desc[0];
+                    float pf[8];
+                    load_tagged_block<false>(s0.y + 256 * (b0 + warp), (s0.NB + kUnitBlocks - 1) / kUnitBlocks,
+                                             s0.yrows, epoch, lane, pf);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) xv[e] += pf[e];
+                }
+                if ((st.asym & (16 | 64)) && s > 0) {
                     const ChainStage pv = s - 1 < kSmemStages ? sm.desc[s - 1] : stages[s - 1];
                     const int pn = (pv.NB + kUnitBlocks - 1) / kUnitBlocks;
                     float pf[8];
@@ -471,6 +480,9 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 #pragma unroll
                     for (int e = 0; e < 8; ++e) xv[e] += pf[e];
                 }
+                if ((st.asym & 128) && sp.rt0 == 0)  // one CTA publishes the updated residual stream
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) st.xout[256 * (b0 + warp) + lane + 32 * e] = xv[e];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) ss += xv[e] * xv[e];
             }
@@ -670,6 +682,12 @@ extern "C" int itq3_chain_smem_bytes(void) { return (int)sizeof(ChainSmem); }
 extern "C" int itq3_chain_write_desc_tp(void*, int, const uint8_t*, void*, int64_t, int64_t, int, int64_t, int64_t,
                                         const void*, int);
 
+// flag 128 (decoder): where the RMSNorm stage `index` writes the residual input it computed
+extern "C" int itq3_chain_set_xout(void* host_desc, int index, float* xout) {
+    reinterpret_cast<ChainStage*>(host_desc)[index].xout = xout;
+    return ITQ3_OK;
+}
+
 extern "C" int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* tiled, void* y, const float* xin,
                                      int64_t rows, int64_t cols, int asymmetric, int reserved) {
     (void)reserved;
@@ -697,14 +715,16 @@ extern "C" int itq3_chain_write_desc_tp(void* host_desc, int index, const uint8_
         set_error("chain: stage %d: an RMSNorm input stage needs cols <= 4096 (got %lld)", index, (long long)cols);
         return ITQ3_E_UNSUPPORTED;
     }
-    if (((asymmetric & 16) && (!(asymmetric & 4) || index < 1 || npeer)) || ((asymmetric & 32) && !(asymmetric & 8))) {
-        set_error("chain: stage %d: flag 16 (residual input) needs flag 4 on a stage >= 1 (single GPU); flag 32 needs "
-                  "flag 8", index);
+    if (((asymmetric & 16) && (!(asymmetric & 4) || index < 1 || npeer)) || ((asymmetric & 32) && !(asymmetric & 8)) ||
+        ((asymmetric & 64) && (!(asymmetric & 4) || index < 2 || npeer)) || ((asymmetric & 128) && !(asymmetric & 4))) {
+        set_error("chain: stage %d: flag 16 (residual input) needs flag 4 on a stage >= 1, flag 64 on a stage >= 2 "
+                  "(single GPU); flag 32 needs flag 8; flag 128 needs flag 4", index);
         return ITQ3_E_DOMAIN;
     }
     st.tiled = tiled;
     st.y = (unsigned long long*)y;
     st.xin = nullptr;
+    st.xout = nullptr;
     st.ypeer = (unsigned long long* const*)d_peers;
     st.rows = rows;
     st.cols = cols;

@@ -8,9 +8,10 @@ GEMV.  Everything but the attention runs inside chain launches (csrc/chain.cu, d
 RMSNorm in the loads of the qkv / gate_up stages (every CTA of a 4096-column stage holds the whole
 input), the SiLU gating in the loads of the down stage, the residual adds in the final folds; the
 attention (RoPE + KV append + split decode attention) is one glue kernel (csrc/decoder_glue.cu).
-A layer is 3 launches: [RMSNorm -> qkv], attention, [o -> (+= residual) -> RMSNorm -> gate_up -> gate ->
-down -> += residual] (the o projection and the MLP share one launch: the gate_up stage's input is
-RMSNorm(x + W_o att) and the final fold adds W_o att before W_down(...)).  A whole token step is ONE CUDA
+A layer is 2 launches: attention, then ONE chain [o -> RMSNorm(x + o) -> gate_up -> SiLU gating -> down
+-> RMSNorm((x + o) + down) -> next layer's qkv] whose last stage also writes the new residual stream
+(ping-pong buffers); the last layer's chain ends in the lm_head.  Plus one [RMSNorm -> qkv] launch for
+layer 0: 2 x layers + 1 launches per token.  A whole token step is ONE CUDA
 graph: the position lives in a device tensor that the graph itself advances, the attention reads
 the full cache under a position mask, so replays need no host work.
 """
@@ -32,9 +33,11 @@ class _Chain:
     previous stage), bit 2 = RMSNorm input with gain `xin`, bit 3 = the fold adds into `out` (the
     residual stream) instead of overwriting it, bit 4 = the RMSNorm input is x0 + the previous
     stage's output (residual after an o projection in the same launch), bit 5 = the fold adds stage
-    0's output first.  A stage-0 `xin` without flag 2 is that stage's input vector."""
+    0's output first, bit 6 = the RMSNorm input is (x0 + stage 0's output) + the previous stage's
+    output (the residual after a whole layer), bit 7 = that stage also writes the residual it formed
+    to `xout`.  A stage-0 `xin` without flag 2 is that stage's input vector."""
 
-    def __init__(self, stages, out: torch.Tensor, dev):
+    def __init__(self, stages, out: torch.Tensor, dev, xout: torch.Tensor | None = None):
         import ctypes
 
         from . import _lib
@@ -50,6 +53,9 @@ class _Chain:
             _lib.check(lib.itq3_chain_write_desc(host, i, _lib.ptr(q.tiled()), _lib.ptr(y),
                                                  _lib.ptr(gain) if gain is not None else None, q.rows, q.cols,
                                                  int(not q.symmetric) | flags, 0))
+            if flags & XOUT:
+                _lib.check(lib.itq3_chain_set_xout(host, i, _lib.ptr(xout)))
+                self.keep.append(xout)
         self.n = len(stages)
         self.desc = torch.frombuffer(bytearray(host.raw), dtype=torch.uint8).to(dev)
         self.epoch = torch.zeros(2, dtype=torch.int32, device=dev)
@@ -62,7 +68,7 @@ class _Chain:
         return self.out
 
 
-GATED, NORM_IN, ADD_OUT, RESID_IN, ADD_OUT0 = 2, 4, 8, 16, 32
+GATED, NORM_IN, ADD_OUT, RESID_IN, ADD_OUT0, RESID2_IN, XOUT = 2, 4, 8, 16, 32, 64, 128
 
 
 class DecoderStack:
@@ -115,7 +121,6 @@ class DecoderStack:
         self.x = torch.zeros(self.h, device=self.dev)
         self.out = torch.zeros(self.h, device=self.dev)
         self.kpos = torch.arange(max_ctx, device=self.dev)
-        self.xs = torch.zeros(self.h, device=self.dev)          # residual stream
         self.att = torch.zeros(self.h, device=self.dev)         # attention output (nh * hd)
         from . import _lib
 
@@ -123,17 +128,27 @@ class DecoderStack:
                                    device=self.dev)  # split partials + per-head counters
         if self.hd != 128 or max_ctx > 1024 or self.nh * self.hd != self.h:
             raise ValueError("DecoderStack: the glue kernels need head_dim 128, max_ctx <= 1024, nh * hd = hidden")
-        # per layer: [RMSNorm -> qkv], attention, [o -> RMSNorm(x + o) -> gate_up -> SiLU gating -> down ->
-        # x += o + down]
+        # launch 0: [RMSNorm -> qkv_0]; layer L: attention, then [o -> RMSNorm(x + o) -> gate_up -> SiLU gating
+        # -> down -> RMSNorm(x + o + down) -> qkv_{L+1} (or the lm_head)], the residual ping-ponging between
+        # self.xs2[L % 2] (read) and self.xs2[(L + 1) % 2] (written by the last stage)
         self.qkv_out = torch.zeros(self.h + 2 * kv, device=self.dev)
+        self.xs2 = [torch.zeros(self.h, device=self.dev), torch.zeros(self.h, device=self.dev)]
+        self.first = _Chain([(self.q[0][0], NORM_IN, self.gain[0][0])], self.qkv_out, self.dev)
         self.chains = []
-        for li, (qkv_w, o_w, gu_w, down_w) in enumerate(self.q):
-            g1, g2 = self.gain[li][0], self.gain[li][1]
-            self.chains.append((_Chain([(qkv_w, NORM_IN, g1)], self.qkv_out, self.dev),
-                                _Chain([(o_w, 0, self.att), (gu_w, NORM_IN | RESID_IN, g2),
-                                        (down_w, GATED | ADD_OUT | ADD_OUT0, None)], self.xs, self.dev)))
-        self.head_chain = (_Chain([(self.lm_head, NORM_IN, self.final_gain)], self.logits, self.dev)
-                           if self.lm_head is not None else None)
+        for li, (_, o_w, gu_w, down_w) in enumerate(self.q):
+            mlp = [(o_w, 0, self.att), (gu_w, NORM_IN | RESID_IN, self.gain[li][1])]
+            if li + 1 < layers:
+                nxt, out = (self.q[li + 1][0], NORM_IN | RESID2_IN | XOUT, self.gain[li + 1][0]), self.qkv_out
+            elif self.lm_head is not None:
+                nxt, out = (self.lm_head, NORM_IN | RESID2_IN | XOUT, self.final_gain), self.logits
+            else:
+                nxt, out = None, self.xs2[li % 2]
+            if nxt is None:  # last layer without a head: fold x += o + down in place
+                stages = mlp + [(down_w, GATED | ADD_OUT | ADD_OUT0, None)]
+            else:
+                stages = mlp + [(down_w, GATED, None), nxt]
+            self.chains.append(_Chain(stages, out, self.dev, xout=self.xs2[(li + 1) % 2]))
+        self.final_xs = self.xs2[layers % 2] if self.lm_head is not None else self.xs2[(layers - 1) % 2]
         self.graph = None
 
     def weight_bytes(self) -> int:
@@ -144,7 +159,7 @@ class DecoderStack:
         return n
 
     def launches_per_step(self) -> int:
-        return 3 * self.layers + (1 if self.lm_head is not None else 0)
+        return 2 * self.layers + 1
 
     def _rms(self, x, gain):
         return torch.nn.functional.rms_norm(x, (self.h,), weight=gain, eps=self.eps)
@@ -154,23 +169,21 @@ class DecoderStack:
         return torch.cat((a * cos - b * sin, a * sin + b * cos), dim=1)
 
     def _step(self) -> None:
-        """One token: per layer 2 chain launches ([RMSNorm -> qkv], [o -> RMSNorm(x + o) -> gate_up -> SiLU
-        gating -> down -> x += o + down]) and one glue launch (RoPE + KV append + split attention)."""
+        """One token: the layer-0 [RMSNorm -> qkv] chain, then per layer one glue launch (RoPE + KV append +
+        split attention) and one chain [o -> ... -> down -> next qkv / lm_head]."""
         from . import _lib
 
         st = _lib.stream_ptr(self.dev)
-        xs = self.xs
-        xs.copy_(self.x)
+        self.xs2[0].copy_(self.x)
+        self.first(self.xs2[0], st)  # qkv_0 = W_qkv RMSNorm(x)
         for li in range(self.layers):
-            c_qkv, c_mlp = self.chains[li]
-            qkv = c_qkv(xs, st)
-            _lib.call("itq3_glue_rope_attention", _lib.ptr(qkv), _lib.ptr(self.cos), _lib.ptr(self.sin),
+            _lib.call("itq3_glue_rope_attention", _lib.ptr(self.qkv_out), _lib.ptr(self.cos), _lib.ptr(self.sin),
                       _lib.ptr(self.pos), _lib.ptr(self.k_cache[li, 0]), _lib.ptr(self.v_cache[li, 0]),
                       _lib.ptr(self.att), self.nh, self.nkv, self.hd, self.max_ctx, _lib.ptr(self.attn_ws), st)
-            c_mlp(xs, st)  # h = xs + W_o att; xs = h + W_down (SiLU(gate) * up)(RMSNorm(h))
-        if self.head_chain is not None:
-            self.head_chain(xs, st)  # logits = W_head RMSNorm(xs)
-        self.out.copy_(xs)
+            # h = x + W_o att; x' = h + W_down (SiLU(gate) * up)(RMSNorm(h)); qkv_{L+1} = W_qkv RMSNorm(x')
+            # (the last layer: logits = W_head RMSNorm(x'))
+            self.chains[li](self.xs2[li % 2], st)
+        self.out.copy_(self.final_xs)
         self.pos.add_(1)
 
     def capture(self) -> None:

@@ -93,7 +93,7 @@ def test_host_side_layout_functions():
     per32 = lib.itq3_mmq_nbytes(1000, 4096, 2)
     assert plain == (1024 // 128) * (4096 // 128) * (4096 + 256 + 128)
     assert per32 == (1024 // 128) * (4096 // 128) * (4096 + 1024 + 512)
-    assert lib.itq3_glue_attention_ws_nbytes(32) == 32 * (4 * 130 * 4 + 4) + 4  # + error word
+    assert lib.itq3_glue_attention_ws_nbytes(32) == 32 * (16 * 130 * 4 + 4) + 4  # 16 splits + error word
     host = ctypes.create_string_buffer(lib.itq3_chain_desc_nbytes() * 2)
     # RMSNorm-input stages need the whole input in one CTA chunk (cols <= 4096)
     assert lib.itq3_chain_write_desc(host, 0, None, None, None, 1024, 4096, 4, 0) == 0

@@ -51,3 +51,18 @@ def test_decoder_kv_cache_bound():
     assert torch.equal(st.k_cache, kc)
     with pytest.raises(ValueError):
         st.reset(8)
+
+
+def test_decoder_without_head_matches_fp32_reference():
+    """lm_head=False: the last layer's chain folds x += o + down in place (flags 8 | 32)."""
+    dev = torch.device("cuda", 0)
+    st = DecoderStack(layers=3, max_ctx=64, seed=8, dev=dev, shapes=SMALL, serving=False, lm_head=False)
+    g = torch.Generator(device=dev)
+    g.manual_seed(9)
+    k_hist, v_hist = [[] for _ in range(3)], [[] for _ in range(3)]
+    for pos in range(20):
+        x = torch.randn(512, generator=g, device=dev)
+        got = st.step(x).clone()
+        want = st.reference_step(x, pos, k_hist, v_hist)
+        err = float((got - want).norm() / want.norm())
+        assert err < 1e-4, (pos, err)

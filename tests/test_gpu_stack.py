@@ -91,7 +91,7 @@ def test_chain_replay_deterministic_and_matches_kernels():
 
 
 def test_chain_beyond_smem_descriptor_cache():
-    """170 stages: descriptors past the kernel's shared-memory cache (150) come from global memory
+    """170 stages: descriptors past the kernel's shared-memory cache (136) come from global memory
     with the work split computed per stage; every stage still matches the oracle bound."""
     shapes = [(512, 256), (256, 512)] * 85
     qs = build(21, shapes=shapes)
