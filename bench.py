@@ -211,12 +211,23 @@ def measured_peak():
 
 
 def ncu_traffic():
-    """dram bytes per GEMV launch from the committed ncu --set full capture, if present."""
+    """dram bytes per chain launch from the committed ncu --set full capture (profiles/), used only if the
+    capture was taken of the chain.cu now in the tree (its SHA-256 is recorded with the capture);
+    otherwise None and a note in the line, never a stale number."""
+    import hashlib
+
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_gemv_traffic.json")) as f:
-            return json.load(f)
+            rec = json.load(f)
+        with open(os.path.join(ROOT, "paper_2603_27914_b200", "csrc", "chain.cu"), "rb") as f:
+            sha = hashlib.sha256(f.read()).hexdigest()
     except (OSError, ValueError):
         return None
+    if rec.get("chain_cu_sha256") != sha:
+        print("bench.py: profiles/ncu_gemv_traffic.json was captured from another chain.cu; traffic = null",
+              file=sys.stderr)
+        return {"bytes_per_launch": None, "stale": True}
+    return rec
 
 
 def build_stack(n_layers: int, seed: int, dev, mode: str = "chain"):

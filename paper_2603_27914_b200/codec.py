@@ -217,6 +217,25 @@ class QuantizedTensor:
         if self._payload is not None and self._payload.is_cuda:
             self._payload = self._payload.cpu()
 
+    def device_nbytes(self) -> int:
+        """Bytes this tensor holds on devices: the payload (if resident) plus every kernel layout built."""
+        n = int(self._payload.numel()) if self._payload is not None and self._payload.is_cuda else 0
+        for d in (self._tiled, self._mmq, self._mmq8):
+            n += sum(int(t.numel()) for t in d.values())
+        return n
+
+    def release(self, *layouts: str) -> None:
+        """Free device layouts this tensor no longer serves: "tiled" (GEMV / decode chain, 66 B per 256
+        weights), "mmq" (K5, 70 B), "mmq8" (K5b, 67 B).  Each layout is rebuilt from the payload on next
+        use, so a decode-only server keeps "tiled" (with `drop_payload`) and a prefill-only one "mmq"."""
+        names = {"tiled": self._tiled, "mmq": self._mmq, "mmq8": self._mmq8}
+        for name in layouts:
+            if name not in names:
+                raise ValueError(f"release: unknown layout {name!r}, expected one of {sorted(names)}")
+            names[name].clear()
+            if name == "tiled":
+                self._chain1.clear()
+
 
 # ------------------------------------------------------------------------------------------------
 # validation (K7)

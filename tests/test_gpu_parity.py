@@ -328,3 +328,19 @@ def test_dequant_tensor_core_path_bit_exact(nblocks, tail):
         assert np.array_equal(got.view(np.uint64), exp.view(np.uint64)) or \
             np.array_equal(np.isnan(got), np.isnan(exp)) and np.array_equal(
                 np.where(np.isnan(got), 0, got).view(np.uint64), np.where(np.isnan(exp), 0, exp).view(np.uint64)), dt
+
+
+def test_release_layouts_and_rebuild():
+    """Weight memory per format (VERDICT r01 weak #9): layouts can be released and are rebuilt on use."""
+    rng = np.random.default_rng(12)
+    q = P.quantize_tensor(rng.standard_normal((512, 1024)) * 0.05)
+    X = torch.from_numpy(rng.standard_normal((1024, 32)).astype(np.float32)).cuda()
+    x = X[:, 0].contiguous()
+    y1, Y1 = P.fused_matvec(q, x).clone(), P.fused_matmul(q, X).clone()
+    base = q.device_nbytes()
+    q.release("tiled", "mmq8")
+    assert q.device_nbytes() < base
+    torch.testing.assert_close(P.fused_matvec(q, x), y1, rtol=0, atol=0)
+    torch.testing.assert_close(P.fused_matmul(q, X), Y1, rtol=0, atol=0)
+    with pytest.raises(ValueError):
+        q.release("bogus")
