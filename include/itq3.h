@@ -231,7 +231,17 @@ int itq3_chain_write_desc_tp(void* host_desc, int index, const uint8_t* tiled, v
  * output; bit 5 (with bit 3) = the final fold adds stage 0's output first; bit 6 = the RMSNorm input
  * is (x0 + stage 0's output) + the previous stage's output; bit 7 = that stage also writes the input
  * it formed (the new residual stream) to the buffer set here. */
-int itq3_chain_set_xout(void* host_desc, int index, float* xout);
+int itq3_chain_set_xout(void* host_desc, int index, void* xout);
+/* decoder, single GPU: the tagged residual buffer (u64 words) a flag-4 / flag-8 stage reads instead of
+ * the launch input x0; flag-64 / flag-32 stages name the o stage whose output they add in flag bits 16-31 */
+int itq3_chain_set_xres(void* host_desc, int index, const void* xres);
+/* decoder attention as chain stages (GATED launches): kind 256 = per (kv head, split) partials of RoPE +
+ * KV append + grouped-query attention over the previous (qkv) stage's outputs, kind 512 = per-head
+ * combine into the next stage's input; params = device struct of itq3_chain_attn_params_nbytes() bytes:
+ * {float* k_cache; float* v_cache; const float* cos; const float* sin; const int64_t* pos;
+ *  int n_heads, n_kv, ctx, splits} (head_dim 128, 4 query heads per kv head, ceil(ctx / splits) <= 64) */
+int itq3_chain_write_desc_attn(void* host_desc, int index, int kind, const void* params, void* y, int64_t yrows);
+int itq3_chain_attn_params_nbytes(void);
 int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch, float* out,
                    int grid, void* d_trace, void* stream);
 /* the same, for chains with gated stages (descriptor flag bit 1) */

@@ -75,6 +75,9 @@ SIGNATURES = {
     "itq3_chain_smem_bytes": (_i32, []),
     "itq3_chain_write_desc": (_i32, [_vp, _i32, _vp, _vp, _vp, _i64, _i64, _i32, _i32]),
     "itq3_chain_set_xout": (_i32, [_vp, _i32, _vp]),
+    "itq3_chain_set_xres": (_i32, [_vp, _i32, _vp]),
+    "itq3_chain_write_desc_attn": (_i32, [_vp, _i32, _i32, _vp, _vp, _i64]),
+    "itq3_chain_attn_params_nbytes": (_i32, []),
     "itq3_chain_write_desc_tp": (_i32, [_vp, _i32, _vp, _vp, _i64, _i64, _i32, _i64, _i64, _vp, _i32]),
     "itq3_chain_run": (_i32, [_vp, _i32, _vp, _i32, _vp, _vp, _i32, _vp, _vp]),
     "itq3_chain_run_gated": (_i32, [_vp, _i32, _vp, _i32, _vp, _vp, _i32, _vp, _vp]),

@@ -30,7 +30,6 @@ constexpr int kSlotCodes = kUnitBlocks * 1024;           // 16 KB
 constexpr int kSlotScales = kUnitBlocks * 32;            // 512 B
 constexpr int kSlotZps = kUnitBlocks * 16;               // 256 B
 constexpr int kSlotBytes = kSlotCodes + kSlotScales + kSlotZps;
-constexpr int kNumSlots = 11;
 constexpr int kMaxChainNB = 256;                         // K up to 65536
 constexpr int kMaxChainPeers = 8;                        // tensor-parallel ranks (one NVLink domain)
 constexpr int kMaxLimbs = 4;
@@ -44,8 +43,12 @@ struct ChainStage {
     // (ypeer[p] = rank p's y, NVLink peer pointers), so the all-gather is fused into the reducer.
     // y is then double-buffered by epoch parity ([2][nch][yrows]) so a rank already in step t+1
     // never overwrites words a slower peer still reads in step t.
-    unsigned long long* const* ypeer;
-    float* xout;  // flag 128: the residual input this RMSNorm stage computed, written once (decoder)
+    union {
+        unsigned long long* const* ypeer;  // npeer > 0: the ranks' copies of y
+        const unsigned long long* xres;    // decoder (npeer == 0): tagged residual stream the flag-16/64
+                                           // input adds (null: the launch input x0, untagged)
+    };
+    unsigned long long* xout;  // flag 128: where this RMSNorm stage writes the residual it formed (tagged)
     int64_t rows, cols;
     int32_t NB, RT, asym, npeer;
     int32_t row0, yrows;
@@ -262,7 +265,226 @@ __device__ __forceinline__ float2 chain_tile(const uint8_t* ring, int warp, int 
     return make_float2(d0 * (fcx * v0 - zf0 * corr), d1 * (fcx * v1 - zf1 * corr));
 }
 
-constexpr int kSmemStages = 136;  // stage descriptors + this CTA's split cached in smem (global beyond)
+// stage descriptors + this CTA's split cached in smem (global beyond) and the weight-ring depth: the
+// decoder instantiation (GATED) trades one ring slot for room to cache a whole token's ~200 stages
+template <bool GATED>
+struct ChainCfg {
+    static constexpr int kSlots = GATED ? 10 : 11;
+    static constexpr int kStages = GATED ? 240 : 136;
+};
+constexpr int kSmemStages = ChainCfg<false>::kStages;
+
+// ------------------------------------------------------------------------------------------------
+// Decoder attention as chain stages (GATED instantiation; the decoder harness of SURVEY.md 8(f)3, not
+// an ITQ3_S function).  ATTN_PART (flag 256): item (kv head, split) of nkv x S items, one per CTA;
+// the 16 consumer warps read q (the kv head's G = 4 query heads), k and v from the qkv stage's tagged
+// outputs, apply RoPE (rotate-half), append k / v to the KV cache at pos (split 0), score the split's
+// positions (warp per position, lane = 4 dims x 4 heads), take the per-head softmax statistics and
+// P V, and publish (max, sum, 4 x 128 weighted V) as tagged words.  ATTN_COMB (flag 512): CTA h < nh
+// combines head h's S partials into 128 tagged attention outputs, the next stage's input.
+// ------------------------------------------------------------------------------------------------
+struct AttnParams {
+    float* kc;           // this layer's K cache [nkv][ctx][128] (fp32)
+    float* vc;           // V cache, same layout
+    const float* cosb;   // [ctx][64] RoPE tables
+    const float* sinb;
+    const int64_t* pos;  // device position of the token
+    unsigned* err;       // bit 0 set when a launch sees a position outside [0, ctx) (no cache write)
+    int nh, nkv, ctx, S;
+};
+constexpr int kAttnG = 4, kAttnHD = 128, kAttnWords = kAttnHD + 2;  // partial record: max, sum, 128 acc
+constexpr int kAttnMaxChunk = 64;  // positions per split: ceil(ctx / S) <= 64 (host-checked)
+
+__device__ __forceinline__ void tagged_load4(const unsigned long long* p, unsigned epoch, int lane, float (&v)[4]) {
+    for (;;) {
+        bool ok = true;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const unsigned long long w = ld_u64_relaxed(p + lane + 32 * j);
+            ok &= (unsigned)(w >> 32) == epoch;
+            v[j] = __uint_as_float((unsigned)w);
+        }
+        if (__all_sync(FULL, ok)) return;
+        __nanosleep(32);
+    }
+}
+
+// one (kv head, split) item; scratch = the consumer warps' rotation scratch (>= 12.5 KB)
+__device__ void attn_part(const AttnParams& P, const unsigned long long* qkv, unsigned long long* part, int item,
+                          unsigned epoch, int warp, int lane, float* scratch) {
+    constexpr int HD = kAttnHD, G = kAttnG;
+    float* qs = scratch;                   // [G][HD]
+    float* kcur = qs + G * HD;             // [HD]
+    float* vcur = kcur + HD;               // [HD]
+    float* ps = vcur + HD;                 // [G][kAttnMaxChunk]
+    float* red = ps + G * kAttnMaxChunk;   // [G classes][G heads][HD]
+    float* stat = red + G * G * HD;        // [G][2]
+    const int t = warp * 32 + lane;
+    const int S = P.S, nh = P.nh, nkv = P.nkv;
+    const int kvh = item / S, sp = item - kvh * S;
+    const int64_t pos64 = *P.pos;
+    if (pos64 < 0 || pos64 >= P.ctx) {  // beyond the KV cache: no cache write, empty partials (output 0)
+        if (warp == 0 && lane == 0) atomicOr(P.err, 1u);
+        const unsigned long long tag = (unsigned long long)epoch << 32;
+        unsigned long long* mine = part + (int64_t)item * G * kAttnWords;
+        for (int i = t; i < G * kAttnWords; i += 32 * kChainConsumerWarps)
+            st_u64_relaxed(mine + i, tag | (i % kAttnWords == 0 ? __float_as_uint(-INFINITY) : 0u));
+        return;
+    }
+    const int pos = (int)pos64;
+    const int chunk = (pos + S) / S;  // ceil((pos + 1) / S)
+    const int lo = sp * chunk, hi = min(pos + 1, lo + chunk), n = max(0, hi - lo);
+    float* kch = P.kc + (int64_t)kvh * P.ctx * HD;
+    float* vch = P.vc + (int64_t)kvh * P.ctx * HD;
+    if (warp < G + 2) {
+        const int base = warp < G ? (kvh * G + warp) * HD : (warp == G ? nh * HD + kvh * HD : (nh + nkv) * HD + kvh * HD);
+        float v[4];  // dims lane, lane + 32, lane + 64, lane + 96
+        tagged_load4(qkv + base, epoch, lane, v);
+        if (warp <= G) {  // RoPE: pairs (i, i + 64)
+            const float c0 = __ldg(P.cosb + (int64_t)pos * (HD / 2) + lane), s0 = __ldg(P.sinb + (int64_t)pos * (HD / 2) + lane);
+            const float c1 = __ldg(P.cosb + (int64_t)pos * (HD / 2) + lane + 32),
+                        s1 = __ldg(P.sinb + (int64_t)pos * (HD / 2) + lane + 32);
+            const float a0 = v[0], b0 = v[2], a1 = v[1], b1 = v[3];
+            v[0] = a0 * c0 - b0 * s0;
+            v[2] = a0 * s0 + b0 * c0;
+            v[1] = a1 * c1 - b1 * s1;
+            v[3] = a1 * s1 + b1 * c1;
+        }
+        float* dst = warp < G ? qs + warp * HD : (warp == G ? kcur : vcur);
+        const float sc = warp < G ? rsqrtf((float)HD) : 1.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dst[lane + 32 * j] = v[j] * sc;
+        if (warp >= G && sp == 0) {  // append k / v at pos (read back by later tokens' launches)
+            float* c = warp == G ? kch : vch;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) c[(int64_t)pos * HD + lane + 32 * j] = v[j];
+        }
+    }
+    consumer_sync();
+    float qr[G][4];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) qr[g][j] = qs[g * HD + lane + 32 * j];
+#pragma unroll 2
+    for (int p = lo + warp; p < hi; p += kChainConsumerWarps) {
+        const float* kp = p == pos ? kcur : kch + (int64_t)p * HD;
+        const float k0 = kp[lane], k1 = kp[lane + 32], k2 = kp[lane + 64], k3 = kp[lane + 96];
+        float d[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) d[g] = qr[g][0] * k0 + qr[g][1] * k1 + qr[g][2] * k2 + qr[g][3] * k3;
+#pragma unroll
+        for (int o = 16; o; o >>= 1)
+#pragma unroll
+            for (int g = 0; g < G; ++g) d[g] += __shfl_xor_sync(FULL, d[g], o);
+        if (lane == 0)
+#pragma unroll
+            for (int g = 0; g < G; ++g) ps[g * kAttnMaxChunk + p - lo] = d[g];
+    }
+    consumer_sync();
+    if (warp < G) {
+        float m = -INFINITY;
+        for (int i = lane; i < n; i += 32) m = fmaxf(m, ps[warp * kAttnMaxChunk + i]);
+        for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(FULL, m, o));
+        float se = 0.f;
+        for (int i = lane; i < n; i += 32) {
+            const float e = __expf(ps[warp * kAttnMaxChunk + i] - m);
+            ps[warp * kAttnMaxChunk + i] = e;
+            se += e;
+        }
+        for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(FULL, se, o);
+        if (lane == 0) {
+            stat[warp * 2] = m;
+            stat[warp * 2 + 1] = se;
+        }
+    }
+    consumer_sync();
+    {  // P V: thread (class c, dim d) takes positions lo + c, lo + c + G, ... for all G heads
+        const int c = t >> 7, dcol = t & (HD - 1);
+        float acc[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) acc[g] = 0.f;
+#pragma unroll 4
+        for (int i = c; i < n; i += G) {
+            const int p = lo + i;
+            const float v = p == pos ? vcur[dcol] : vch[(int64_t)p * HD + dcol];
+#pragma unroll
+            for (int g = 0; g < G; ++g) acc[g] += ps[g * kAttnMaxChunk + i] * v;
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) red[(c * G + g) * HD + dcol] = acc[g];
+    }
+    consumer_sync();
+    {
+        const unsigned long long tag = (unsigned long long)epoch << 32;
+        const int g = t >> 7, dcol = t & (HD - 1);
+        float o = 0.f;
+#pragma unroll
+        for (int c = 0; c < G; ++c) o += red[(c * G + g) * HD + dcol];
+        unsigned long long* mine = part + ((int64_t)item * G + g) * kAttnWords;
+        st_u64_relaxed(mine + 2 + dcol, tag | __float_as_uint(o));
+        if (dcol == 0) {
+            st_u64_relaxed(mine, tag | __float_as_uint(stat[g * 2]));
+            st_u64_relaxed(mine + 1, tag | __float_as_uint(stat[g * 2 + 1]));
+        }
+    }
+    consumer_sync();  // the scratch is free for the next item / stage
+}
+
+// head h: combine the S (<= 32) partials of its kv head into 128 tagged outputs (threads 0..127).  The
+// loads of a poll are independent (lane j fetches split j's max and sum; every thread its weighted-V
+// words, 8 splits per round trip), so a combine costs ~S / 8 L2 round trips, not S.
+__device__ void attn_comb(const AttnParams& P, const unsigned long long* part, unsigned long long* att, int h,
+                          unsigned epoch, int t) {
+    constexpr int HD = kAttnHD, G = kAttnG, kGrp = 8;
+    const int kvh = h / G, g = h - kvh * G, S = P.S, lane = t & 31;
+    const unsigned long long* base = part + ((int64_t)kvh * S * G + g) * kAttnWords;  // split j: + j G kAttnWords
+    float mj = -INFINITY, sj = 0.f;
+    for (;;) {  // split statistics: lane j holds split j's (max, sum)
+        bool ok = true;
+        if (lane < S) {
+            const unsigned long long w0 = ld_u64_relaxed(base + (int64_t)lane * G * kAttnWords);
+            const unsigned long long w1 = ld_u64_relaxed(base + (int64_t)lane * G * kAttnWords + 1);
+            ok = (unsigned)(w0 >> 32) == epoch && (unsigned)(w1 >> 32) == epoch;
+            mj = __uint_as_float((unsigned)w0);
+            sj = __uint_as_float((unsigned)w1);
+        }
+        if (__all_sync(FULL, ok)) break;
+        __nanosleep(32);
+    }
+    float m = mj;
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(FULL, m, o));
+    const float fj = mj == -INFINITY ? 0.f : __expf(mj - m);  // lane j's split weight
+    float num = 0.f, den = 0.f;
+    for (int j0 = 0; j0 < S; j0 += kGrp) {  // fixed split order: deterministic
+        float a[kGrp];
+        for (;;) {
+            bool ok = true;
+#pragma unroll
+            for (int u = 0; u < kGrp; ++u) {
+                a[u] = 0.f;
+                if (j0 + u < S) {
+                    const unsigned long long w = ld_u64_relaxed(base + (int64_t)(j0 + u) * G * kAttnWords + 2 + t);
+                    ok &= (unsigned)(w >> 32) == epoch;
+                    a[u] = __uint_as_float((unsigned)w);
+                }
+            }
+            if (__all_sync(FULL, ok)) break;
+            __nanosleep(32);
+        }
+#pragma unroll
+        for (int u = 0; u < kGrp; ++u) {
+            const float f = __shfl_sync(FULL, fj, (j0 + u) & 31), sden = __shfl_sync(FULL, sj * fj, (j0 + u) & 31);
+            if (j0 + u < S) {
+                num += f * a[u];
+                den += sden;
+            }
+        }
+    }
+    const float o = den > 0.f ? num / den : 0.f;  // den == 0: every split empty (position out of range)
+    st_u64_relaxed(att + (int64_t)h * HD + t, ((unsigned long long)epoch << 32) | __float_as_uint(o));
+}
+
 
 // Work split of stage st for CTA cta: K-chunk ch (CTAs c with c % nch == ch), and the row
 // tiles rt = rt0, rt0 + Gc, ... (Gc CTAs per chunk); active = 0 if the CTA is idle.
@@ -270,20 +492,23 @@ struct StageSplit {
     int nch, ch, rt0, Gc, active;
 };
 
+template <bool GATED>
 struct ChainSmem {
-    ChainStage desc[kSmemStages];
-    StageSplit split[kSmemStages];
-    alignas(128) uint8_t ring[kNumSlots][kSlotBytes];
-    uint8_t rot[kChainConsumerWarps][kActSmemBlock];   // per-warp rotation scratch (own block only)
-    float part[kNumSlots][kChainConsumerWarps][16];    // per-warp row partials of a unit
-    float normsq[kChainConsumerWarps];                 // per-warp sums of squares (RMSNorm input stages)
-    uint64_t full[kNumSlots];
-    uint64_t empty[kNumSlots];
-    uint64_t parts[kNumSlots];  // 16 warps' partials of the unit in this slot are written
-    int partcnt[kNumSlots];
+    static constexpr int NSL = ChainCfg<GATED>::kSlots, NST = ChainCfg<GATED>::kStages;
+    ChainStage desc[NST];
+    StageSplit split[NST];
+    alignas(128) uint8_t ring[NSL][kSlotBytes];
+    alignas(16) uint8_t rot[kChainConsumerWarps][kActSmemBlock];  // per-warp rotation scratch (attention scratch)
+    float part[NSL][kChainConsumerWarps][16];           // per-warp row partials of a unit
+    float normsq[kChainConsumerWarps];                  // per-warp sums of squares (RMSNorm input stages)
+    uint64_t full[NSL];
+    uint64_t empty[NSL];
+    uint64_t parts[NSL];  // 16 warps' partials of the unit in this slot are written
+    int partcnt[NSL];
 };
 
-static_assert(sizeof(ChainSmem) <= 227 * 1024, "chain kernel shared memory exceeds the 227 KB per-CTA limit");
+static_assert(sizeof(ChainSmem<false>) <= 227 * 1024, "chain kernel shared memory exceeds the 227 KB per-CTA limit");
+static_assert(sizeof(ChainSmem<true>) <= 227 * 1024, "chain kernel shared memory exceeds the 227 KB per-CTA limit");
 
 __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
     unsigned v;
@@ -310,9 +535,10 @@ __device__ __forceinline__ bool compute_split(const ChainStage& st, int cta, int
 }
 // Stage s's descriptor and this CTA's split: from the smem cache (filled at kernel start, so the
 // per-stage critical path has no dependent global loads or integer divisions) or computed.
-__device__ __forceinline__ bool stage_get(const ChainSmem& sm, const ChainStage* stages, int cta, int G, int s,
+template <bool GATED>
+__device__ __forceinline__ bool stage_get(const ChainSmem<GATED>& sm, const ChainStage* stages, int cta, int G, int s,
                                           ChainStage& st, StageSplit& sp) {
-    if (s < kSmemStages) {
+    if (s < ChainSmem<GATED>::NST) {
         st = sm.desc[s];
         sp = sm.split[s];
         return sp.active;
@@ -332,7 +558,8 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                  unsigned* __restrict__ epoch_ptr, float* __restrict__ out,
                  unsigned long long* __restrict__ trace) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    ChainSmem& sm = *reinterpret_cast<ChainSmem*>(smem_raw);
+    ChainSmem<GATED>& sm = *reinterpret_cast<ChainSmem<GATED>*>(smem_raw);
+    constexpr int NSL = ChainSmem<GATED>::NSL, NST = ChainSmem<GATED>::NST;  // ring slots, cached stages
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int cta = blockIdx.x, G = gridDim.x;
     // Step epoch: tags of this launch = stored epoch + 1; every CTA checks in on epoch_ptr[1] after
@@ -341,13 +568,13 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     const unsigned epoch = *reinterpret_cast<volatile unsigned*>(epoch_ptr) + 1u;
     if (threadIdx.x == 0) atomicAdd(epoch_ptr + 1, 1u);
 
-    for (int s = tid; s < min(S, kSmemStages); s += kChainThreads) {
+    for (int s = tid; s < min(S, NST); s += kChainThreads) {
         const ChainStage st = stages[s];
         sm.desc[s] = st;
         compute_split(st, cta, G, s, sm.split[s]);
     }
     if (tid == 0) {
-        for (int i = 0; i < kNumSlots; ++i) {
+        for (int i = 0; i < NSL; ++i) {
             mbar_init(&sm.full[i], 1);
             mbar_init(&sm.empty[i], kChainConsumerWarps + 1);  // compute warps + reducer
             mbar_init(&sm.parts[i], kChainConsumerWarps);
@@ -375,8 +602,8 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             const unsigned long long tag = (unsigned long long)epoch << 32;
             for (int j = 0; j < n_units; ++j) {
                 const int useq = seq + j;
-                const int slot = useq % kNumSlots;
-                mbar_wait(&sm.parts[slot], (unsigned)(useq / kNumSlots) & 1u);
+                const int slot = useq % NSL;
+                mbar_wait(&sm.parts[slot], (unsigned)(useq / NSL) & 1u);
                 if (lane < 16) {
                     float part[kChainConsumerWarps];
 #pragma unroll
@@ -409,7 +636,27 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             for (int s = 0; s < S; ++s) {
                 ChainStage st;
                 StageSplit sp;
-                if (!stage_get(sm, stages, cta, G, s, st, sp)) continue;
+                const bool active = stage_get(sm, stages, cta, G, s, st, sp);
+                if (GATED && (st.asym & 256)) {
+                    // attention partials ahead: pull this CTA's cached K / V rows into L2 now (they do not
+                    // depend on the token), so the consumers' score and P V loads hit L2
+                    const AttnParams& P = *reinterpret_cast<const AttnParams*>(st.tiled);
+                    const int64_t pos = *P.pos;
+                    if (cta < P.nkv * P.S && pos >= 0 && pos < P.ctx) {
+                        const int kvh = cta / P.S, spl = cta - kvh * P.S;
+                        const int chunk = (int)(pos + P.S) / P.S, lo = spl * chunk;
+                        const int hi = min((int)pos, lo + chunk);  // rows before pos (pos itself is the new token)
+                        if (hi > lo) {
+                            const size_t off = ((size_t)kvh * P.ctx + lo) * kAttnHD;
+                            const unsigned bytes = (unsigned)(hi - lo) * kAttnHD * 4;
+                            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.kc + off), "r"(bytes)
+                                         : "memory");
+                            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.vc + off), "r"(bytes)
+                                         : "memory");
+                        }
+                    }
+                }
+                if (!active) continue;
                 const uint8_t* scales = st.tiled + (int64_t)st.RT * st.NB * 1024;
                 const uint8_t* zps = scales + (int64_t)st.RT * st.NB * 32;
                 const int b0 = sp.ch * kUnitBlocks;
@@ -423,7 +670,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                     bulk_g2s(dst, st.tiled + t0 * 1024, nb * 1024, &sm.full[slot]);
                     bulk_g2s(dst + kSlotCodes, scales + t0 * 32, nb * 32, &sm.full[slot]);
                     if (st.asym & 1) bulk_g2s(dst + kSlotCodes + kSlotScales, zps + t0 * 16, nb * 16, &sm.full[slot]);
-                    if (++slot == kNumSlots) {
+                    if (++slot == NSL) {
                         slot = 0;
                         phase ^= 1u;
                     }
@@ -442,12 +689,26 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     int cs = 0;        // ring slot of the CTA's next unit
     unsigned cp = 0;   // and its full-barrier phase parity
     uint8_t* rot = sm.rot[warp];
+    if (GATED) trace = nullptr;  // the decoder instantiation is not traced (registers: it sits at the cap)
     const bool prof = trace != nullptr && cta == 0;
     long long c_wait = 0, c_tile = 0, c_rot = 0, c_in = 0, c_start = clock64();
     for (int s = 0; s < S; ++s) {
         ChainStage st;
         StageSplit sp;
-        if (!stage_get(sm, stages, cta, G, s, st, sp)) continue;
+        const bool active = stage_get(sm, stages, cta, G, s, st, sp);
+        if (GATED && (st.asym & (256 | 512))) {  // decoder attention stages (no weights, no ring units)
+            const AttnParams& P = *reinterpret_cast<const AttnParams*>(st.tiled);
+            const ChainStage pv = s - 1 < NST ? sm.desc[s - 1] : stages[s - 1];
+            if (st.asym & 256) {
+                consumer_sync();  // every consumer warp is done with its rotation scratch
+                for (int item = cta; item < P.nkv * P.S; item += G)
+                    attn_part(P, pv.y, st.y, item, epoch, warp, lane, reinterpret_cast<float*>(&sm.rot[0][0]));
+            } else if (tid < kAttnHD) {
+                for (int h = cta; h < P.nh; h += G) attn_comb(P, pv.y, st.y, h, epoch, tid);
+            }
+            continue;
+        }
+        if (!active) continue;
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 0] = globaltimer();
         const int b0 = sp.ch * kUnitBlocks;
         const int nb = min(kUnitBlocks, st.NB - b0);
@@ -462,10 +723,16 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             // folded into the same launch (h + W_o att, then RMSNorm, as the reference step orders it).
             float ss = 0.f;
             if (has_block) {
+                // the residual stream: the launch input x0, or (decoder, single GPU) a tagged buffer a
+                // flag-128 stage of this launch wrote
+                if (st.npeer == 0 && st.xres)
+                    load_tagged_block<false>(st.xres + 256 * (b0 + warp), 1, 0, epoch, lane, xv);
+                else
 #pragma unroll
-                for (int e = 0; e < 8; ++e) xv[e] = __ldg(x0 + 256 * (b0 + warp) + lane + 32 * e);
-                if ((st.asym & 64) && s > 1) {  // flag 64: x0 + stage 0's output first, then the previous stage's
-                    const ChainStage s0 = sm.desc[0];
+                    for (int e = 0; e < 8; ++e) xv[e] = __ldg(x0 + 256 * (b0 + warp) + lane + 32 * e);
+                if ((st.asym & 64) && s > 1) {  // flag 64: + the o stage's output (index in bits 16-31) first
+                    const int ref = (int)((unsigned)st.asym >> 16);
+                    const ChainStage s0 = ref < NST ? sm.desc[ref] : stages[ref];
                     float pf[8];
                     load_tagged_block<false>(s0.y + 256 * (b0 + warp), (s0.NB + kUnitBlocks - 1) / kUnitBlocks,
                                              s0.yrows, epoch, lane, pf);
@@ -473,16 +740,18 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                     for (int e = 0; e < 8; ++e) xv[e] += pf[e];
                 }
                 if ((st.asym & (16 | 64)) && s > 0) {
-                    const ChainStage pv = s - 1 < kSmemStages ? sm.desc[s - 1] : stages[s - 1];
+                    const ChainStage pv = s - 1 < NST ? sm.desc[s - 1] : stages[s - 1];
                     const int pn = (pv.NB + kUnitBlocks - 1) / kUnitBlocks;
                     float pf[8];
                     load_tagged_block<false>(pv.y + 256 * (b0 + warp), pn, pv.yrows, epoch, lane, pf);
 #pragma unroll
                     for (int e = 0; e < 8; ++e) xv[e] += pf[e];
                 }
-                if ((st.asym & 128) && sp.rt0 == 0)  // one CTA publishes the updated residual stream
+                if ((st.asym & 128) && sp.rt0 == 0)  // one CTA publishes the updated residual stream (tagged)
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) st.xout[256 * (b0 + warp) + lane + 32 * e] = xv[e];
+                    for (int e = 0; e < 8; ++e)
+                        st_u64_relaxed(st.xout + 256 * (b0 + warp) + lane + 32 * e,
+                                       ((unsigned long long)epoch << 32) | __float_as_uint(xv[e]));
 #pragma unroll
                 for (int e = 0; e < 8; ++e) ss += xv[e] * xv[e];
             }
@@ -508,7 +777,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 #pragma unroll
                 for (int e = 0; e < 8; ++e) f[e] = __ldg(xs + 256 * (b0 + warp) + lane + 32 * e);
             } else {
-                const ChainStage pv = s - 1 < kSmemStages ? sm.desc[s - 1] : stages[s - 1];
+                const ChainStage pv = s - 1 < NST ? sm.desc[s - 1] : stages[s - 1];
                 const int pn = (pv.NB + kUnitBlocks - 1) / kUnitBlocks;
                 const unsigned long long* src = pv.y + 256 * (b0 + warp);
                 if (pv.npeer == 0) {
@@ -545,10 +814,10 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         if (prof) c_rot += clock64() - c0;
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 2] = globaltimer();
         const int n_units = (st.RT - 1 - sp.rt0) / sp.Gc + 1;
-        for (int u0 = 0; u0 < n_units; u0 += kNumSlots) {
-            // rounds of at most kNumSlots units: no warp waits a ring slot more than one phase ahead
+        for (int u0 = 0; u0 < n_units; u0 += NSL) {
+            // rounds of at most NSL units: no warp waits a ring slot more than one phase ahead
             if (u0 > 0) consumer_sync();
-            const int u1 = min(n_units, u0 + kNumSlots);
+            const int u1 = min(n_units, u0 + NSL);
             // two units per iteration: their independent dependency chains interleave in the
             // warp's in-order issue stream (software pipelining across ring slots)
             for (int j = u0; j < u1; j += 2) {
@@ -556,10 +825,10 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                 // ring position of the two units, advanced incrementally (no division by the ring size)
                 const int slot0 = cs;
                 const unsigned ph0 = cp;
-                if (++cs == kNumSlots) cs = 0, cp ^= 1u;
+                if (++cs == NSL) cs = 0, cp ^= 1u;
                 const int slot1 = cs;
                 const unsigned ph1 = cp;
-                if (two && ++cs == kNumSlots) cs = 0, cp ^= 1u;
+                if (two && ++cs == NSL) cs = 0, cp ^= 1u;
                 long long c1 = prof ? clock64() : 0;
                 mbar_wait(&sm.full[slot0], ph0);
                 if (two) mbar_wait(&sm.full[slot1], ph1);
@@ -639,9 +908,22 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         if (GATED && (last.asym & 8)) {
             // residual accumulation (decoder): out is the residual stream.  Flag 32: stage 0's output
             // (an o projection in the same launch) is added first: out = (out + y_0) + y_last.
-            float base = out[r];
+            float base;
+            if (last.npeer == 0 && last.xres) {  // the residual is a tagged buffer of this launch
+                for (;;) {
+                    const unsigned long long w = ld_u64_relaxed(last.xres + r);
+                    if ((unsigned)(w >> 32) == epoch) {
+                        base = __uint_as_float((unsigned)w);
+                        break;
+                    }
+                    __nanosleep(64);
+                }
+            } else {
+                base = x0[r];  // the launch input is the residual (in place when out == x0)
+            }
             if (last.asym & 32) {
-                const ChainStage s0 = sm.desc[0];
+                const int ref = (int)((unsigned)last.asym >> 16);
+                const ChainStage s0 = ref < NST ? sm.desc[ref] : stages[ref];
                 const int n0 = (s0.NB + kUnitBlocks - 1) / kUnitBlocks;
                 float v0;
                 for (;;) {
@@ -677,14 +959,47 @@ using namespace itq3;
 
 extern "C" int64_t itq3_chain_desc_nbytes(void) { return (int64_t)sizeof(ChainStage); }
 extern "C" int itq3_chain_act_block_bytes(int limbs) { return act_block_bytes(limbs); }
-extern "C" int itq3_chain_smem_bytes(void) { return (int)sizeof(ChainSmem); }
+extern "C" int itq3_chain_smem_bytes(void) { return (int)sizeof(ChainSmem<false>); }
 
 extern "C" int itq3_chain_write_desc_tp(void*, int, const uint8_t*, void*, int64_t, int64_t, int, int64_t, int64_t,
                                         const void*, int);
 
 // flag 128 (decoder): where the RMSNorm stage `index` writes the residual input it computed
-extern "C" int itq3_chain_set_xout(void* host_desc, int index, float* xout) {
-    reinterpret_cast<ChainStage*>(host_desc)[index].xout = xout;
+extern "C" int itq3_chain_set_xout(void* host_desc, int index, void* xout) {
+    reinterpret_cast<ChainStage*>(host_desc)[index].xout = (unsigned long long*)xout;
+    return ITQ3_OK;
+}
+// decoder attention stage (flags 256 = partials, 512 = combine): `params` = device AttnParams, `y` = the
+// stage's tagged output (partials: nkv x S x 4 x 130 words; combine: n_heads x 128 words)
+extern "C" int itq3_chain_write_desc_attn(void* host_desc, int index, int kind, const void* params, void* y,
+                                          int64_t yrows) {
+    if ((kind != 256 && kind != 512) || index < 1 || params == nullptr) {
+        set_error("chain: stage %d: attention stage needs kind 256 / 512, a previous stage and params", index);
+        return ITQ3_E_DOMAIN;
+    }
+    ChainStage& st = reinterpret_cast<ChainStage*>(host_desc)[index];
+    memset(&st, 0, sizeof(st));
+    st.tiled = (const uint8_t*)params;
+    st.y = (unsigned long long*)y;
+    st.rows = yrows;
+    st.cols = 0;
+    st.NB = 1;  // a consumer of this stage's output reads one partial
+    st.RT = 0;  // no weight units: producer and reducer skip the stage
+    st.asym = kind;
+    st.yrows = (int32_t)yrows;
+    return ITQ3_OK;
+}
+extern "C" int itq3_chain_attn_params_nbytes(void) { return (int)sizeof(AttnParams); }
+
+// decoder, single GPU: the tagged residual buffer a flag-4/8 stage reads instead of the launch input
+// (written by a flag-128 stage of the same launch)
+extern "C" int itq3_chain_set_xres(void* host_desc, int index, const void* xres) {
+    ChainStage& st = reinterpret_cast<ChainStage*>(host_desc)[index];
+    if (st.npeer) {
+        set_error("chain: stage %d: a residual buffer needs a single-GPU stage", index);
+        return ITQ3_E_DOMAIN;
+    }
+    st.xres = (const unsigned long long*)xres;
     return ITQ3_OK;
 }
 
@@ -745,7 +1060,7 @@ static int chain_run(const void* d_desc, int n_stages, const float* x0, int limb
         return ITQ3_E_DOMAIN;
     }
     static std::atomic<unsigned long long> smem_attr{0};
-    const int smem = (int)sizeof(ChainSmem);
+    const int smem = (int)sizeof(ChainSmem<GATED>);
     if (int rc = ensure_smem_attr(chain_kernel<GATED>, smem, smem_attr, "chain: smem attribute")) return rc;
     if (grid <= 0) grid = device_sms();
     cudaLaunchConfig_t cfg = {};

@@ -4,16 +4,15 @@ batch-1 decode tokens/s metric.  None of it exists in the reference; it only fra
 
 Per layer and token: [residual +] RMSNorm -> qkv GEMV -> RoPE + KV-cache append + grouped-query
 attention over the cache -> o GEMV -> residual + RMSNorm -> gate_up GEMV -> SiLU(gate) * up -> down
-GEMV.  Everything but the attention runs inside chain launches (csrc/chain.cu, decoder flags): the
-RMSNorm in the loads of the qkv / gate_up stages (every CTA of a 4096-column stage holds the whole
-input), the SiLU gating in the loads of the down stage, the residual adds in the final folds; the
-attention (RoPE + KV append + split decode attention) is one glue kernel (csrc/decoder_glue.cu).
-A layer is 2 launches: attention, then ONE chain [o -> RMSNorm(x + o) -> gate_up -> SiLU gating -> down
--> RMSNorm((x + o) + down) -> next layer's qkv] whose last stage also writes the new residual stream
-(ping-pong buffers); the last layer's chain ends in the lm_head.  Plus one [RMSNorm -> qkv] launch for
-layer 0: 2 x layers + 1 launches per token.  A whole token step is ONE CUDA
-graph: the position lives in a device tensor that the graph itself advances, the attention reads
-the full cache under a position mask, so replays need no host work.
+GEMV.  The WHOLE token is ONE persistent chain launch (csrc/chain.cu, decoder flags): per layer the
+stages [attention partials, attention combine, o, gate_up, down, next qkv] -- the RMSNorm in the loads
+of the qkv / gate_up stages (every CTA of a 4096-column stage holds the whole input), the SiLU gating
+in the loads of the down stage, the residual stream as tagged buffers written by each layer's last
+stage (the residual adds folded into the norm inputs); the attention stages read q / k / v from the
+qkv stage's tagged outputs (RoPE, KV append, grouped-query attention over 18 position splits per kv
+head, then a per-head combine); the last layer ends in the lm_head.  A token step is one CUDA graph
+of that one launch: the position lives in a device tensor that the graph itself advances, so replays
+need no host work.
 """
 
 from __future__ import annotations
@@ -28,16 +27,17 @@ LLAMA3_8B = dict(hidden=4096, inter=14336, n_heads=32, n_kv=8, head_dim=128, rop
 
 
 class _Chain:
-    """A short chain of ITQ3_S stages run as ONE cooperative launch (csrc/chain.cu, decoder flags):
-    stages = [(QuantizedTensor, flags, xin)], flags bit 1 = gated input (SiLU(gate) * up of the
-    previous stage), bit 2 = RMSNorm input with gain `xin`, bit 3 = the fold adds into `out` (the
-    residual stream) instead of overwriting it, bit 4 = the RMSNorm input is x0 + the previous
-    stage's output (residual after an o projection in the same launch), bit 5 = the fold adds stage
-    0's output first, bit 6 = the RMSNorm input is (x0 + stage 0's output) + the previous stage's
-    output (the residual after a whole layer), bit 7 = that stage also writes the residual it formed
-    to `xout`.  A stage-0 `xin` without flag 2 is that stage's input vector."""
+    """ONE cooperative launch of the chain kernel (csrc/chain.cu, GATED instantiation) over a list of
+    stages, each a dict: {"q": QuantizedTensor, "flags", "xin", "xres", "xout", "ref"} for an ITQ3_S
+    GEMV stage, or {"attn": 256 | 512, "params": device AttnParams, "y": tagged output} for an
+    attention stage.  Flags: bit 1 gated input (SiLU(gate) * up of the previous stage), bit 2 RMSNorm
+    input with gain `xin`, bit 3 the final fold adds the residual, bit 4 the norm input is residual +
+    the previous stage's output, bit 5 the fold adds the `ref` stage's output first, bit 6 the norm
+    input is (residual + the `ref` stage's output) + the previous stage's output, bit 7 the stage
+    also writes the residual it formed (tagged) to `xout`.  The residual is `xres` (a tagged buffer
+    written earlier in the launch) or, when None, the launch input x0."""
 
-    def __init__(self, stages, out: torch.Tensor, dev, xout: torch.Tensor | None = None):
+    def __init__(self, stages, out: torch.Tensor, dev):
         import ctypes
 
         from . import _lib
@@ -46,16 +46,26 @@ class _Chain:
         lib = _lib.load()
         host = ctypes.create_string_buffer(lib.itq3_chain_desc_nbytes() * len(stages))
         self.y, self.keep = [], []
-        for i, (q, flags, gain) in enumerate(stages):
+        for i, st in enumerate(stages):
+            if "attn" in st:
+                self.keep.append(st["params"])
+                self.y.append(st["y"])
+                _lib.check(lib.itq3_chain_write_desc_attn(host, i, st["attn"], _lib.ptr(st["params"]),
+                                                          _lib.ptr(st["y"]), st["y"].numel()))
+                continue
+            q, flags, xin = st["q"], st.get("flags", 0), st.get("xin")
             y = torch.zeros((-(-q.cols // 4096), q.rows), dtype=torch.int64, device=dev)  # tagged outputs
             self.y.append(y)
-            self.keep.append(gain)
+            self.keep.append(xin)
             _lib.check(lib.itq3_chain_write_desc(host, i, _lib.ptr(q.tiled()), _lib.ptr(y),
-                                                 _lib.ptr(gain) if gain is not None else None, q.rows, q.cols,
-                                                 int(not q.symmetric) | flags, 0))
+                                                 _lib.ptr(xin) if xin is not None else None, q.rows, q.cols,
+                                                 int(not q.symmetric) | flags | (st.get("ref", 0) << 16), 0))
+            if st.get("xres") is not None:
+                _lib.check(lib.itq3_chain_set_xres(host, i, _lib.ptr(st["xres"])))
+                self.keep.append(st["xres"])
             if flags & XOUT:
-                _lib.check(lib.itq3_chain_set_xout(host, i, _lib.ptr(xout)))
-                self.keep.append(xout)
+                _lib.check(lib.itq3_chain_set_xout(host, i, _lib.ptr(st["xout"])))
+                self.keep.append(st["xout"])
         self.n = len(stages)
         self.desc = torch.frombuffer(bytearray(host.raw), dtype=torch.uint8).to(dev)
         self.epoch = torch.zeros(2, dtype=torch.int32, device=dev)
@@ -124,31 +134,52 @@ class DecoderStack:
         self.att = torch.zeros(self.h, device=self.dev)         # attention output (nh * hd)
         from . import _lib
 
-        self.attn_ws = torch.zeros(_lib.load().itq3_glue_attention_ws_nbytes(self.nh), dtype=torch.uint8,
-                                   device=self.dev)  # split partials + per-head counters
         if self.hd != 128 or max_ctx > 1024 or self.nh * self.hd != self.h:
-            raise ValueError("DecoderStack: the glue kernels need head_dim 128, max_ctx <= 1024, nh * hd = hidden")
-        # launch 0: [RMSNorm -> qkv_0]; layer L: attention, then [o -> RMSNorm(x + o) -> gate_up -> SiLU gating
-        # -> down -> RMSNorm(x + o + down) -> qkv_{L+1} (or the lm_head)], the residual ping-ponging between
-        # self.xs2[L % 2] (read) and self.xs2[(L + 1) % 2] (written by the last stage)
-        self.qkv_out = torch.zeros(self.h + 2 * kv, device=self.dev)
-        self.xs2 = [torch.zeros(self.h, device=self.dev), torch.zeros(self.h, device=self.dev)]
-        self.first = _Chain([(self.q[0][0], NORM_IN, self.gain[0][0])], self.qkv_out, self.dev)
-        self.chains = []
+            raise ValueError("DecoderStack: the attention stages need head_dim 128, max_ctx <= 1024, nh * hd = hidden")
+        # ONE launch per token: qkv_0, then per layer [attention partials, attention combine, o, gate_up,
+        # down, next qkv / lm_head]; the residual after layer L lives in the tagged buffer res[L + 1]
+        import struct
+
+        G = self.nh // self.nkv
+        if G != 4:
+            raise ValueError("DecoderStack: the in-chain attention needs 4 query heads per kv head")
+        sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
+        self.splits = max(1, min(32, sms // self.nkv))  # attention items (kv head, split), <= 32 splits
+        if -(-max_ctx // self.splits) > 64:  # positions per split (the chain's score scratch)
+            raise ValueError("DecoderStack: ceil(max_ctx / attention splits) must be <= 64")
+        self.res = [None] + [torch.zeros(self.h, dtype=torch.int64, device=self.dev) for _ in range(layers)]
+        self.att_y = [torch.zeros(self.h, dtype=torch.int64, device=self.dev) for _ in range(layers)]
+        self.part_y = [torch.zeros(self.nkv * self.splits * 4 * 130, dtype=torch.int64, device=self.dev)
+                       for _ in range(layers)]
+        self.attn_params = []
+        self.attn_err = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        for li in range(layers):
+            raw = struct.pack("<QQQQQQiiii", self.k_cache[li, 0].data_ptr(), self.v_cache[li, 0].data_ptr(),
+                              self.cos.data_ptr(), self.sin.data_ptr(), self.pos.data_ptr(),
+                              self.attn_err.data_ptr(), self.nh, self.nkv, max_ctx, self.splits)
+            assert len(raw) == _lib.load().itq3_chain_attn_params_nbytes()
+            self.attn_params.append(torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(self.dev))
+        stages = [dict(q=self.q[0][0], flags=NORM_IN, xin=self.gain[0][0])]
         for li, (_, o_w, gu_w, down_w) in enumerate(self.q):
-            mlp = [(o_w, 0, self.att), (gu_w, NORM_IN | RESID_IN, self.gain[li][1])]
+            stages.append(dict(attn=256, params=self.attn_params[li], y=self.part_y[li]))
+            stages.append(dict(attn=512, params=self.attn_params[li], y=self.att_y[li]))
+            o_idx = len(stages)
+            stages.append(dict(q=o_w))
+            stages.append(dict(q=gu_w, flags=NORM_IN | RESID_IN, xin=self.gain[li][1], xres=self.res[li]))
             if li + 1 < layers:
-                nxt, out = (self.q[li + 1][0], NORM_IN | RESID2_IN | XOUT, self.gain[li + 1][0]), self.qkv_out
+                nxt = dict(q=self.q[li + 1][0], xin=self.gain[li + 1][0])
             elif self.lm_head is not None:
-                nxt, out = (self.lm_head, NORM_IN | RESID2_IN | XOUT, self.final_gain), self.logits
+                nxt = dict(q=self.lm_head, xin=self.final_gain)
             else:
-                nxt, out = None, self.xs2[li % 2]
-            if nxt is None:  # last layer without a head: fold x += o + down in place
-                stages = mlp + [(down_w, GATED | ADD_OUT | ADD_OUT0, None)]
+                nxt = None
+            if nxt is None:  # the last layer without a head folds x + o + down into `out`
+                stages.append(dict(q=down_w, flags=GATED | ADD_OUT | ADD_OUT0, ref=o_idx, xres=self.res[li]))
             else:
-                stages = mlp + [(down_w, GATED, None), nxt]
-            self.chains.append(_Chain(stages, out, self.dev, xout=self.xs2[(li + 1) % 2]))
-        self.final_xs = self.xs2[layers % 2] if self.lm_head is not None else self.xs2[(layers - 1) % 2]
+                stages.append(dict(q=down_w, flags=GATED))
+                nxt.update(flags=NORM_IN | RESID2_IN | XOUT, ref=o_idx, xres=self.res[li], xout=self.res[li + 1])
+                stages.append(nxt)
+        self.n_stages = len(stages)
+        self.token_chain = _Chain(stages, self.logits if self.lm_head is not None else self.out, self.dev)
         self.graph = None
 
     def weight_bytes(self) -> int:
@@ -159,7 +190,7 @@ class DecoderStack:
         return n
 
     def launches_per_step(self) -> int:
-        return 2 * self.layers + 1
+        return 1
 
     def _rms(self, x, gain):
         return torch.nn.functional.rms_norm(x, (self.h,), weight=gain, eps=self.eps)
@@ -169,21 +200,14 @@ class DecoderStack:
         return torch.cat((a * cos - b * sin, a * sin + b * cos), dim=1)
 
     def _step(self) -> None:
-        """One token: the layer-0 [RMSNorm -> qkv] chain, then per layer one glue launch (RoPE + KV append +
-        split attention) and one chain [o -> ... -> down -> next qkv / lm_head]."""
+        """One token: ONE chain launch over all layers (attention stages included), then the position
+        advance (a device op, so the graphed step needs no host work)."""
         from . import _lib
 
-        st = _lib.stream_ptr(self.dev)
-        self.xs2[0].copy_(self.x)
-        self.first(self.xs2[0], st)  # qkv_0 = W_qkv RMSNorm(x)
-        for li in range(self.layers):
-            _lib.call("itq3_glue_rope_attention", _lib.ptr(self.qkv_out), _lib.ptr(self.cos), _lib.ptr(self.sin),
-                      _lib.ptr(self.pos), _lib.ptr(self.k_cache[li, 0]), _lib.ptr(self.v_cache[li, 0]),
-                      _lib.ptr(self.att), self.nh, self.nkv, self.hd, self.max_ctx, _lib.ptr(self.attn_ws), st)
-            # h = x + W_o att; x' = h + W_down (SiLU(gate) * up)(RMSNorm(h)); qkv_{L+1} = W_qkv RMSNorm(x')
-            # (the last layer: logits = W_head RMSNorm(x'))
-            self.chains[li](self.xs2[li % 2], st)
-        self.out.copy_(self.final_xs)
+        self.token_chain(self.x, _lib.stream_ptr(self.dev))
+        if self.lm_head is not None:  # the final residual stream: low halves of the tagged words
+            self.out.copy_(self.res[self.layers].view(torch.int32)[0::2].view(torch.float32))
+
         self.pos.add_(1)
 
     def capture(self) -> None:
@@ -217,7 +241,7 @@ class DecoderStack:
     def step(self, x: torch.Tensor | None = None) -> torch.Tensor:
         """Decode one token: hidden state in (device, len hidden), hidden state out; advances the position.
         Raises once the KV cache is full (the glue kernel also refuses positions >= max_ctx on the
-        device and writes no cache entry: its error word, attn_ws's last u32, is set)."""
+        device and writes no cache entry: its error word, `device_error()`, is set)."""
         if x is not None:
             self.x.copy_(x)
         if self.graph is None:
@@ -226,8 +250,8 @@ class DecoderStack:
         return self.out
 
     def device_error(self) -> int:
-        """The glue kernel's out-of-cache flag (non-zero after a replay at a position >= max_ctx)."""
-        return int(self.attn_ws.view(torch.int32)[-1].item())
+        """The attention stages' out-of-cache flag (non-zero after a replay at a position >= max_ctx)."""
+        return int(self.attn_err.item())
 
     def reference_step(self, x: torch.Tensor, pos: int, k_hist: list, v_hist: list) -> torch.Tensor:  # noqa: C901
         """The same token step in plain torch fp32 with dequantised weights (numerics test only)."""

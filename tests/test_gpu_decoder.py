@@ -10,7 +10,7 @@ pytestmark = pytest.mark.gpu
 P = pytest.importorskip("paper_2603_27914_b200")
 from paper_2603_27914_b200.decoder import DecoderStack  # noqa: E402
 
-SMALL = dict(hidden=512, inter=1024, n_heads=4, n_kv=2, head_dim=128, rope_theta=10000.0, vocab=2000)
+SMALL = dict(hidden=512, inter=1024, n_heads=4, n_kv=1, head_dim=128, rope_theta=10000.0, vocab=2000)
 
 
 def test_decoder_steps_match_fp32_reference():
