@@ -551,7 +551,9 @@ __device__ __forceinline__ bool stage_get(const ChainSmem<GATED>& sm, const Chai
 //   0 stage entered, 1 input observed ready, 2 input rotated, 3 own units done
 // 18 warps: the per-SMSP register file (16K) caps a 5-warp SMSP at 96 registers/thread
 
-template <bool GATED>  // GATED: some stage reads SiLU(gate) * up (a separate instantiation keeps the
+template <bool GATED, bool TRACE = false>  // TRACE: globaltimer stamps + cycle counters (tools/trace_chain.py)
+                      // in their own instantiation, so the measured kernels carry no counter registers.
+                      // GATED: some stage reads SiLU(gate) * up (a separate instantiation keeps the
                       // plain kernel's register allocation)
 __global__ void __launch_bounds__(kChainThreads, 1)
     chain_kernel(const ChainStage* __restrict__ stages, int S, const float* __restrict__ x0, int L,
@@ -689,7 +691,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     int cs = 0;        // ring slot of the CTA's next unit
     unsigned cp = 0;   // and its full-barrier phase parity
     uint8_t* rot = sm.rot[warp];
-    if (GATED) trace = nullptr;  // the decoder instantiation is not traced (registers: it sits at the cap)
+    if (!TRACE) trace = nullptr;
     const bool prof = trace != nullptr && cta == 0;
     long long c_wait = 0, c_tile = 0, c_rot = 0, c_in = 0, c_start = clock64();
     for (int s = 0; s < S; ++s) {
@@ -1059,9 +1061,11 @@ static int chain_run(const void* d_desc, int n_stages, const float* x0, int limb
         set_error("chain: limbs must be in [1, %d]", kMaxLimbs);
         return ITQ3_E_DOMAIN;
     }
-    static std::atomic<unsigned long long> smem_attr{0};
+    static std::atomic<unsigned long long> smem_attr{0}, smem_attr_tr{0};
     const int smem = (int)sizeof(ChainSmem<GATED>);
     if (int rc = ensure_smem_attr(chain_kernel<GATED>, smem, smem_attr, "chain: smem attribute")) return rc;
+    if (!GATED && d_trace)
+        if (int rc = ensure_smem_attr(chain_kernel<false, true>, smem, smem_attr_tr, "chain: smem attribute")) return rc;
     if (grid <= 0) grid = device_sms();
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
@@ -1073,7 +1077,8 @@ static int chain_run(const void* d_desc, int n_stages, const float* x0, int limb
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, chain_kernel<GATED>, (const ChainStage*)d_desc, n_stages, x0, limbs,
+    auto kern = (!GATED && d_trace) ? chain_kernel<false, true> : chain_kernel<GATED>;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, (const ChainStage*)d_desc, n_stages, x0, limbs,
                                              d_epoch, out, (unsigned long long*)d_trace);
     if (e != cudaSuccess) {
         set_error("chain: launch failed: %s", cudaGetErrorString(e));
