@@ -17,6 +17,7 @@
 // Co-residency of all CTAs (required by the spin waits) is guaranteed by a cooperative
 // launch sized to one CTA per SM.
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -238,30 +239,31 @@ __device__ void chain_rotate_to_smem(const float (&fin)[8], int L, uint8_t* img,
 
 // One 16-row x 256-k tile of the warp's block from a ring slot: returns the (row g, row g+8)
 // contributions of this lane's limb-pair columns (before the quad combine).
+template <bool ASYM>  // asymmetric zero-points: a separate instantiation, so symmetric tiles skip the zp terms
 __device__ __forceinline__ float2 chain_tile(const uint8_t* ring, int warp, int lane, int g, const uint2 (&bf)[8],
-                                             float fcx, float corr, int asym) {
+                                             float fcx, float corr) {
     const uint4 wa0 = reinterpret_cast<const uint4*>(ring + warp * 1024)[lane];
     const uint4 wa1 = reinterpret_cast<const uint4*>(ring + warp * 1024 + 512)[lane];
     const uint32_t sc = reinterpret_cast<const uint32_t*>(ring + kSlotCodes + warp * 32)[g];
-    int C0[4] = {0, 0, 0, 0}, C1[4] = {0, 0, 0, 0};  // group 0 / group 1 (two 4-deep chains)
+    // ONE accumulator for both k groups (an 8-deep IMMA chain; the two units of an iteration and the
+    // warps of the SMSP give the tensor pipe enough independent chains), so no group merge afterwards
+    int C[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const uint32_t mk = i == 3 ? 0xffffffffu : (0x04040404u << (2 * i)) - 0x01010101u;  // cumulative
-        mma_u8s8_c(C0, wa0.x & mk, wa0.y & mk, wa0.z & mk, wa0.w & mk, bf[i].x, bf[i].y);
-        mma_u8s8_c(C1, wa1.x & mk, wa1.y & mk, wa1.z & mk, wa1.w & mk, bf[4 + i].x, bf[4 + i].y);
+        mma_u8s8_c(C, wa0.x & mk, wa0.y & mk, wa0.z & mk, wa0.w & mk, bf[i].x, bf[i].y);
+        mma_u8s8_c(C, wa1.x & mk, wa1.y & mk, wa1.z & mk, wa1.w & mk, bf[4 + i].x, bf[4 + i].y);
     }
-    // columns 2t, 2t+1 = limbs 2t, 2t+1 (factors differ by 256); |C| < 2^22, so the pair
-    // combination stays below 2^31
-    const float v0 = (float)((C0[0] + C1[0]) + 256 * (C0[1] + C1[1]));
-    const float v1 = (float)((C0[2] + C1[2]) + 256 * (C0[3] + C1[3]));
+    // columns 2t, 2t+1 = limbs 2t, 2t+1 (factors differ by 256); |C| <= 8 x 32 x 170 x 128 < 2^23, so
+    // the pair combination stays below 2^31
+    const float v0 = (float)(C[0] + 256 * C[1]);
+    const float v1 = (float)(C[2] + 256 * C[3]);
     const float d0 = f16_bits_to_f32((uint16_t)(sc & 0xffffu));
     const float d1 = f16_bits_to_f32((uint16_t)(sc >> 16));
-    float zf0 = 1.f, zf1 = 1.f;
-    if (asym) {
-        const uint16_t zz = reinterpret_cast<const uint16_t*>(ring + kSlotCodes + kSlotScales + warp * 16)[g];
-        zf0 = (float)(1 + (int)(int8_t)(zz & 0xff));
-        zf1 = (float)(1 + (int)(int8_t)(zz >> 8));
-    }
+    if (!ASYM) return make_float2(d0 * (fcx * v0 - corr), d1 * (fcx * v1 - corr));
+    const uint16_t zz = reinterpret_cast<const uint16_t*>(ring + kSlotCodes + kSlotScales + warp * 16)[g];
+    const float zf0 = (float)(1 + (int)(int8_t)(zz & 0xff));
+    const float zf1 = (float)(1 + (int)(int8_t)(zz >> 8));
     return make_float2(d0 * (fcx * v0 - zf0 * corr), d1 * (fcx * v1 - zf1 * corr));
 }
 
@@ -816,6 +818,9 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         if (prof) c_rot += clock64() - c0;
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 2] = globaltimer();
         const int n_units = (st.RT - 1 - sp.rt0) / sp.Gc + 1;
+        // the stage's units, with the zero-point terms compiled in only for asymmetric stages
+        auto units = [&](auto asym_tag) {
+        constexpr bool ASYM = decltype(asym_tag)::value;
         for (int u0 = 0; u0 < n_units; u0 += NSL) {
             // rounds of at most NSL units: no warp waits a ring slot more than one phase ahead
             if (u0 > 0) consumer_sync();
@@ -845,8 +850,8 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 #else
                 if (has_block) {
 #endif
-                    ra = chain_tile(sm.ring[slot0], warp, lane, g, bf, fcx, corr, st.asym & 1);
-                    if (two) rb = chain_tile(sm.ring[slot1], warp, lane, g, bf, fcx, corr, st.asym & 1);
+                    ra = chain_tile<ASYM>(sm.ring[slot0], warp, lane, g, bf, fcx, corr);
+                    if (two) rb = chain_tile<ASYM>(sm.ring[slot1], warp, lane, g, bf, fcx, corr);
                     // combine the quad's limb-pair columns (lanes t = 0..3, fixed order)
                     ra.x += __shfl_xor_sync(FULL, ra.x, 1);
                     ra.y += __shfl_xor_sync(FULL, ra.y, 1);
@@ -876,6 +881,11 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                 }
             }
         }
+        };
+        if (st.asym & 1)
+            units(std::true_type{});
+        else
+            units(std::false_type{});
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 3] = globaltimer();
     }
     if (prof && lane == 0) {
