@@ -23,6 +23,10 @@
 
 namespace itq3 {
 
+#ifndef CHAIN_PF_UNITS  // L2 prefetch distance of the producer, in units beyond the ring (0: off)
+#define CHAIN_PF_UNITS 4
+#endif
+
 constexpr int kChainConsumerWarps = 16;
 constexpr int kChainThreads = 32 * (kChainConsumerWarps + 2);  // + producer warp + reducer warp
 constexpr int kProducerWarp = kChainConsumerWarps, kReducerWarp = kChainConsumerWarps + 1;
@@ -174,7 +178,8 @@ __device__ void chain_rotate_to_smem(const float (&fin)[8], int L, uint8_t* img,
     const float sc_in = pow2f(-e_in);
     int v[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = __float2int_rn(f[e] * sc_in);
+    for (int e = 0; e < 8; ++e)  // |f sc_in| < 2^22, sc_in a power of two: one FMA rounds to nearest even
+        v[e] = __float_as_int(fmaf(f[e], sc_in, 12582912.0f)) - 0x4B400000;
 #pragma unroll
     for (int h = 1; h < 32; h <<= 1) {
         const bool high = (lane & h) != 0;
@@ -637,6 +642,49 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         if (lane == 0) {
             int slot = 0;
             unsigned phase = 0;
+#if CHAIN_PF_UNITS > 0
+            // L2 prefetch cursor, CHAIN_PF_UNITS units ahead of the ring cursor (across stages): HBM keeps
+            // streaming into L2 while the ring is full and the consumers sit at a stage boundary, and the
+            // ring refills from L2 after it.  Measured on the Llama-2-7B stack (tools/ab_run.sh): 0.562 ->
+            // 0.528 ms per token at 4 units (+ scales); 1-16 units within 2%, 32 units (~100 MB in
+            // flight) thrashes L2 (0.669 ms).
+            int pf_s = 0, pf_rt = -1;
+            ChainStage pf_st;
+            StageSplit pf_sp;
+            bool pf_done = false;
+            auto pf_next = [&]() {  // advance to the next unit of this CTA and prefetch it
+                for (;;) {
+                    if (pf_rt >= 0) {
+                        pf_rt += pf_sp.Gc;
+                        if (pf_rt < pf_st.RT) break;
+                        ++pf_s;
+                    }
+                    if (pf_s >= S) {
+                        pf_done = true;
+                        return;
+                    }
+                    if (stage_get(sm, stages, cta, G, pf_s, pf_st, pf_sp) && pf_st.RT > 0 && !(pf_st.asym & (256 | 512))) {
+                        pf_rt = pf_sp.rt0;
+                        break;
+                    }
+                    pf_rt = -1;
+                    ++pf_s;
+                }
+                const int b0 = pf_sp.ch * kUnitBlocks;
+                const int nb = min(kUnitBlocks, pf_st.NB - b0);
+                const int64_t t0 = (int64_t)pf_rt * pf_st.NB + b0;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf_st.tiled + t0 * 1024),
+                             "r"(nb * 1024) : "memory");
+                const uint8_t* pf_sc = pf_st.tiled + (int64_t)pf_st.RT * pf_st.NB * 1024;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf_sc + t0 * 32), "r"(nb * 32)
+                             : "memory");
+                if (pf_st.asym & 1)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf_sc + (int64_t)pf_st.RT * pf_st.NB * 32 +
+                                                                                    t0 * 16),
+                                 "r"(nb * 16) : "memory");
+            };
+            for (int i = 0; i < CHAIN_PF_UNITS && !pf_done; ++i) pf_next();
+#endif
             for (int s = 0; s < S; ++s) {
                 ChainStage st;
                 StageSplit sp;
@@ -674,6 +722,9 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                     bulk_g2s(dst, st.tiled + t0 * 1024, nb * 1024, &sm.full[slot]);
                     bulk_g2s(dst + kSlotCodes, scales + t0 * 32, nb * 32, &sm.full[slot]);
                     if (st.asym & 1) bulk_g2s(dst + kSlotCodes + kSlotScales, zps + t0 * 16, nb * 16, &sm.full[slot]);
+#if CHAIN_PF_UNITS > 0
+                    if (!pf_done) pf_next();
+#endif
                     if (++slot == NSL) {
                         slot = 0;
                         phase ^= 1u;
@@ -852,22 +903,21 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 #endif
                     ra = chain_tile<ASYM>(sm.ring[slot0], warp, lane, g, bf, fcx, corr);
                     if (two) rb = chain_tile<ASYM>(sm.ring[slot1], warp, lane, g, bf, fcx, corr);
-                    // combine the quad's limb-pair columns (lanes t = 0..3, fixed order)
+                    // combine the quad's limb-pair columns: lanes t = 0, 1 hold columns 0..3 (the four
+                    // limbs); t = 2, 3 hold the zero columns 4..7 and are left out
                     ra.x += __shfl_xor_sync(FULL, ra.x, 1);
                     ra.y += __shfl_xor_sync(FULL, ra.y, 1);
                     rb.x += __shfl_xor_sync(FULL, rb.x, 1);
                     rb.y += __shfl_xor_sync(FULL, rb.y, 1);
-                    ra.x += __shfl_xor_sync(FULL, ra.x, 2);
-                    ra.y += __shfl_xor_sync(FULL, ra.y, 2);
-                    rb.x += __shfl_xor_sync(FULL, rb.x, 2);
-                    rb.y += __shfl_xor_sync(FULL, rb.y, 2);
                 }
-                // every lane of a quad holds the quad's sums: all four store the same value (no branch)
-                sm.part[slot0][warp][g] = ra.x;
-                sm.part[slot0][warp][g + 8] = ra.y;
-                if (two) {
-                    sm.part[slot1][warp][g] = rb.x;
-                    sm.part[slot1][warp][g + 8] = rb.y;
+                // lanes t = 0, 1 of a quad hold the quad's sums and store the same value
+                if (t < 2) {
+                    sm.part[slot0][warp][g] = ra.x;
+                    sm.part[slot0][warp][g + 8] = ra.y;
+                    if (two) {
+                        sm.part[slot1][warp][g] = rb.x;
+                        sm.part[slot1][warp][g + 8] = rb.y;
+                    }
                 }
                 __syncwarp();
                 if (prof) c_tile += clock64() - c1;
