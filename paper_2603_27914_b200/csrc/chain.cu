@@ -106,12 +106,6 @@ __device__ __forceinline__ void mma_u8s8_c(int (&c)[4], uint32_t a0, uint32_t a1
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// Rotate 256 fp32 values (read through L2; the sum of `nparts` K-chunk partial buffers) into
-// a compact fragment record in shared memory.
-// Integer pipeline on the INT32 pipe: y -> 23-bit fixed point with the block's power-of-two
-// scale s_in = 2^(ilogb(max|y|) - 21) (|y_int| < 2^22, as fine as fp32's own rounding of the
-// largest elements), exact int32 butterfly (|x'| < 2^30), then x' rounded to the limb range
-// |q| <= 2^(8L-2) with one more power-of-two shift k (tests/test_gpu_stack.py chain_bound).
 __device__ __forceinline__ float pow2f(int e) {  // exact 2^e, bit-built on the normal range
     return (e >= -126 && e <= 127) ? __int_as_float((e + 127) << 23) : ldexpf(1.0f, e);
 }
@@ -138,24 +132,25 @@ __device__ __forceinline__ unsigned long long ld_tag(const unsigned long long* p
     return SYS ? ld_u64_relaxed_sys(p) : ld_u64_relaxed(p);
 }
 
-// Wait for, and sum, one 256-block of a producing stage's tagged K-chunk partials.  Each 64-bit
-// word carries its value and the step epoch in one single-copy-atomic access, so the consumer
-// needs no flag, counter or fence: it spins until all 256 x nparts tags equal `epoch`.
+// Wait for, and sum, one 256-block of a producing stage's tagged K-chunk partials (this lane's elements
+// el + 32 e, el = rot_lane_element(lane)).  Each 64-bit word carries its value and the step epoch in one
+// single-copy-atomic access, so the consumer needs no flag, counter or fence: it spins until all
+// 256 x nparts tags equal `epoch`.
 template <bool SYS>
 __device__ __forceinline__ void load_tagged_block(const unsigned long long* src, int nparts, int64_t part_stride,
-                                                  unsigned epoch, int lane, float (&f)[8]) {
+                                                  unsigned epoch, int el, float (&f)[8]) {
     for (;;) {
         bool ok = true;
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-            const unsigned long long w = ld_tag<SYS>(src + lane + 32 * e);
+            const unsigned long long w = ld_tag<SYS>(src + el + 32 * e);
             ok &= (unsigned)(w >> 32) == epoch;
             f[e] = __uint_as_float((unsigned)w);
         }
         for (int c = 1; c < nparts; ++c)  // K-chunk partials, fixed order
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                const unsigned long long w = ld_tag<SYS>(src + c * part_stride + lane + 32 * e);
+                const unsigned long long w = ld_tag<SYS>(src + c * part_stride + el + 32 * e);
                 ok &= (unsigned)(w >> 32) == epoch;
                 f[e] += __uint_as_float((unsigned)w);
             }
@@ -164,29 +159,51 @@ __device__ __forceinline__ void load_tagged_block(const unsigned long long* src,
     }
 }
 
-__device__ void chain_rotate_to_smem(const float (&fin)[8], int L, uint8_t* img, int lane) {
-    float f[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) f[e] = fin[e];
-    // warp max of |f| as an integer max of the (non-negative) float bit patterns: one REDUX
+// Element layout of a rotation: lane L holds the block's elements k = rot_lane_element(L) + 32 e,
+// e = 0..7, i.e. the lane bits (0, 1) and (2, 3) of k swapped.  The butterflies do not care (H_256 is a
+// tensor product over the bits of k), and it puts the four bytes beta = k & 3 of every B-fragment word
+// into the COLUMNS of a stmatrix.m16n8.trans.b8 source matrix: lane L = 4 c' + j holds source row c' =
+// (k bits 0, 1, 4) and column pair j = k bits (2, 3); byte b of the register (limb b) goes to smem row
+// 2 j + (b & 1), byte column c' + 8 (b >> 1) (tools/probes/stsm_probe.cu).  So each 128-byte chunk image
+// is 8 rows (t, limb & 1) x 16 bytes (limb >> 1, h, beta), and one stmatrix.x4 writes four chunks: two
+// instructions replace 32 byte stores and 24 byte shifts (tools/probes/rot_probe.cu: 1703 -> 1290 cycles
+// per rotation with 16 warps, fragments identical).
+__device__ __forceinline__ int rot_lane_element(int L) { return ((L & 3) << 2) | ((L >> 2) & 3) | (L & 16); }
+
+// Rotate 256 fp32 values (this lane's elements rot_lane_element(lane) + 32 e) into the fragment image.
+// Integer pipeline: y -> 23-bit fixed point with the block's power-of-two scale s_in =
+// 2^(ilogb(max|y|) - 21) (|y_int| < 2^22, as fine as fp32's own rounding of the largest elements),
+// exact int32 butterfly (|x'| < 2^30), then x' rounded to the limb range |q| <= 2^(8L-2) by one more
+// power-of-two shift k (tests/test_gpu_stack.py chain_bound).
+__device__ __forceinline__ void chain_rotate_to_smem(const float (&f)[8], int L, uint8_t* img, int lane) {
+    // warp max of |f| as an integer max of the float bit patterns (sign cleared): one REDUX
     unsigned fbits = 0;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) fbits = max(fbits, __float_as_uint(fabsf(f[e])));
+    for (int e = 0; e < 8; ++e) fbits = max(fbits, __float_as_uint(f[e]) & 0x7fffffffu);
     fbits = __reduce_max_sync(FULL, fbits);
-    const float fmaxa = __uint_as_float(fbits);
-    const int e_in = fmaxa > 0.f ? ilogbf(fmaxa) - 21 : 0;
-    const float sc_in = pow2f(-e_in);
+    const int bexp = (int)(fbits >> 23);  // biased exponent of max|f|
+    int e_in;
+    float sc_in;
+    if (bexp >= 21) {  // max|f| >= 2^-106: s_in^-1 = 2^-e_in is a normal float, built from its bits
+        e_in = bexp - 148;
+        sc_in = __int_as_float((127 - e_in) << 23);
+    } else {
+        const float fmaxa = __uint_as_float(fbits);
+        e_in = fmaxa > 0.f ? ilogbf(fmaxa) - 21 : 0;
+        sc_in = pow2f(-e_in);
+    }
     int v[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e)  // |f sc_in| < 2^22, sc_in a power of two: one FMA rounds to nearest even
         v[e] = __float_as_int(fmaf(f[e], sc_in, 12582912.0f)) - 0x4B400000;
+    const int v0 = v[0];  // lane 0: element 0 (sum_k (H v)_k = 256 v_0, the exact zero-point correction)
 #pragma unroll
-    for (int h = 1; h < 32; h <<= 1) {
-        const bool high = (lane & h) != 0;
+    for (int h = 1; h < 32; h <<= 1) {  // lane bits: p + v on the low lane, p - v on the high lane (one IMAD)
+        const int sg = (lane & h) ? -1 : 1;
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             const int p = __shfl_xor_sync(FULL, v[e], h);
-            v[e] = high ? p - v[e] : v[e] + p;
+            v[e] = p + sg * v[e];
         }
     }
 #pragma unroll
@@ -208,8 +225,7 @@ __device__ void chain_rotate_to_smem(const float (&fin)[8], int L, uint8_t* img,
     // balanced record limbs of an int32)
     const int k = max(0, bl - min(8 * L - 2, 22));
     const int ex = e_in + k;
-    int Q = 0;
-    const int tt = (lane & 15) >> 2, beta = lane & 3, half = lane >> 4;
+    const int rnd = (1 << k) >> 1;
     // Class folding: chunk e = 4G + i pairs with the A operand c * 4^i (bit pair i of the code
     // bytes), so its activations are stored pre-scaled by 4^(3-i); every IMMA of a tile then
     // accumulates 64 * sum(c x') into ONE integer accumulator (no per-tile class recombination).
@@ -221,25 +237,37 @@ __device__ void chain_rotate_to_smem(const float (&fin)[8], int L, uint8_t* img,
     // A register group instead of 4 and produces the same integer accumulators.
     int qs[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-        const int q = k ? ((v[e] + (1 << (k - 1))) >> k) : v[e];
-        Q += q;
-        qs[e] = q << (2 * (3 - (e & 3)));
-    }
+    for (int e = 0; e < 8; ++e) qs[e] = ((v[e] + rnd) >> k) << (2 * (3 - (e & 3)));
+    uint32_t lw[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
         const int dq = (e & 3) < 3 ? qs[e] - qs[e + 1] : qs[e];  // |dq| < 2^29
-        const uint32_t limbs = (uint32_t)(dq + (int)0x80808080u) ^ 0x80808080u;
-        uint8_t* dst = img + (e * 16 + tt) * 8 + half * 4 + beta;  // (chunk e, column 0, t, byte)
-#pragma unroll
-        for (int l = 0; l < 4; ++l) dst[l * 32] = (uint8_t)(limbs >> (8 * l));  // column l: +4*8 B
+        lw[e] = (uint32_t)(dq + (int)0x80808080u) ^ 0x80808080u;
     }
-    Q = __reduce_add_sync(FULL, Q);
+    // lanes 8 m .. 8 m + 7 address the 8 rows of matrix m (chunk m of the first store, 4 + m of the second)
+    const uint32_t a = smem_u32(img) + (lane >> 3) * 128 + (lane & 7) * 16;
+    asm volatile("stmatrix.sync.aligned.m16n8.x4.trans.shared.b8 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(lw[0]),
+                 "r"(lw[1]), "r"(lw[2]), "r"(lw[3])
+                 : "memory");
+    asm volatile("stmatrix.sync.aligned.m16n8.x4.trans.shared.b8 [%0], {%1, %2, %3, %4};" ::"r"(a + 512), "r"(lw[4]),
+                 "r"(lw[5]), "r"(lw[6]), "r"(lw[7])
+                 : "memory");
     float* meta = reinterpret_cast<float*>(img + 8 * 16 * 8);  // f[0..7], corr[0..7]
     if (lane < 8) {
-        meta[lane] = lane < 4 ? pow2f(8 * lane + ex - 10) : 0.0f;  // 256^l 2^ex / 16 / 64
-        meta[8 + lane] = lane == 0 ? (float)Q * pow2f(ex - 4) : 0.0f;
+        meta[lane] = lane < 4 ? __int_as_float((8 * lane + ex - 10 + 127) << 23) : 0.0f;  // 256^l 2^ex / 16 / 64
+        // sum_k x'_k / 16 = 16 x_0 (fixed point), exact: the tile's error is then sum_k c_k (q_k 2^ex - x'_k)
+        meta[8 + lane] = lane == 0 ? (float)v0 * pow2f(e_in + 4) : 0.0f;
     }
+}
+
+// B fragments of lane (g, t) from a rotation image: chunk q's words (limb g, t-group t, h = 0 / 1) are one
+// 8-byte pair at row 2 t + (g & 1), byte 8 (g >> 1) (conflict-free: 16 lanes read 128 distinct bytes);
+// columns g >= 4 are zero.
+__device__ __forceinline__ void chain_load_frags(const uint8_t* img, int g, int t, uint2 (&bf)[8]) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+        bf[q] = g < 4 ? *reinterpret_cast<const uint2*>(img + q * 128 + (2 * t + (g & 1)) * 16 + 8 * (g >> 1))
+                      : make_uint2(0u, 0u);
 }
 
 // One 16-row x 256-k tile of the warp's block from a ring slot: returns the (row g, row g+8)
@@ -741,6 +769,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     // fragments in registers for every unit; each unit's 16 per-warp partials are summed by the
     // last warp to finish it, in warp order (deterministic).
     const int g = lane >> 2, t = lane & 3;
+    const int el = rot_lane_element(lane);  // this lane's elements el + 32 e of a 256-block (rotation layout)
     int cs = 0;        // ring slot of the CTA's next unit
     unsigned cp = 0;   // and its full-barrier phase parity
     uint8_t* rot = sm.rot[warp];
@@ -781,16 +810,16 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                 // the residual stream: the launch input x0, or (decoder, single GPU) a tagged buffer a
                 // flag-128 stage of this launch wrote
                 if (st.npeer == 0 && st.xres)
-                    load_tagged_block<false>(st.xres + 256 * (b0 + warp), 1, 0, epoch, lane, xv);
+                    load_tagged_block<false>(st.xres + 256 * (b0 + warp), 1, 0, epoch, el, xv);
                 else
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) xv[e] = __ldg(x0 + 256 * (b0 + warp) + lane + 32 * e);
+                    for (int e = 0; e < 8; ++e) xv[e] = __ldg(x0 + 256 * (b0 + warp) + el + 32 * e);
                 if ((st.asym & 64) && s > 1) {  // flag 64: + the o stage's output (index in bits 16-31) first
                     const int ref = (int)((unsigned)st.asym >> 16);
                     const ChainStage s0 = ref < NST ? sm.desc[ref] : stages[ref];
                     float pf[8];
                     load_tagged_block<false>(s0.y + 256 * (b0 + warp), (s0.NB + kUnitBlocks - 1) / kUnitBlocks,
-                                             s0.yrows, epoch, lane, pf);
+                                             s0.yrows, epoch, el, pf);
 #pragma unroll
                     for (int e = 0; e < 8; ++e) xv[e] += pf[e];
                 }
@@ -798,14 +827,14 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                     const ChainStage pv = s - 1 < NST ? sm.desc[s - 1] : stages[s - 1];
                     const int pn = (pv.NB + kUnitBlocks - 1) / kUnitBlocks;
                     float pf[8];
-                    load_tagged_block<false>(pv.y + 256 * (b0 + warp), pn, pv.yrows, epoch, lane, pf);
+                    load_tagged_block<false>(pv.y + 256 * (b0 + warp), pn, pv.yrows, epoch, el, pf);
 #pragma unroll
                     for (int e = 0; e < 8; ++e) xv[e] += pf[e];
                 }
                 if ((st.asym & 128) && sp.rt0 == 0)  // one CTA publishes the updated residual stream (tagged)
 #pragma unroll
                     for (int e = 0; e < 8; ++e)
-                        st_u64_relaxed(st.xout + 256 * (b0 + warp) + lane + 32 * e,
+                        st_u64_relaxed(st.xout + 256 * (b0 + warp) + el + 32 * e,
                                        ((unsigned long long)epoch << 32) | __float_as_uint(xv[e]));
 #pragma unroll
                 for (int e = 0; e < 8; ++e) ss += xv[e] * xv[e];
@@ -826,27 +855,27 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             if (GATED && (st.asym & 4)) {
                 // RMSNorm input: x * rsqrt(mean(x^2) + 1e-5) * gain (gain in st.xin)
 #pragma unroll
-                for (int e = 0; e < 8; ++e) f[e] = xv[e] * nscale * __ldg(st.xin + 256 * (b0 + warp) + lane + 32 * e);
+                for (int e = 0; e < 8; ++e) f[e] = xv[e] * nscale * __ldg(st.xin + 256 * (b0 + warp) + el + 32 * e);
             } else if (s == 0 || st.xin) {
                 const float* xs = st.xin ? st.xin : x0;
 #pragma unroll
-                for (int e = 0; e < 8; ++e) f[e] = __ldg(xs + 256 * (b0 + warp) + lane + 32 * e);
+                for (int e = 0; e < 8; ++e) f[e] = __ldg(xs + 256 * (b0 + warp) + el + 32 * e);
             } else {
                 const ChainStage pv = s - 1 < NST ? sm.desc[s - 1] : stages[s - 1];
                 const int pn = (pv.NB + kUnitBlocks - 1) / kUnitBlocks;
                 const unsigned long long* src = pv.y + 256 * (b0 + warp);
                 if (pv.npeer == 0) {
-                    load_tagged_block<false>(src, pn, pv.yrows, epoch, lane, f);
+                    load_tagged_block<false>(src, pn, pv.yrows, epoch, el, f);
                 } else {
                     src += (int64_t)(epoch & 1u) * pn * pv.yrows;
-                    load_tagged_block<true>(src, pn, pv.yrows, epoch, lane, f);
+                    load_tagged_block<true>(src, pn, pv.yrows, epoch, el, f);
                 }
                 if (GATED && (st.asym & 2)) {  // gated input: SiLU(prev[i]) * prev[cols + i] (gate | up halves)
                     float u[8];
                     if (pv.npeer == 0)
-                        load_tagged_block<false>(src + st.cols, pn, pv.yrows, epoch, lane, u);
+                        load_tagged_block<false>(src + st.cols, pn, pv.yrows, epoch, el, u);
                     else
-                        load_tagged_block<true>(src + st.cols, pn, pv.yrows, epoch, lane, u);
+                        load_tagged_block<true>(src + st.cols, pn, pv.yrows, epoch, el, u);
 #pragma unroll
                     for (int e = 0; e < 8; ++e) f[e] = f[e] / (1.f + __expf(-f[e])) * u[e];
                 }
@@ -858,9 +887,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 #endif
             __syncwarp();
             // fragments for lane (g, t): columns g < 4 hold limbs, columns >= 4 are zero
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                bf[q] = g < 4 ? reinterpret_cast<const uint2*>(rot)[(q * 4 + g) * 4 + t] : make_uint2(0u, 0u);
+            chain_load_frags(rot, g, t, bf);
             const float2 fc = reinterpret_cast<const float2*>(rot + 8 * 16 * 8)[t];       // f[2t], f[2t+1]
             const float2 cc = reinterpret_cast<const float2*>(rot + 8 * 16 * 8 + 32)[t];  // corr[2t], corr[2t+1]
             fcx = fc.x;  // columns 2t, 2t+1 = limbs 2t, 2t+1: factors differ by exactly 256

@@ -41,7 +41,7 @@ def chain_bound_cols(payload, rows, cols, X, limbs):
     quants, sb, zb, _ = O.split_payload(payload, n, False)
     codes, _ = O.unpack_planes(quants, n)
     t = codes.astype(np.float64) - np.trunc(O.f16_value(zb))[:, None]
-    t1 = np.abs(t).sum(axis=1).reshape(rows, nb)
+    t1 = np.maximum(np.abs(t).sum(axis=1), codes.astype(np.float64).sum(axis=1)).reshape(rows, nb)  # see chain_bound
     ht1 = np.abs(t @ H256).sum(axis=1).reshape(rows, nb)
     d = O.f16_value(sb).reshape(rows, nb)
     xb = X.T.reshape(-1, nb, n)                                         # (m, nb, n)

@@ -95,7 +95,9 @@ def perf_bound(payload, rows, cols, x, limbs):
     deq = O.dequantize(payload, rows, cols, n, False)
     quants, sb, zb, _ = O.split_payload(payload, n, False)
     codes, _ = O.unpack_planes(quants, n)
-    t1 = np.abs(codes.astype(np.float64) - np.trunc(O.f16_value(zb))[:, None]).sum(axis=1).reshape(rows, nb)
+    # max(|t|_1, |c|_1): the chain kernel (k = 1) subtracts the exact sum of x' (test_gpu_stack.chain_bound)
+    t1 = np.maximum(np.abs(codes.astype(np.float64) - np.trunc(O.f16_value(zb))[:, None]).sum(axis=1),
+                    codes.astype(np.float64).sum(axis=1)).reshape(rows, nb)
     d = O.f16_value(sb).reshape(rows, nb)
     xb = O.butterfly(np.asarray(x, np.float64).reshape(nb, n))
     amax = np.abs(xb).max(axis=1)

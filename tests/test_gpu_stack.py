@@ -23,7 +23,8 @@ def chain_bound(payload, rows, cols, x, limbs=3):
 
     The chain rotates in integers: x -> x_int = rint(x / s_in), s_in = 2^(ilogb(max|x_b|) - 21),
     exact butterfly, x' rounded to |q| <= 2^(8L-2) by a shift k (csrc/chain.cu).  Per block:
-        |err| <= d/16 * ( |t|_1 * 2^(e_in+k) / 2 + |H t|_1 * s_in / 2 )
+        |err| <= d/16 * ( max(|t|_1, |c|_1) * 2^(e_in+k) / 2 + |H t|_1 * s_in / 2 )
+    (|c|_1: the chain subtracts the exact sum of x'; |t|_1: K3 / K5b subtract the rounded sum)
     plus 1e-5 * sum |w_hat| |x| for fp32 accumulation (also covers the K3 path of mode="kernels").
     """
     n = 256
@@ -32,7 +33,9 @@ def chain_bound(payload, rows, cols, x, limbs=3):
     quants, sb, zb, _ = O.split_payload(payload, n, False)
     codes, _ = O.unpack_planes(quants, n)
     t = codes.astype(np.float64) - np.trunc(O.f16_value(zb))[:, None]
-    t1 = np.abs(t).sum(axis=1).reshape(rows, nb)
+    # the chain kernel corrects with the exact sum of x' (256 x_0): its limb-rounding term is |c|_1;
+    # K3/K5b correct with the rounded sum: |t|_1 -- the max covers both
+    t1 = np.maximum(np.abs(t).sum(axis=1), codes.astype(np.float64).sum(axis=1)).reshape(rows, nb)
     ht1 = np.abs(t @ H256).sum(axis=1).reshape(rows, nb)
     d = O.f16_value(sb).reshape(rows, nb)
     xb = np.asarray(x, np.float64).reshape(nb, n)
