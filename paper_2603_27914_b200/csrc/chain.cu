@@ -302,9 +302,12 @@ __device__ __forceinline__ float2 chain_tile(const uint8_t* ring, int warp, int 
 
 // stage descriptors + this CTA's split cached in smem (global beyond) and the weight-ring depth: the
 // decoder instantiation (GATED) trades one ring slot for room to cache a whole token's ~200 stages
+#ifndef CHAIN_NSL
+#define CHAIN_NSL 10
+#endif
 template <bool GATED>
 struct ChainCfg {
-    static constexpr int kSlots = GATED ? 10 : 11;
+    static constexpr int kSlots = GATED ? 9 : CHAIN_NSL;
     static constexpr int kStages = GATED ? 240 : 136;
 };
 constexpr int kSmemStages = ChainCfg<false>::kStages;
@@ -534,7 +537,7 @@ struct ChainSmem {
     StageSplit split[NST];
     alignas(128) uint8_t ring[NSL][kSlotBytes];
     alignas(16) uint8_t rot[kChainConsumerWarps][kActSmemBlock];  // per-warp rotation scratch (attention scratch)
-    float part[NSL][kChainConsumerWarps][16];           // per-warp row partials of a unit
+    float part[NSL][kChainConsumerWarps][2][16];        // per-warp row partials of a unit (limb pairs t = 0, 1)
     float normsq[kChainConsumerWarps];                  // per-warp sums of squares (RMSNorm input stages)
     uint64_t full[NSL];
     uint64_t empty[NSL];
@@ -641,13 +644,19 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                 const int useq = seq + j;
                 const int slot = useq % NSL;
                 mbar_wait(&sm.parts[slot], (unsigned)(useq / NSL) & 1u);
-                if (lane < 16) {
+                float sum;
+                {
+                    // lane = (limb pair t = lane >> 4, row lane & 15): the 16 warps' partials in warp order,
+                    // then the two limb pairs
                     float part[kChainConsumerWarps];
 #pragma unroll
-                    for (int w = 0; w < kChainConsumerWarps; ++w) part[w] = sm.part[slot][w][lane];
-                    float sum = part[0];
+                    for (int w = 0; w < kChainConsumerWarps; ++w) part[w] = sm.part[slot][w][lane >> 4][lane & 15];
+                    sum = part[0];
 #pragma unroll
                     for (int w = 1; w < kChainConsumerWarps; ++w) sum += part[w];
+                    sum += __shfl_xor_sync(FULL, sum, 16);
+                }
+                if (lane < 16) {
                     const int64_t row = (int64_t)(sp.rt0 + j * sp.Gc) * 16 + lane;
                     if (row < st.rows) {
                         const unsigned long long word = tag | __float_as_uint(sum);
@@ -930,20 +939,15 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 #endif
                     ra = chain_tile<ASYM>(sm.ring[slot0], warp, lane, g, bf, fcx, corr);
                     if (two) rb = chain_tile<ASYM>(sm.ring[slot1], warp, lane, g, bf, fcx, corr);
-                    // combine the quad's limb-pair columns: lanes t = 0, 1 hold columns 0..3 (the four
-                    // limbs); t = 2, 3 hold the zero columns 4..7 and are left out
-                    ra.x += __shfl_xor_sync(FULL, ra.x, 1);
-                    ra.y += __shfl_xor_sync(FULL, ra.y, 1);
-                    rb.x += __shfl_xor_sync(FULL, rb.x, 1);
-                    rb.y += __shfl_xor_sync(FULL, rb.y, 1);
                 }
-                // lanes t = 0, 1 of a quad hold the quad's sums and store the same value
+                // lanes t = 0, 1 hold the limb-pair columns 0..3 (t = 2, 3: the zero columns 4..7); the
+                // reducer adds the two pairs
                 if (t < 2) {
-                    sm.part[slot0][warp][g] = ra.x;
-                    sm.part[slot0][warp][g + 8] = ra.y;
+                    sm.part[slot0][warp][t][g] = ra.x;
+                    sm.part[slot0][warp][t][g + 8] = ra.y;
                     if (two) {
-                        sm.part[slot1][warp][g] = rb.x;
-                        sm.part[slot1][warp][g + 8] = rb.y;
+                        sm.part[slot1][warp][t][g] = rb.x;
+                        sm.part[slot1][warp][t][g + 8] = rb.y;
                     }
                 }
                 __syncwarp();
