@@ -300,6 +300,44 @@ __device__ __forceinline__ float2 chain_tile(const uint8_t* ring, int warp, int 
     return make_float2(d0 * (fcx * v0 - zf0 * corr), d1 * (fcx * v1 - zf1 * corr));
 }
 
+// Two units' tiles with their IMMA chains interleaved: each IMMA's accumulator input is two MMAs back
+// (the chains of one unit alone stall ~13 cycles per IMMA on the accumulator dependency -- the fixed
+// stall counts ptxas puts before every dependent IMMA).  Same integer accumulators as chain_tile.
+template <bool ASYM>
+__device__ __forceinline__ void chain_tile2(const uint8_t* ringA, const uint8_t* ringB, int warp, int lane, int g,
+                                            const uint2 (&bf)[8], float fcx, float corr, float2& ra, float2& rb) {
+    const uint4 a0 = reinterpret_cast<const uint4*>(ringA + warp * 1024)[lane];
+    const uint4 a1 = reinterpret_cast<const uint4*>(ringA + warp * 1024 + 512)[lane];
+    const uint4 b0 = reinterpret_cast<const uint4*>(ringB + warp * 1024)[lane];
+    const uint4 b1 = reinterpret_cast<const uint4*>(ringB + warp * 1024 + 512)[lane];
+    int CA[4] = {0, 0, 0, 0}, CB[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t mk = i == 3 ? 0xffffffffu : (0x04040404u << (2 * i)) - 0x01010101u;  // cumulative
+        mma_u8s8_c(CA, a0.x & mk, a0.y & mk, a0.z & mk, a0.w & mk, bf[i].x, bf[i].y);
+        mma_u8s8_c(CB, b0.x & mk, b0.y & mk, b0.z & mk, b0.w & mk, bf[i].x, bf[i].y);
+        mma_u8s8_c(CA, a1.x & mk, a1.y & mk, a1.z & mk, a1.w & mk, bf[4 + i].x, bf[4 + i].y);
+        mma_u8s8_c(CB, b1.x & mk, b1.y & mk, b1.z & mk, b1.w & mk, bf[4 + i].x, bf[4 + i].y);
+    }
+    const uint32_t sa = reinterpret_cast<const uint32_t*>(ringA + kSlotCodes + warp * 32)[g];
+    const uint32_t sb = reinterpret_cast<const uint32_t*>(ringB + kSlotCodes + warp * 32)[g];
+    const float va0 = (float)(CA[0] + 256 * CA[1]), va1 = (float)(CA[2] + 256 * CA[3]);
+    const float vb0 = (float)(CB[0] + 256 * CB[1]), vb1 = (float)(CB[2] + 256 * CB[3]);
+    const float da0 = f16_bits_to_f32((uint16_t)(sa & 0xffffu)), da1 = f16_bits_to_f32((uint16_t)(sa >> 16));
+    const float db0 = f16_bits_to_f32((uint16_t)(sb & 0xffffu)), db1 = f16_bits_to_f32((uint16_t)(sb >> 16));
+    if (!ASYM) {
+        ra = make_float2(da0 * (fcx * va0 - corr), da1 * (fcx * va1 - corr));
+        rb = make_float2(db0 * (fcx * vb0 - corr), db1 * (fcx * vb1 - corr));
+        return;
+    }
+    const uint16_t za = reinterpret_cast<const uint16_t*>(ringA + kSlotCodes + kSlotScales + warp * 16)[g];
+    const uint16_t zb = reinterpret_cast<const uint16_t*>(ringB + kSlotCodes + kSlotScales + warp * 16)[g];
+    ra = make_float2(da0 * (fcx * va0 - (float)(1 + (int)(int8_t)(za & 0xff)) * corr),
+                     da1 * (fcx * va1 - (float)(1 + (int)(int8_t)(za >> 8)) * corr));
+    rb = make_float2(db0 * (fcx * vb0 - (float)(1 + (int)(int8_t)(zb & 0xff)) * corr),
+                     db1 * (fcx * vb1 - (float)(1 + (int)(int8_t)(zb >> 8)) * corr));
+}
+
 // stage descriptors + this CTA's split cached in smem (global beyond) and the weight-ring depth: the
 // decoder instantiation (GATED) trades one ring slot for room to cache a whole token's ~200 stages
 #ifndef CHAIN_NSL
@@ -937,8 +975,10 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 #else
                 if (has_block) {
 #endif
-                    ra = chain_tile<ASYM>(sm.ring[slot0], warp, lane, g, bf, fcx, corr);
-                    if (two) rb = chain_tile<ASYM>(sm.ring[slot1], warp, lane, g, bf, fcx, corr);
+                    if (two)
+                        chain_tile2<ASYM>(sm.ring[slot0], sm.ring[slot1], warp, lane, g, bf, fcx, corr, ra, rb);
+                    else
+                        ra = chain_tile<ASYM>(sm.ring[slot0], warp, lane, g, bf, fcx, corr);
                 }
                 // lanes t = 0, 1 hold the limb-pair columns 0..3 (t = 2, 3: the zero columns 4..7); the
                 // reducer adds the two pairs
