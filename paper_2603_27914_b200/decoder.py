@@ -9,7 +9,7 @@ stages [attention partials, attention combine, o, gate_up, down, next qkv] -- th
 of the qkv / gate_up stages (every CTA of a 4096-column stage holds the whole input), the SiLU gating
 in the loads of the down stage, the residual stream as tagged buffers written by each layer's last
 stage (the residual adds folded into the norm inputs); the attention stages read q / k / v from the
-qkv stage's tagged outputs (RoPE, KV append, grouped-query attention over 18 position splits per kv
+qkv stage's tagged outputs (RoPE, KV append, grouped-query attention over 16 position splits per kv
 head, then a per-head combine); the last layer ends in the lm_head.  A token step is one CUDA graph
 of that one launch: the position lives in a device tensor that the graph itself advances, so replays
 need no host work.
@@ -138,13 +138,18 @@ class DecoderStack:
             raise ValueError("DecoderStack: the attention stages need head_dim 128, max_ctx <= 1024, nh * hd = hidden")
         # ONE launch per token: qkv_0, then per layer [attention partials, attention combine, o, gate_up,
         # down, next qkv / lm_head]; the residual after layer L lives in the tagged buffer res[L + 1]
+        import os
         import struct
 
         G = self.nh // self.nkv
         if G != 4:
             raise ValueError("DecoderStack: the in-chain attention needs 4 query heads per kv head")
         sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
-        self.splits = max(1, min(32, sms // self.nkv))  # attention items (kv head, split), <= 32 splits
+        # attention items (kv head, split), at most one per SM: the combine fetches 8 splits per L2 round trip,
+        # so the split count is rounded down to a multiple of 8 (B200, 8 kv heads: 16 splits, 1000 tok/s, vs
+        # 18: 984 and 24 (two items on some SMs): 861).  ITQ3_ATTN_SPLITS overrides; ceil(max_ctx / splits) <= 64.
+        per_sm = min(32, sms // self.nkv)
+        self.splits = int(os.environ.get("ITQ3_ATTN_SPLITS", "0")) or max(1, per_sm - per_sm % 8 if per_sm >= 8 else per_sm)
         if -(-max_ctx // self.splits) > 64:  # positions per split (the chain's score scratch)
             raise ValueError("DecoderStack: ceil(max_ctx / attention splits) must be <= 64")
         self.res = [None] + [torch.zeros(self.h, dtype=torch.int64, device=self.dev) for _ in range(layers)]
