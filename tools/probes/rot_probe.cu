@@ -394,8 +394,8 @@ __global__ void __launch_bounds__(576, 1) rot_probe(const float* x, int nwarps, 
 }
 
 
-// correctness: the stmatrix image's fragments (elements loaded in the sig_lane order) must equal the
-// kernel image's fragments word for word (meta f too; corr differs by design: exact 256 v_0 vs sum q)
+// correctness: the kernel's rotation (chain_rotate_to_smem + chain_load_frags) must give the same fragments
+// and factors as the probe's stmatrix reference (stsm_rotate_to_smem + stsm_load_frags)
 __global__ void check(const float* x, long long* out) {
     __shared__ __align__(16) uint8_t i0[kActSmemBlock], i1[kActSmemBlock];
     const int lane = threadIdx.x, g = lane >> 2, t = lane & 3;
@@ -403,14 +403,14 @@ __global__ void check(const float* x, long long* out) {
     for (int b = 0; b < 16; ++b) {
         float f0[8], f1[8];
         for (int e = 0; e < 8; ++e) {
-            f0[e] = x[b * 256 + lane + 32 * e] * (b + 1);
+            f0[e] = x[b * 256 + rot_lane_element(lane) + 32 * e] * (b + 1);
             f1[e] = x[b * 256 + sig_lane(lane) + 32 * e] * (b + 1);
         }
         chain_rotate_to_smem(f0, 3, i0, lane);
         stsm_rotate_to_smem(f1, 3, i1, lane);
         __syncwarp();
         uint2 b0[8], b1[8];
-        for (int q = 0; q < 8; ++q) b0[q] = g < 4 ? reinterpret_cast<const uint2*>(i0)[(q * 4 + g) * 4 + t] : make_uint2(0u, 0u);
+        chain_load_frags(i0, g, t, b0);
         stsm_load_frags(i1, g, t, b1);
         for (int q = 0; q < 8; ++q) bad += (b0[q].x != b1[q].x) + (b0[q].y != b1[q].y);
         if (lane < 8) badm += reinterpret_cast<const float*>(i0 + 1024)[lane] != reinterpret_cast<const float*>(i1 + 1024)[lane];
@@ -453,7 +453,7 @@ int main() {
     cudaDeviceSynchronize();
     long long hc[2];
     cudaMemcpy(hc, dout, 16, cudaMemcpyDeviceToHost);
-    printf("fragment check (stmatrix image vs kernel image, 16 blocks): %lld mismatching words, %lld meta f diffs\n", hc[0], hc[1]);
+    printf("fragment check (kernel rotation vs the probe's stmatrix reference, 16 blocks): %lld mismatching words, %lld meta f diffs\n", hc[0], hc[1]);
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
