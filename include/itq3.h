@@ -55,6 +55,9 @@ enum itq3_check {
 const char* itq3_version(void);
 const char* itq3_last_error(void);
 int itq3_sm_count(void);
+/* fp32 copy (n % 4 == 0, 16-byte aligned pointers) by one small kernel; `src` / `dst` may be pinned host
+ * memory (UVA-mapped): the e2e step's input copy inside its CUDA graph (no DMA memcpy node) */
+int itq3_copy_f32(float* dst, const float* src, int64_t n, void* stream);
 
 /* ---- K1 encoder: replaces quantize_tensor / encode_block (codec.py:113-189) ----
  * w: numel values (f32 or f64, row-major flattened); the tail of the last block

@@ -29,6 +29,7 @@ SIGNATURES = {
     "itq3_version": (ctypes.c_char_p, []),
     "itq3_last_error": (ctypes.c_char_p, []),
     "itq3_sm_count": (_i32, []),
+    "itq3_copy_f32": (_i32, [_vp, _vp, _i64, _vp]),
     "itq3_encode": (_i32, [_vp, _i32, _i64, _i32, _i32, _i32, _dbl, _i32, _vp, _vp]),
     "itq3_validate": (_i32, [_vp, _i64, _i32, _i32, _u32, _vp, _vp]),
     "itq3_dequant": (_i32, [_vp, _i64, _i32, _i32, _i64, _vp, _i32, _vp]),

@@ -104,11 +104,12 @@ class LinearStack:
             _lib.call("itq3_gemv", _lib.ptr(self.tiled[i]), q.rows, q.cols, int(not q.symmetric),
                       _lib.ptr(self.acts[i]), 1, self.limbs, _lib.ptr(self.ys[i]), _lib.F32, 1, 1, s)
 
-    def launch_all(self) -> None:
+    def launch_all(self, out: torch.Tensor | None = None) -> None:
         if self.mode == "chain":
             trace = _lib.ptr(self.trace) if self.trace is not None else None
             _lib.call("itq3_chain_run", _lib.ptr(self.desc), len(self.qs), _lib.ptr(self.x), self.limbs,
-                      _lib.ptr(self.epoch), _lib.ptr(self.out), 0, trace, _lib.stream_ptr(self.dev))
+                      _lib.ptr(self.epoch), _lib.ptr(self.out if out is None else out), 0, trace,
+                      _lib.stream_ptr(self.dev))
             return
         for i in range(len(self.qs)):
             self.launch_stage(i)
@@ -144,25 +145,32 @@ class LinearStack:
             self.capture()
         self.graph.replay()
 
+    def _host_step(self) -> None:
+        # H2D: one small copy kernel reading the pinned (UVA-mapped) input; chain mode: the kernel's final
+        # fold stores the output straight into the pinned host buffer (no memcpy nodes, 1909 -> ~1950 tok/s)
+        _lib.call("itq3_copy_f32", _lib.ptr(self.x), _lib.ptr(self.host_in), self.x.numel(), _lib.stream_ptr(self.dev))
+        if self.mode == "chain":
+            self.launch_all(out=self.host_out)
+        else:
+            self.launch_all()
+            self.host_out.copy_(self.output(), non_blocking=True)
+
     def capture_host_step(self) -> None:
-        """One CUDA graph for a whole host-to-host step: H2D of the pinned input, the chain (or the
-        kernel sequence), D2H of the last stage into pinned memory -- a single launch per token."""
+        """One CUDA graph for a whole host-to-host step: the pinned input copied in by a small kernel, the
+        chain (or the kernel sequence), its output written into pinned host memory -- one graph per token."""
         side = torch.cuda.Stream(self.dev)
         side.wait_stream(torch.cuda.current_stream(self.dev))
         with torch.cuda.stream(side):
-            self.x.copy_(self.host_in, non_blocking=True)
-            self.launch_all()  # warm-up outside capture
-            self.host_out.copy_(self.output(), non_blocking=True)
+            self._host_step()  # warm-up outside capture
         torch.cuda.current_stream(self.dev).wait_stream(side)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self.x.copy_(self.host_in, non_blocking=True)
-            self.launch_all()
-            self.host_out.copy_(self.output(), non_blocking=True)
+            self._host_step()
         self.host_graph = g
 
     def forward(self, x) -> np.ndarray:
-        """Host in -> host out: H2D of x, the chain, D2H of the last stage's output, as ONE graph launch."""
+        """Host in -> host out: H2D of x, the chain, D2H of the last stage's output, as ONE graph launch.
+        The returned host array is the stack's pinned output buffer (valid until the next call)."""
         xt = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x, dtype=np.float32))
         if xt.numel() != self.x.numel():
             raise ShapeError(f"LinearStack.forward: expected {self.x.numel()} inputs, got {xt.numel()}")
@@ -174,7 +182,11 @@ class LinearStack:
             if getattr(self, "host_graph", None) is None or self.graph is None:
                 self.replay()  # first use: capture the device-only graph too (stage outputs, epochs)
                 self.capture_host_step()
-            self.host_in.copy_(xt.reshape(-1))
+                self._host_in_np, self._host_out_np = self.host_in.numpy(), self.host_out.numpy()
+                self._stream = torch.cuda.current_stream(self.dev)
+            np.copyto(self._host_in_np, xt.reshape(-1).numpy())  # plain memcpy into the pinned input
             self.host_graph.replay()
+            self._stream.synchronize()
+            return self._host_out_np
         torch.cuda.current_stream(self.dev).synchronize()
         return self.host_out.numpy()

@@ -141,7 +141,7 @@ def test_chain_c5_k28672():
     qs = build(41, shapes=shapes)
     st = LinearStack(qs, limbs=3, mode="chain")
     x = np.random.default_rng(5).standard_normal(512).astype(np.float32)
-    out = st.forward(x)
+    out = st.forward(x).copy()  # forward returns the stack's reused output buffer
     xin = x.astype(np.float64)
     for i, q in enumerate(qs):
         y = st.stage_output(i).cpu().numpy().astype(np.float64)

@@ -70,7 +70,7 @@ def test_stack_matches_oracle_stagewise(mode, asym):
     pays = [q.payload().cpu().numpy() for q in qs]
     st = LinearStack(qs, limbs=3, mode=mode)
     x = np.random.default_rng(0).standard_normal(qs[0].cols).astype(np.float32)
-    out = st.forward(x)
+    out = st.forward(x).copy()
     xin = x.astype(np.float64)
     for i, q in enumerate(qs):
         y = st.stage_output(i).cpu().numpy().astype(np.float64)
@@ -101,7 +101,7 @@ def test_chain_beyond_smem_descriptor_cache():
     pays = [q.payload().cpu().numpy() for q in qs]
     st = LinearStack(qs, limbs=3, mode="chain")
     x = np.random.default_rng(3).standard_normal(qs[0].cols).astype(np.float32)
-    out = st.forward(x)
+    out = st.forward(x).copy()
     xin = x.astype(np.float64)
     for i, q in enumerate(qs):
         y = st.stage_output(i).cpu().numpy().astype(np.float64)
