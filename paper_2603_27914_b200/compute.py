@@ -149,8 +149,16 @@ def _matmul_on_device(q: QuantizedTensor, X: torch.Tensor, out_dtype: torch.dtyp
         if flag is not None:
             _raise_if_nonfinite(flag)
         return Y
+    if q.mmq_ok() and out_dtype != torch.float64 and not q.fast_layout() and k < MMQ_MIN_TOKENS \
+            and q.k5_range_ok() and X.dtype != torch.float64:
+        # variant ss / block_n != 256 with k < 8: K5 on X zero-padded to 8 tokens (the padded columns are
+        # exact zeros, the real ones see K5's arithmetic and bound) -- instead of the exact fp64 kernel
+        Xp = torch.zeros((cols, MMQ_MIN_TOKENS), dtype=X.dtype, device=dev)
+        Xp[:, :k] = X
+        return _matmul_on_device(q, Xp, out_dtype, limbs, check_finite)[:, :k]
     if q.mmq_ok() and out_dtype != torch.float64 and k >= MMQ_MIN_TOKENS and q.k5_range_ok():
         # K5: block_n 256 variant s for k > MMQ8_MAX_TOKENS; variant ss and block_n != 256 for every k >= MMQ_MIN_TOKENS
+        # (and, zero-padded, k < MMQ_MIN_TOKENS)
         mmq = q.mmq_layout()
         s = _lib.stream_ptr(dev)
         act = _scratch(dev, s, "act", _lib.load().itq3_mmq_act_nbytes(cols, k))

@@ -173,3 +173,26 @@ def test_mmq_huge_scale_takes_exact_path(variant):
     exact, bound = mmq_bound(q.payload().cpu().numpy(), 256, 512, X, ss=variant == "ss")
     assert np.all(np.isfinite(Y))
     assert np.all(np.abs(Y - exact) <= bound), np.max(np.abs(Y - exact) / bound)
+
+
+@pytest.mark.parametrize("fmt", [dict(variant="ss"), dict(block_n=64), dict(block_n=512, variant="ss"),
+                                 dict(block_n=128, symmetric=False)])
+@pytest.mark.parametrize("m", [1, 3, 7])
+def test_small_k_other_formats_on_k5(fmt, m):
+    """Variant ss / block_n != 256 at k < 8 (incl. the k = 1 GEMV): K5 on X zero-padded to 8 tokens,
+    within the K5 bound per column; the padded columns never leak into the result's shape."""
+    rng = np.random.default_rng(m + len(str(fmt)))
+    rows, cols = 700, 1536
+    w = rng.standard_normal((rows, cols)) * np.repeat(rng.uniform(0.01, 0.3, (1, cols // 32)), 32, axis=1)
+    q = P.quantize_tensor(w, P.QuantConfig(**fmt))
+    assert q.mmq_ok() and not q.fast_layout()
+    X = rng.standard_normal((cols, m)).astype(np.float32)
+    Y = P.fused_matmul(q, torch.from_numpy(X).cuda())
+    assert tuple(Y.shape) == (rows, m)
+    exact, bound = mmq_bound(q.payload().cpu().numpy(), rows, cols, X, ss=fmt.get("variant") == "ss",
+                             n=fmt.get("block_n", 256))
+    Yn = Y.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(Yn - exact) <= bound), np.max(np.abs(Yn - exact) / bound)
+    if m == 1:  # fused_matvec goes the same way
+        y = P.fused_matvec(q, torch.from_numpy(X[:, 0]).cuda()).cpu().numpy().astype(np.float64).reshape(-1)
+        assert np.all(np.abs(y - exact[:, 0]) <= bound[:, 0])
