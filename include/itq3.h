@@ -216,6 +216,10 @@ int itq3_chain_act_block_bytes(int limbs);
 int itq3_chain_smem_bytes(void);
 int itq3_chain_write_desc(void* host_desc, int index, const uint8_t* tiled, void* y, const float* xin, int64_t rows,
                           int64_t cols, int asymmetric, int reserved);
+/* Host-balanced work split of stage `index` (optional): d_work = device int32[grid], CTA c computes K-chunk
+ * d_work[c] / Gc and the row tiles d_work[c] % Gc + j Gc (Gc = grid / ceil(cols / 4096)), -1 = idle; every
+ * (chunk, first row tile) pair exactly once.  Outputs do not depend on the assignment. */
+int itq3_chain_set_work(void* host_desc, int index, const int32_t* d_work);
 /* Tensor-parallel stage (no single reference counterpart: the reference's TP path is the per-stage
  * matvec + all-gather of SURVEY.md C5).  This rank computes output rows [row0, row0 + rows) of a
  * yrows-row stage from its row shard `tiled`, and the reducer stores every tagged output word into

@@ -75,6 +75,7 @@ SIGNATURES = {
     "itq3_chain_act_block_bytes": (_i32, [_i32]),
     "itq3_chain_smem_bytes": (_i32, []),
     "itq3_chain_write_desc": (_i32, [_vp, _i32, _vp, _vp, _vp, _i64, _i64, _i32, _i32]),
+    "itq3_chain_set_work": (_i32, [_vp, _i32, _vp]),
     "itq3_chain_set_xout": (_i32, [_vp, _i32, _vp]),
     "itq3_chain_set_xres": (_i32, [_vp, _i32, _vp]),
     "itq3_chain_write_desc_attn": (_i32, [_vp, _i32, _i32, _vp, _vp, _i64]),

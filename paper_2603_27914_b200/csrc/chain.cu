@@ -54,6 +54,8 @@ struct ChainStage {
                                            // input adds (null: the launch input x0, untagged)
     };
     unsigned long long* xout;  // flag 128: where this RMSNorm stage writes the residual it formed (tagged)
+    const int32_t* work;       // optional [gridDim.x]: CTA c takes K-chunk work[c] / Gc, row tiles from
+                               // work[c] % Gc (-1: idle) -- a host-balanced assignment (itq3_chain_set_work)
     int64_t rows, cols;
     int32_t NB, RT, asym, npeer;
     int32_t row0, yrows;
@@ -601,9 +603,17 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 __device__ __forceinline__ bool compute_split(const ChainStage& st, int cta, int G, int s, StageSplit& sp) {
     sp.nch = (st.NB + kUnitBlocks - 1) / kUnitBlocks;
     sp.Gc = G / sp.nch;
+    sp.active = 0;
+    if (st.work) {
+        const int v = st.work[cta];
+        if (v < 0) return false;
+        sp.ch = v / sp.Gc;
+        sp.rt0 = v - sp.ch * sp.Gc;
+        sp.active = sp.rt0 < st.RT;
+        return sp.active;
+    }
     sp.ch = cta % sp.nch;
     const int idx = cta / sp.nch;
-    sp.active = 0;
     if (idx >= sp.Gc) return false;
     sp.rt0 = (idx + 7 * s) % sp.Gc;
     sp.active = sp.rt0 < st.RT;
@@ -1097,6 +1107,16 @@ extern "C" int itq3_chain_smem_bytes(void) { return (int)sizeof(ChainSmem<false>
 extern "C" int itq3_chain_write_desc_tp(void*, int, const uint8_t*, void*, int64_t, int64_t, int, int64_t, int64_t,
                                         const void*, int);
 
+// Host-balanced work split of stage `index`: d_work = device int32[grid]: CTA c computes K-chunk
+// d_work[c] / Gc and row tiles d_work[c] % Gc, + Gc, ... (Gc = grid / nch), -1 = idle; every (chunk, first row
+// tile) pair must appear exactly once.  Any such permutation gives the same outputs (each row's arithmetic does
+// not depend on which CTA computes it); LinearStack balances the units a CTA carries across stages whose
+// input is complete early (see stack.py).
+extern "C" int itq3_chain_set_work(void* host_desc, int index, const int32_t* d_work) {
+    reinterpret_cast<ChainStage*>(host_desc)[index].work = d_work;
+    return ITQ3_OK;
+}
+
 // flag 128 (decoder): where the RMSNorm stage `index` writes the residual input it computed
 extern "C" int itq3_chain_set_xout(void* host_desc, int index, void* xout) {
     reinterpret_cast<ChainStage*>(host_desc)[index].xout = (unsigned long long*)xout;
@@ -1173,6 +1193,7 @@ extern "C" int itq3_chain_write_desc_tp(void* host_desc, int index, const uint8_
     st.y = (unsigned long long*)y;
     st.xin = nullptr;
     st.xout = nullptr;
+    st.work = nullptr;
     st.ypeer = (unsigned long long* const*)d_peers;
     st.rows = rows;
     st.cols = cols;

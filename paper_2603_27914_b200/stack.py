@@ -19,9 +19,45 @@ from .codec import QuantizedTensor
 from .errors import ShapeError
 
 
+def balanced_work(shapes: list[tuple[int, int]], grid: int) -> np.ndarray:
+    """Host-balanced chain work split (itq3_chain_set_work): for every stage, which (K-chunk, first row
+    tile) each CTA takes, as chunk * Gc + rt0 (-1 idle).
+
+    A stage whose input is a strict prefix of the previous stage's output (qkv -> o, gate_up -> down in a
+    decoder layer) finds that input complete after the previous stage's first rounds, so each CTA starts it
+    right after its own units of the previous stage: the stage ends at max over CTAs of the units carried
+    since the last full-input stage.  Greedily giving the cheapest (chunk, row-tile) items to the CTAs that
+    carry the most units brings that max down to the mean (Llama-2-7B: qkv + o 8 -> 7 units, gate_up + down
+    15.5 -> 15).  Stages that read the whole previous output restart the count."""
+    S = len(shapes)
+    tab = np.full((S, grid), -1, dtype=np.int32)
+    load = np.zeros(grid)
+    for s, (rows, cols) in enumerate(shapes):
+        nb = cols // 256
+        nch = -(-nb // 16)
+        gc = grid // nch
+        rt = -(-rows // 16)
+        if not (s > 0 and cols < shapes[s - 1][0]):
+            load[:] = 0.0
+        items = []
+        for ch in range(nch):
+            w = min(16, nb - 16 * ch) / 16.0
+            for v in range(gc):
+                n = (rt - 1 - v) // gc + 1 if v < rt else 0
+                items.append((n * w, ch, v))
+        items.sort()
+        order = np.argsort(-load, kind="stable")
+        for c, (cost, ch, v) in zip(order, items):
+            tab[s, c] = ch * gc + v
+            load[c] += cost
+    return tab
+
+
 class LinearStack:
     """mode="chain": one persistent cooperative kernel per step (csrc/chain.cu, default);
     mode="kernels": 2 launches per stage (K3 rotate_act + K4 gemv), for comparison."""
+
+    balance = True  # host-balanced work split (balanced_work); False: the kernel's default round robin
 
     def __init__(self, qs: list[QuantizedTensor], limbs: int = 3, mode: str = "chain", independent: bool = False):
         if not qs:
@@ -67,6 +103,11 @@ class LinearStack:
                 xin = _lib.ptr(self._xin)
             _lib.check(lib.itq3_chain_write_desc(host, i, _lib.ptr(self.tiled[i]), _lib.ptr(self.yparts[i]), xin,
                                                  q.rows, q.cols, int(not q.symmetric), 0))
+        if self.balance and not self.independent:
+            grid = lib.itq3_sm_count()
+            self.work = torch.from_numpy(balanced_work([(q.rows, q.cols) for q in self.qs], grid)).to(self.dev)
+            for i in range(S):
+                _lib.check(lib.itq3_chain_set_work(host, i, _lib.ptr(self.work[i])))
         self.epoch = torch.zeros(2, dtype=torch.int32, device=self.dev)  # (step epoch, check-in count)
         self.trace = None
         self.desc = torch.frombuffer(bytearray(host.raw), dtype=torch.uint8).to(self.dev)

@@ -13,6 +13,7 @@ import torch
 sys.path.insert(0, os.getcwd())
 import bench
 from paper_2603_27914_b200.stack import LinearStack
+LinearStack.balance = "--no-balance" not in sys.argv
 dev = torch.device("cuda", 0)
 res = {}
 for indep in (False, True):
