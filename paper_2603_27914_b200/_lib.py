@@ -83,6 +83,7 @@ SIGNATURES = {
     "itq3_chain_write_desc_tp": (_i32, [_vp, _i32, _vp, _vp, _i64, _i64, _i32, _i64, _i64, _vp, _i32]),
     "itq3_chain_run": (_i32, [_vp, _i32, _vp, _i32, _vp, _vp, _i32, _vp, _vp]),
     "itq3_chain_run_gated": (_i32, [_vp, _i32, _vp, _i32, _vp, _vp, _i32, _vp, _vp]),
+    "itq3_chain_run_ex": (_i32, [_vp, _i32, _vp, _i32, _vp, _vp, _i32, _vp, _vp, _i32]),
     "itq3_f16_encode": (ctypes.c_uint16, [_dbl]),
     "itq3_f16_decode": (_dbl, [ctypes.c_uint16]),
 }

@@ -177,6 +177,7 @@ __device__ __forceinline__ int rot_lane_element(int L) { return ((L & 3) << 2) |
 // 2^(ilogb(max|y|) - 21) (|y_int| < 2^22, as fine as fp32's own rounding of the largest elements),
 // exact int32 butterfly (|x'| < 2^30), then x' rounded to the limb range |q| <= 2^(8L-2) by one more
 // power-of-two shift k (tests/test_gpu_stack.py chain_bound).
+template <bool MAD = false>  // MAD: butterflies as one register-operand mad each (the symmetric-only kernels)
 __device__ __forceinline__ void chain_rotate_to_smem(const float (&f)[8], int L, uint8_t* img, int lane) {
     // warp max of |f| as an integer max of the float bit patterns (sign cleared): one REDUX
     unsigned fbits = 0;
@@ -205,7 +206,10 @@ __device__ __forceinline__ void chain_rotate_to_smem(const float (&f)[8], int L,
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             const int p = __shfl_xor_sync(FULL, v[e], h);
-            v[e] = p + sg * v[e];
+            if (MAD)  // an opaque +-1 multiplier keeps ptxas from splitting it into negate + add
+                asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(v[e]) : "r"(v[e]), "r"(1 - ((lane & h) ? 2 : 0)), "r"(p));
+            else
+                v[e] = p + sg * v[e];
         }
     }
 #pragma unroll
@@ -637,10 +641,13 @@ __device__ __forceinline__ bool stage_get(const ChainSmem<GATED>& sm, const Chai
 //   0 stage entered, 1 input observed ready, 2 input rotated, 3 own units done
 // 18 warps: the per-SMSP register file (16K) caps a 5-warp SMSP at 96 registers/thread
 
-template <bool GATED, bool TRACE = false>  // TRACE: globaltimer stamps + cycle counters (tools/trace_chain.py)
-                      // in their own instantiation, so the measured kernels carry no counter registers.
+template <bool GATED, bool TRACE = false, bool ASYM = true>
+                      // TRACE: globaltimer stamps + cycle counters (tools/trace_chain.py) in their own
+                      // instantiation, so the measured kernels carry no counter registers.
                       // GATED: some stage reads SiLU(gate) * up (a separate instantiation keeps the
-                      // plain kernel's register allocation)
+                      // plain kernel's register allocation).  ASYM = false: every stage is symmetric -- no
+                      // zero-point tile loop in the kernel, which frees the tile loop's register allocation
+                      // (Llama-2-7B 0.494 -> 0.483 ms with the MAD butterflies that then fit)
 __global__ void __launch_bounds__(kChainThreads, 1)
     chain_kernel(const ChainStage* __restrict__ stages, int S, const float* __restrict__ x0, int L,
                  unsigned* __restrict__ epoch_ptr, float* __restrict__ out,
@@ -850,6 +857,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             continue;
         }
         if (!active) continue;
+        if (!ASYM && (st.asym & 1)) __trap();  // a zero-point stage in a symmetric-only launch: fail loudly
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 0] = globaltimer();
         const int b0 = sp.ch * kUnitBlocks;
         const int nb = min(kUnitBlocks, st.NB - b0);
@@ -940,7 +948,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 1] = globaltimer();
             if (prof) c_in += clock64() - c0;
 #ifndef CHAIN_EXP_NOROT
-            chain_rotate_to_smem(f, L, rot, lane);
+            chain_rotate_to_smem<!ASYM>(f, L, rot, lane);
 #endif
             __syncwarp();
             // fragments for lane (g, t): columns g < 4 hold limbs, columns >= 4 are zero
@@ -1013,8 +1021,8 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             }
         }
         };
-        if (st.asym & 1)
-            units(std::true_type{});
+        if (ASYM && (st.asym & 1))
+            units(std::integral_constant<bool, ASYM>{});
         else
             units(std::false_type{});
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 3] = globaltimer();
@@ -1206,7 +1214,7 @@ extern "C" int itq3_chain_write_desc_tp(void* host_desc, int index, const uint8_
     return ITQ3_OK;
 }
 
-template <bool GATED>
+template <bool GATED, bool ASYM>
 static int chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch, float* out,
                      int grid, void* d_trace, void* stream) {
     if (limbs < 1 || limbs > kMaxLimbs) {
@@ -1215,9 +1223,9 @@ static int chain_run(const void* d_desc, int n_stages, const float* x0, int limb
     }
     static std::atomic<unsigned long long> smem_attr{0}, smem_attr_tr{0};
     const int smem = (int)sizeof(ChainSmem<GATED>);
-    if (int rc = ensure_smem_attr(chain_kernel<GATED>, smem, smem_attr, "chain: smem attribute")) return rc;
-    if (!GATED && d_trace)
-        if (int rc = ensure_smem_attr(chain_kernel<false, true>, smem, smem_attr_tr, "chain: smem attribute")) return rc;
+    const bool tr = !GATED && d_trace;  // the trace instantiation is the asymmetric-capable plain kernel
+    auto kern = tr ? chain_kernel<false, true, true> : chain_kernel<GATED, false, ASYM>;
+    if (int rc = ensure_smem_attr(kern, smem, tr ? smem_attr_tr : smem_attr, "chain: smem attribute")) return rc;
     if (grid <= 0) grid = device_sms();
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
@@ -1229,7 +1237,6 @@ static int chain_run(const void* d_desc, int n_stages, const float* x0, int limb
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    auto kern = (!GATED && d_trace) ? chain_kernel<false, true> : chain_kernel<GATED>;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, (const ChainStage*)d_desc, n_stages, x0, limbs,
                                              d_epoch, out, (unsigned long long*)d_trace);
     if (e != cudaSuccess) {
@@ -1239,12 +1246,25 @@ static int chain_run(const void* d_desc, int n_stages, const float* x0, int limb
     return check_launch("itq3_chain_run");
 }
 
+// flags: bit 0 = gated chain (decoder stages: SiLU gating, RMSNorm, residuals, attention); bit 1 = every
+// weight stage is symmetric (no zero-points): the launch uses an instantiation without the zero-point
+// tile loop (faster; a stage with zero-points then traps the kernel instead of computing wrongly)
+extern "C" int itq3_chain_run_ex(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch,
+                                 float* out, int grid, void* d_trace, void* stream, int flags) {
+    const bool gated = flags & 1, sym = flags & 2;
+    if (gated)
+        return sym ? chain_run<true, false>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream)
+                   : chain_run<true, true>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
+    return sym ? chain_run<false, false>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream)
+               : chain_run<false, true>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
+}
+
 extern "C" int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch,
                               float* out, int grid, void* d_trace, void* stream) {
-    return chain_run<false>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
+    return chain_run<false, true>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
 }
 
 extern "C" int itq3_chain_run_gated(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch,
                                     float* out, int grid, void* d_trace, void* stream) {
-    return chain_run<true>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
+    return chain_run<true, true>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
 }

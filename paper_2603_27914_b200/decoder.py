@@ -17,6 +17,8 @@ need no host work.
 
 from __future__ import annotations
 
+import os
+
 import math
 
 import torch
@@ -67,14 +69,18 @@ class _Chain:
                 _lib.check(lib.itq3_chain_set_xout(host, i, _lib.ptr(st["xout"])))
                 self.keep.append(st["xout"])
         self.n = len(stages)
+        # the gated instantiation WITH the zero-point loop: its symmetric-only twin spills more in the attention
+        # path (997 vs 1000 tok/s on the Llama-3-8B decoder); ITQ3_GATED_SYM=1 selects the twin
+        sym = os.environ.get("ITQ3_GATED_SYM") == "1" and all(st["q"].symmetric for st in stages if "attn" not in st)
+        self.run_flags = 1 | (2 if sym else 0)
         self.desc = torch.frombuffer(bytearray(host.raw), dtype=torch.uint8).to(dev)
         self.epoch = torch.zeros(2, dtype=torch.int32, device=dev)
         self.out = out
 
     def __call__(self, x: torch.Tensor, stream: int) -> torch.Tensor:
         lib = self._lib
-        lib.call("itq3_chain_run_gated", lib.ptr(self.desc), self.n, lib.ptr(x), 3, lib.ptr(self.epoch),
-                 lib.ptr(self.out), 0, None, stream)
+        lib.call("itq3_chain_run_ex", lib.ptr(self.desc), self.n, lib.ptr(x), 3, lib.ptr(self.epoch),
+                 lib.ptr(self.out), 0, None, stream, self.run_flags)
         return self.out
 
 

@@ -256,8 +256,9 @@ class TPChainStack:
     def launch_all(self, stream: int | None = None) -> None:
         lib = self._lib
         s = stream if stream is not None else lib.stream_ptr(self.dev)
-        lib.call("itq3_chain_run", lib.ptr(self.desc), len(self.qs), lib.ptr(self.x), self.limbs,
-                 lib.ptr(self.epoch), lib.ptr(self.out), self.grid, None, s)
+        sym = 2 if all(q.symmetric for q in self.qs) else 0  # no zero-point tile loop in the kernel
+        lib.call("itq3_chain_run_ex", lib.ptr(self.desc), len(self.qs), lib.ptr(self.x), self.limbs,
+                 lib.ptr(self.epoch), lib.ptr(self.out), self.grid, None, s, sym)
 
     def capture(self) -> None:
         side = torch.cuda.Stream(self.dev)
