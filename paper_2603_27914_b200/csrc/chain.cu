@@ -647,13 +647,15 @@ template <bool GATED, bool TRACE = false, bool ASYM = true>
                       // GATED: some stage reads SiLU(gate) * up (a separate instantiation keeps the
                       // plain kernel's register allocation).  ASYM = false: every stage is symmetric -- no
                       // zero-point tile loop in the kernel, which frees the tile loop's register allocation
-                      // (Llama-2-7B 0.494 -> 0.483 ms with the MAD butterflies that then fit)
+                      // (Llama-2-7B 0.494 -> 0.483 ms with the MAD butterflies that then fit); the plain
+                      // symmetric kernel also leaves out the tensor-parallel (peer-store) paths
 __global__ void __launch_bounds__(kChainThreads, 1)
     chain_kernel(const ChainStage* __restrict__ stages, int S, const float* __restrict__ x0, int L,
                  unsigned* __restrict__ epoch_ptr, float* __restrict__ out,
                  unsigned long long* __restrict__ trace) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     ChainSmem<GATED>& sm = *reinterpret_cast<ChainSmem<GATED>*>(smem_raw);
+    constexpr bool TP = ASYM || GATED;  // the symmetric plain kernel is single-GPU only: no peer paths compiled
     constexpr int NSL = ChainSmem<GATED>::NSL, NST = ChainSmem<GATED>::NST;  // ring slots, cached stages
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int cta = blockIdx.x, G = gridDim.x;
@@ -692,7 +694,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             const int n_units = (st.RT - 1 - sp.rt0) / sp.Gc + 1;
             // y offset of this CTA's K-chunk (+ the epoch-parity half for tensor-parallel stages)
             const int64_t yoff = (int64_t)sp.ch * st.yrows + st.row0 +
-                                 (st.npeer ? (int64_t)(epoch & 1u) * sp.nch * st.yrows : 0);
+                                 (TP && st.npeer ? (int64_t)(epoch & 1u) * sp.nch * st.yrows : 0);
             unsigned long long* yout = st.y + yoff;
             const unsigned long long tag = (unsigned long long)epoch << 32;
             for (int j = 0; j < n_units; ++j) {
@@ -715,7 +717,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                     const int64_t row = (int64_t)(sp.rt0 + j * sp.Gc) * 16 + lane;
                     if (row < st.rows) {
                         const unsigned long long word = tag | __float_as_uint(sum);
-                        if (st.npeer == 0) {
+                        if (!TP || st.npeer == 0) {
                             st_u64_relaxed(yout + row, word);
                         } else {
                             for (int p = 0; p < st.npeer; ++p) st_u64_relaxed_sys(st.ypeer[p] + yoff + row, word);
@@ -857,7 +859,8 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             continue;
         }
         if (!active) continue;
-        if (!ASYM && (st.asym & 1)) __trap();  // a zero-point stage in a symmetric-only launch: fail loudly
+        // a zero-point or tensor-parallel stage in a symmetric single-GPU launch: fail loudly
+        if (!ASYM && ((st.asym & 1) || st.npeer)) __trap();
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 0] = globaltimer();
         const int b0 = sp.ch * kUnitBlocks;
         const int nb = min(kUnitBlocks, st.NB - b0);
@@ -929,7 +932,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                 const ChainStage pv = s - 1 < NST ? sm.desc[s - 1] : stages[s - 1];
                 const int pn = (pv.NB + kUnitBlocks - 1) / kUnitBlocks;
                 const unsigned long long* src = pv.y + 256 * (b0 + warp);
-                if (pv.npeer == 0) {
+                if (!TP || pv.npeer == 0) {
                     load_tagged_block<false>(src, pn, pv.yrows, epoch, el, f);
                 } else {
                     src += (int64_t)(epoch & 1u) * pn * pv.yrows;
@@ -1038,18 +1041,19 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     // fold the last stage's K-chunk partials into `out` (fixed order), waiting on the tags
     const ChainStage last = stages[S - 1];
     const int ln = (last.NB + kUnitBlocks - 1) / kUnitBlocks;
-    const unsigned long long* ylast = last.y + (last.npeer ? (int64_t)(epoch & 1u) * ln * last.yrows : 0);
+    const bool last_tp = TP && last.npeer;
+    const unsigned long long* ylast = last.y + (last_tp ? (int64_t)(epoch & 1u) * ln * last.yrows : 0);
     for (int64_t r = (int64_t)cta * (32 * kChainConsumerWarps) + tid; r < last.yrows;
          r += (int64_t)G * 32 * kChainConsumerWarps) {
         float v;
         for (;;) {
             bool ok = true;
-            unsigned long long w = last.npeer ? ld_u64_relaxed_sys(ylast + r) : ld_u64_relaxed(ylast + r);
+            unsigned long long w = last_tp ? ld_u64_relaxed_sys(ylast + r) : ld_u64_relaxed(ylast + r);
             ok &= (unsigned)(w >> 32) == epoch;
             v = __uint_as_float((unsigned)w);
             for (int c = 1; c < ln; ++c) {
-                w = last.npeer ? ld_u64_relaxed_sys(ylast + c * last.yrows + r)
-                               : ld_u64_relaxed(ylast + c * last.yrows + r);
+                w = last_tp ? ld_u64_relaxed_sys(ylast + c * last.yrows + r)
+                            : ld_u64_relaxed(ylast + c * last.yrows + r);
                 ok &= (unsigned)(w >> 32) == epoch;
                 v += __uint_as_float((unsigned)w);
             }

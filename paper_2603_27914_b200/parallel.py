@@ -256,9 +256,9 @@ class TPChainStack:
     def launch_all(self, stream: int | None = None) -> None:
         lib = self._lib
         s = stream if stream is not None else lib.stream_ptr(self.dev)
-        sym = 2 if all(q.symmetric for q in self.qs) else 0  # no zero-point tile loop in the kernel
+        # the general kernel: the symmetric-only one is single-GPU (no peer-store paths)
         lib.call("itq3_chain_run_ex", lib.ptr(self.desc), len(self.qs), lib.ptr(self.x), self.limbs,
-                 lib.ptr(self.epoch), lib.ptr(self.out), self.grid, None, s, sym)
+                 lib.ptr(self.epoch), lib.ptr(self.out), self.grid, None, s, 0)
 
     def capture(self) -> None:
         side = torch.cuda.Stream(self.dev)
