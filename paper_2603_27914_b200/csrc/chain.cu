@@ -641,7 +641,7 @@ __device__ __forceinline__ bool stage_get(const ChainSmem<GATED>& sm, const Chai
 //   0 stage entered, 1 input observed ready, 2 input rotated, 3 own units done
 // 18 warps: the per-SMSP register file (16K) caps a 5-warp SMSP at 96 registers/thread
 
-template <bool GATED, bool TRACE = false, bool ASYM = true>
+template <bool GATED, bool TRACE = false, bool ASYM = true, bool TP = true>
                       // TRACE: globaltimer stamps + cycle counters (tools/trace_chain.py) in their own
                       // instantiation, so the measured kernels carry no counter registers.
                       // GATED: some stage reads SiLU(gate) * up (a separate instantiation keeps the
@@ -655,7 +655,6 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                  unsigned long long* __restrict__ trace) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     ChainSmem<GATED>& sm = *reinterpret_cast<ChainSmem<GATED>*>(smem_raw);
-    constexpr bool TP = ASYM || GATED;  // the symmetric plain kernel is single-GPU only: no peer paths compiled
     constexpr int NSL = ChainSmem<GATED>::NSL, NST = ChainSmem<GATED>::NST;  // ring slots, cached stages
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int cta = blockIdx.x, G = gridDim.x;
@@ -860,7 +859,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         }
         if (!active) continue;
         // a zero-point or tensor-parallel stage in a symmetric single-GPU launch: fail loudly
-        if (!ASYM && ((st.asym & 1) || st.npeer)) __trap();
+        if ((!ASYM && (st.asym & 1)) || (!TP && st.npeer)) __trap();
         if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 0] = globaltimer();
         const int b0 = sp.ch * kUnitBlocks;
         const int nb = min(kUnitBlocks, st.NB - b0);
@@ -1218,7 +1217,7 @@ extern "C" int itq3_chain_write_desc_tp(void* host_desc, int index, const uint8_
     return ITQ3_OK;
 }
 
-template <bool GATED, bool ASYM>
+template <bool GATED, bool ASYM, bool TP>
 static int chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch, float* out,
                      int grid, void* d_trace, void* stream) {
     if (limbs < 1 || limbs > kMaxLimbs) {
@@ -1228,7 +1227,7 @@ static int chain_run(const void* d_desc, int n_stages, const float* x0, int limb
     static std::atomic<unsigned long long> smem_attr{0}, smem_attr_tr{0};
     const int smem = (int)sizeof(ChainSmem<GATED>);
     const bool tr = !GATED && d_trace;  // the trace instantiation is the asymmetric-capable plain kernel
-    auto kern = tr ? chain_kernel<false, true, true> : chain_kernel<GATED, false, ASYM>;
+    auto kern = tr ? chain_kernel<false, true, true, true> : chain_kernel<GATED, false, ASYM, TP>;
     if (int rc = ensure_smem_attr(kern, smem, tr ? smem_attr_tr : smem_attr, "chain: smem attribute")) return rc;
     if (grid <= 0) grid = device_sms();
     cudaLaunchConfig_t cfg = {};
@@ -1251,24 +1250,26 @@ static int chain_run(const void* d_desc, int n_stages, const float* x0, int limb
 }
 
 // flags: bit 0 = gated chain (decoder stages: SiLU gating, RMSNorm, residuals, attention); bit 1 = every
-// weight stage is symmetric (no zero-points): the launch uses an instantiation without the zero-point
-// tile loop (faster; a stage with zero-points then traps the kernel instead of computing wrongly)
+// weight stage is symmetric (no zero-points); bit 2 = single GPU (no tensor-parallel stage).  Bits 1 and 2 pick
+// instantiations without the zero-point tile loop / the peer-store paths (faster: the kernel is at its
+// register cap, so every compiled path shapes the tile loop); a stage needing what was left out traps.
+// Instantiated: plain general, plain symmetric single-GPU, gated general, gated single-GPU.
 extern "C" int itq3_chain_run_ex(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch,
                                  float* out, int grid, void* d_trace, void* stream, int flags) {
-    const bool gated = flags & 1, sym = flags & 2;
+    const bool gated = flags & 1, sym = flags & 2, single = flags & 4;
     if (gated)
-        return sym ? chain_run<true, false>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream)
-                   : chain_run<true, true>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
-    return sym ? chain_run<false, false>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream)
-               : chain_run<false, true>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
+        return single ? chain_run<true, true, false>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream)
+                      : chain_run<true, true, true>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
+    return sym && single ? chain_run<false, false, false>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream)
+                         : chain_run<false, true, true>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
 }
 
 extern "C" int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch,
                               float* out, int grid, void* d_trace, void* stream) {
-    return chain_run<false, true>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
+    return chain_run<false, true, true>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
 }
 
 extern "C" int itq3_chain_run_gated(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch,
                                     float* out, int grid, void* d_trace, void* stream) {
-    return chain_run<true, true>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
+    return chain_run<true, true, true>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
 }

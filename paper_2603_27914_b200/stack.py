@@ -148,7 +148,7 @@ class LinearStack:
     def launch_all(self, out: torch.Tensor | None = None) -> None:
         if self.mode == "chain":
             trace = _lib.ptr(self.trace) if self.trace is not None else None
-            sym = 2 if all(q.symmetric for q in self.qs) else 0  # no zero-point tile loop in the kernel
+            sym = 6 if all(q.symmetric for q in self.qs) else 4  # single GPU (+ no zero-point tile loop)
             _lib.call("itq3_chain_run_ex", _lib.ptr(self.desc), len(self.qs), _lib.ptr(self.x), self.limbs,
                       _lib.ptr(self.epoch), _lib.ptr(self.out if out is None else out), 0, trace,
                       _lib.stream_ptr(self.dev), sym)
