@@ -386,7 +386,6 @@ __device__ __forceinline__ void tagged_load4(const unsigned long long* p, unsign
             v[j] = __uint_as_float((unsigned)w);
         }
         if (__all_sync(FULL, ok)) return;
-        __nanosleep(32);
     }
 }
 
@@ -531,7 +530,6 @@ __device__ void attn_comb(const AttnParams& P, const unsigned long long* part, u
             sj = __uint_as_float((unsigned)w1);
         }
         if (__all_sync(FULL, ok)) break;
-        __nanosleep(32);
     }
     float m = mj;
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(FULL, m, o));
@@ -551,7 +549,6 @@ __device__ void attn_comb(const AttnParams& P, const unsigned long long* part, u
                 }
             }
             if (__all_sync(FULL, ok)) break;
-            __nanosleep(32);
         }
 #pragma unroll
         for (int u = 0; u < kGrp; ++u) {
