@@ -254,9 +254,9 @@ int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs,
 /* the same, for chains with gated stages (descriptor flag bit 1) */
 int itq3_chain_run_gated(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch, float* out,
                          int grid, void* d_trace, void* stream);
-/* flags: bit 0 = gated chain (itq3_chain_run_gated), bit 1 = every weight stage symmetric, bit 2 = single GPU
- * (no tensor-parallel stage): instantiations without the zero-point tile loop (plain chains, with bit 2) and
- * without the peer-store paths (faster); a stage needing what was left out traps the launch. */
+/* flags: bit 0 = gated chain (itq3_chain_run_gated), bit 1 = every weight stage symmetric (plain chains: no
+ * zero-point tile loop), bit 2 = single GPU (no tensor-parallel stage: no peer-store paths); the specialised
+ * instantiations are faster, and a stage needing what was left out traps the launch. */
 int itq3_chain_run_ex(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch, float* out,
                       int grid, void* d_trace, void* stream, int flags);
 

@@ -256,9 +256,10 @@ class TPChainStack:
     def launch_all(self, stream: int | None = None) -> None:
         lib = self._lib
         s = stream if stream is not None else lib.stream_ptr(self.dev)
-        # the general kernel: the symmetric-only one is single-GPU (no peer-store paths)
+        # symmetric weights: the instantiation without the zero-point tile loop (with the peer-store paths)
+        sym = 2 if all(q.symmetric for q in self.qs) else 0
         lib.call("itq3_chain_run_ex", lib.ptr(self.desc), len(self.qs), lib.ptr(self.x), self.limbs,
-                 lib.ptr(self.epoch), lib.ptr(self.out), self.grid, None, s, 0)
+                 lib.ptr(self.epoch), lib.ptr(self.out), self.grid, None, s, sym)
 
     def capture(self) -> None:
         side = torch.cuda.Stream(self.dev)
