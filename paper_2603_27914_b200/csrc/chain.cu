@@ -28,7 +28,13 @@ namespace itq3 {
 #endif
 
 constexpr int kChainConsumerWarps = 16;
-constexpr int kChainThreads = 32 * (kChainConsumerWarps + 2);  // + producer warp + reducer warp
+#ifndef CHAIN_REDUCERS
+#define CHAIN_REDUCERS 2
+#endif
+// Reducer warps take alternate units (a unit's reduction sits between its last tile and its publish, and
+// one warp alone falls behind).  Up to 20 warps keep 5 per SMSP, i.e. the same 96-register cap as 18.
+constexpr int kChainReducers = CHAIN_REDUCERS;
+constexpr int kChainThreads = 32 * (kChainConsumerWarps + 1 + kChainReducers);  // + producer + reducers
 constexpr int kProducerWarp = kChainConsumerWarps, kReducerWarp = kChainConsumerWarps + 1;
 constexpr int kUnitBlocks = 16;                          // 256-blocks per unit (one per consumer warp)
 constexpr int kSlotCodes = kUnitBlocks * 1024;           // 16 KB
@@ -676,7 +682,8 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     }
     __syncthreads();
 
-    if (warp == kReducerWarp) {
+    if (warp >= kReducerWarp) {
+        const int rr = warp - kReducerWarp;  // this reducer's units: unit sequence number % kChainReducers == rr
         // ------------------------------ reducer ------------------------------
         // Sums each unit's 16 per-warp row partials in warp order (deterministic), stores the
         // tagged outputs and releases the ring slot.  Runs behind the compute warps so they
@@ -692,7 +699,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                                  (TP && st.npeer ? (int64_t)(epoch & 1u) * sp.nch * st.yrows : 0);
             unsigned long long* yout = st.y + yoff;
             const unsigned long long tag = (unsigned long long)epoch << 32;
-            for (int j = 0; j < n_units; ++j) {
+            for (int j = (rr - seq % kChainReducers + kChainReducers) % kChainReducers; j < n_units; j += kChainReducers) {
                 const int useq = seq + j;
                 const int slot = useq % NSL;
                 mbar_wait(&sm.parts[slot], (unsigned)(useq / NSL) & 1u);
