@@ -95,7 +95,7 @@ class _ChainGemv:
                                              q.cols, int(not q.symmetric), 0))
         self.desc = torch.frombuffer(bytearray(host.raw), dtype=torch.uint8).to(dev)
         self.epoch = torch.zeros(2, dtype=torch.int32, device=dev)  # (step epoch, check-in count)
-        self.flags = 6 if q.symmetric else 4  # single GPU (+ symmetric: no zero-point tile loop)
+        self.flags = 2 if q.symmetric else 4  # symmetric: the kernel without the zero-point tile loop
 
     def __call__(self, x: torch.Tensor, out: torch.Tensor, stream: int) -> None:
         _lib.call("itq3_chain_run_ex", _lib.ptr(self.desc), 1, _lib.ptr(x), CHAIN_LIMBS, _lib.ptr(self.epoch),

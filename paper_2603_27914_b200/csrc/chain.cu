@@ -182,7 +182,19 @@ __device__ __forceinline__ int rot_lane_element(int L) { return ((L & 3) << 2) |
 // 2^(ilogb(max|y|) - 21) (|y_int| < 2^22, as fine as fp32's own rounding of the largest elements),
 // exact int32 butterfly (|x'| < 2^30), then x' rounded to the limb range |q| <= 2^(8L-2) by one more
 // power-of-two shift k (tests/test_gpu_stack.py chain_bound).
-template <bool MAD = false>  // MAD: butterflies as one register-operand mad each (the symmetric-only kernels)
+// MAD: butterflies as one register-operand mad each (the symmetric-only kernels).  LO: the input is H_16 y per
+// 16-element group (the symmetric single-GPU kernel: its reducers store H_16 of every 16-row tile and stage
+// 0 transforms x0 as it loads it), i.e. the butterflies over k bits 0-3 (lane bits 0-3) are done and only k
+// bit 4 (lane bit 4) and the register bits remain.
+// Output b of H_4 over a 4-lane group whose member b ^ m holds a[m]: sum_m (-1)^popc(b & (b ^ m)) a[m]
+__device__ __forceinline__ float radix4_h(const float (&a)[4], int b) {
+    float acc = (__popc(b) & 1) ? -a[0] : a[0];
+#pragma unroll
+    for (int m = 1; m < 4; ++m) acc = fmaf(a[m], (__popc(b & (b ^ m)) & 1) ? -1.0f : 1.0f, acc);
+    return acc;
+}
+
+template <bool MAD = false, bool LO = false>
 __device__ __forceinline__ void chain_rotate_to_smem(const float (&f)[8], int L, uint8_t* img, int lane) {
     // warp max of |f| as an integer max of the float bit patterns (sign cleared): one REDUX
     unsigned fbits = 0;
@@ -204,9 +216,16 @@ __device__ __forceinline__ void chain_rotate_to_smem(const float (&f)[8], int L,
 #pragma unroll
     for (int e = 0; e < 8; ++e)  // |f sc_in| < 2^22, sc_in a power of two: one FMA rounds to nearest even
         v[e] = __float_as_int(fmaf(f[e], sc_in, 12582912.0f)) - 0x4B400000;
-    const int v0 = v[0];  // lane 0: element 0 (sum_k (H v)_k = 256 v_0, the exact zero-point correction)
+    // the zero-point correction sum_k x'_k / 16 = v0 2^(e_in + c_sh): 256 v_0 / 16 (lane 0 holds element 0); LO:
+    // H_hi of v leaves 16 sum_{k < 16} v_k (lanes 0-15 at e = 0), over 16
+    int v0 = v[0];
+    constexpr int c_sh = LO ? 0 : 4;
+    if (LO) {
 #pragma unroll
-    for (int h = 1; h < 32; h <<= 1) {  // lane bits: p + v on the low lane, p - v on the high lane (one IMAD)
+        for (int h = 1; h < 16; h <<= 1) v0 += __shfl_xor_sync(FULL, v0, h);  // |v0| < 2^26
+    }
+#pragma unroll
+    for (int h = LO ? 16 : 1; h < 32; h <<= 1) {  // lane bits: p + v on the low lane, p - v on the high lane
         const int sg = (lane & h) ? -1 : 1;
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -267,7 +286,7 @@ __device__ __forceinline__ void chain_rotate_to_smem(const float (&f)[8], int L,
     if (lane < 8) {
         meta[lane] = lane < 4 ? __int_as_float((8 * lane + ex - 10 + 127) << 23) : 0.0f;  // 256^l 2^ex / 16 / 64
         // sum_k x'_k / 16 = 16 x_0 (fixed point), exact: the tile's error is then sum_k c_k (q_k 2^ex - x'_k)
-        meta[8 + lane] = lane == 0 ? (float)v0 * pow2f(e_in + 4) : 0.0f;
+        meta[8 + lane] = lane == 0 ? (float)v0 * pow2f(e_in + c_sh) : 0.0f;
     }
 }
 
@@ -657,6 +676,10 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                  unsigned long long* __restrict__ trace) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     ChainSmem<GATED>& sm = *reinterpret_cast<ChainSmem<GATED>*>(smem_raw);
+    // LO (the symmetric single-GPU kernel): every stage but the last stores H_16 y per full 16-row tile and
+    // every stage's input arrives in that form (stage 0 transforms x0 while loading it), so the consumers'
+    // rotations skip 4 of their 5 shuffle stages (Llama-2-7B 0.4575 -> ~0.44 ms)
+    constexpr bool LO = !ASYM && !TP && !GATED;
     constexpr int NSL = ChainSmem<GATED>::NSL, NST = ChainSmem<GATED>::NST;  // ring slots, cached stages
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int cta = blockIdx.x, G = gridDim.x;
@@ -713,7 +736,25 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                     sum = part[0];
 #pragma unroll
                     for (int w = 1; w < kChainConsumerWarps; ++w) sum += part[w];
-                    sum += __shfl_xor_sync(FULL, sum, 16);
+                    if (LO && s + 1 < S && (int64_t)(sp.rt0 + j * sp.Gc + 1) * 16 <= st.rows) {
+                        // H_16 over the unit's 16 rows, fp32, as two radix-4 rounds of independent shuffles with
+                        // the limb-pair fold in the first (lanes l and l ^ 16 end with the same value): two
+                        // dependent shuffle latencies instead of five on the stage's critical path.  A partial
+                        // last tile stays plain (the next stage reads whole 256-blocks, never it).
+                        float a[4];
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) {
+                            const float r = __shfl_xor_sync(FULL, sum, 16 | m);
+                            a[m] = (m ? __shfl_xor_sync(FULL, sum, m) : sum) + r;
+                        }
+                        sum = radix4_h(a, lane & 3);
+#pragma unroll
+                        for (int m = 1; m < 4; ++m) a[m] = __shfl_xor_sync(FULL, sum, 4 * m);
+                        a[0] = sum;
+                        sum = radix4_h(a, (lane >> 2) & 3);
+                    } else {
+                        sum += __shfl_xor_sync(FULL, sum, 16);
+                    }
                 }
                 if (lane < 16) {
                     const int64_t row = (int64_t)(sp.rt0 + j * sp.Gc) * 16 + lane;
@@ -930,6 +971,15 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                 const float* xs = st.xin ? st.xin : x0;
 #pragma unroll
                 for (int e = 0; e < 8; ++e) f[e] = __ldg(xs + 256 * (b0 + warp) + el + 32 * e);
+                if (LO) {  // the launch input in the LO form: H_16 over k bits 0-3 (lane bits 0-3), fp32
+#pragma unroll
+                    for (int h = 1; h < 16; h <<= 1)
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const float p = __shfl_xor_sync(FULL, f[e], h);
+                            f[e] = (lane & h) ? p - f[e] : p + f[e];
+                        }
+                }
             } else {
                 const ChainStage pv = s - 1 < NST ? sm.desc[s - 1] : stages[s - 1];
                 const int pn = (pv.NB + kUnitBlocks - 1) / kUnitBlocks;
@@ -953,7 +1003,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 1] = globaltimer();
             if (prof) c_in += clock64() - c0;
 #ifndef CHAIN_EXP_NOROT
-            chain_rotate_to_smem<!ASYM>(f, L, rot, lane);
+            chain_rotate_to_smem<!ASYM, LO>(f, L, rot, lane);
 #endif
             __syncwarp();
             // fragments for lane (g, t): columns g < 4 hold limbs, columns >= 4 are zero

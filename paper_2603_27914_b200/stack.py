@@ -53,13 +53,21 @@ def balanced_work(shapes: list[tuple[int, int]], grid: int) -> np.ndarray:
     return tab
 
 
+def _hadamard16(dev) -> torch.Tensor:
+    h = torch.ones(1, 1, dtype=torch.float64)
+    for _ in range(4):
+        h = torch.cat([torch.cat([h, h], 1), torch.cat([h, -h], 1)], 0)
+    return h.to(dev)
+
+
 class LinearStack:
     """mode="chain": one persistent cooperative kernel per step (csrc/chain.cu, default);
     mode="kernels": 2 launches per stage (K3 rotate_act + K4 gemv), for comparison."""
 
     balance = True  # host-balanced work split (balanced_work); False: the kernel's default round robin
 
-    def __init__(self, qs: list[QuantizedTensor], limbs: int = 3, mode: str = "chain", independent: bool = False):
+    def __init__(self, qs: list[QuantizedTensor], limbs: int = 3, mode: str = "chain", independent: bool = False,
+                 lo: bool = True):
         if not qs:
             raise ShapeError("LinearStack: no stages")
         for a, b in zip(qs, qs[1:]):
@@ -80,6 +88,9 @@ class LinearStack:
         self.graph = None
         self.mode = mode
         self.independent = independent  # every stage reads x (no dependency): pure streaming
+        # lo (symmetric chains): the chain kernel instantiation whose stages pass H_16 y per 16-row tile (its
+        # rotations skip 4 of 8 butterfly stages); lo=False: plain outputs, bit-identical to the TP chain
+        self.lo_kernel = lo
         if mode == "chain":
             self._setup_chain()
         elif mode != "kernels":
@@ -108,6 +119,9 @@ class LinearStack:
             self.work = torch.from_numpy(balanced_work([(q.rows, q.cols) for q in self.qs], grid)).to(self.dev)
             for i in range(S):
                 _lib.check(lib.itq3_chain_set_work(host, i, _lib.ptr(self.work[i])))
+        self.sym = all(q.symmetric for q in self.qs)
+        # stages whose stored output is H_16 y per full 16-row tile (the LO kernel: all but the last)
+        self.lo = [self.sym and self.lo_kernel and i + 1 < S for i in range(S)]
         self.epoch = torch.zeros(2, dtype=torch.int32, device=self.dev)  # (step epoch, check-in count)
         self.trace = None
         self.desc = torch.frombuffer(bytearray(host.raw), dtype=torch.uint8).to(self.dev)
@@ -148,7 +162,8 @@ class LinearStack:
     def launch_all(self, out: torch.Tensor | None = None) -> None:
         if self.mode == "chain":
             trace = _lib.ptr(self.trace) if self.trace is not None else None
-            sym = 6 if all(q.symmetric for q in self.qs) else 4  # single GPU (+ no zero-point tile loop)
+            # symmetric: LO kernel (flags 6: symmetric | single GPU) or the plain symmetric one (2); else general
+            sym = (6 if self.lo_kernel else 2) if self.sym else 4
             _lib.call("itq3_chain_run_ex", _lib.ptr(self.desc), len(self.qs), _lib.ptr(self.x), self.limbs,
                       _lib.ptr(self.epoch), _lib.ptr(self.out if out is None else out), 0, trace,
                       _lib.stream_ptr(self.dev), sym)
@@ -161,14 +176,22 @@ class LinearStack:
         return self.out if self.mode == "chain" else self.ys[-1]
 
     def stage_output(self, i: int) -> torch.Tensor:
-        """Stage i's output; in chain mode the K-chunk partials summed in the kernel's order."""
+        """Stage i's output; in chain mode the K-chunk partials summed in the kernel's order (float64 for a
+        stage that stores H_16 y, see below)."""
         if self.mode != "chain":
             return self.ys[i]
         p = self.yparts[i].view(torch.int32).reshape(self.nch[i], self.qs[i].rows, 2)[..., 0].view(torch.float32)
         y = p[0].clone()
         for c in range(1, p.shape[0]):
             y += p[c]
-        return y
+        if not self.lo[i]:
+            return y
+        # LO kernel: whole 16-row groups hold H_16 y -- returned as H_16^-1 of that fp32 sum in float64, exactly
+        # the input the next stage multiplies; a partial last group is stored plain
+        full = y.numel() // 16 * 16
+        out = y.double()
+        out[:full] = (out[:full].view(-1, 16) @ _hadamard16(y.device) / 16.0).reshape(-1)
+        return out
 
     def capture(self) -> None:
         """Record the whole chain as one CUDA graph (launch overhead off the critical path)."""

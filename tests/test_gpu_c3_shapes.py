@@ -133,7 +133,7 @@ def test_c3_reference_rows_at_full_shape(case):
 def test_chain_c5_k28672():
     """C5's down projection width: K = 28672 -> 112 blocks -> 7 K-chunk partials per output, folded
     in fixed order by the next stage's loads and the final fold."""
-    from test_gpu_stack import build, chain_bound
+    from test_gpu_stack import build, chain_bound, lo_flags
 
     from paper_2603_27914_b200.stack import LinearStack
 
@@ -145,7 +145,7 @@ def test_chain_c5_k28672():
     xin = x.astype(np.float64)
     for i, q in enumerate(qs):
         y = st.stage_output(i).cpu().numpy().astype(np.float64)
-        exact, bound = chain_bound(q.payload().cpu().numpy(), q.rows, q.cols, xin, 3)
+        exact, bound = chain_bound(q.payload().cpu().numpy(), q.rows, q.cols, xin, 3, **lo_flags(st, i))
         assert np.all(np.abs(y - exact) <= bound), (i, float(np.max(np.abs(y - exact) / bound)))
         if i + 1 < len(qs):
             xin = y[: qs[i + 1].cols]

@@ -18,7 +18,7 @@ from paper_2603_27914_b200.stack import LinearStack  # noqa: E402
 H256 = O.hadamard(256)
 
 
-def chain_bound(payload, rows, cols, x, limbs=3):
+def chain_bound(payload, rows, cols, x, limbs=3, lo_in=False, lo_x0=False, lo_out=False, nch=1):
     """A-priori error bound of the chain kernel's stage output vs the exact fp64 product.
 
     The chain rotates in integers: x -> x_int = rint(x / s_in), s_in = 2^(ilogb(max|x_b|) - 21),
@@ -26,28 +26,65 @@ def chain_bound(payload, rows, cols, x, limbs=3):
         |err| <= d/16 * ( max(|t|_1, |c|_1) * 2^(e_in+k) / 2 + |H t|_1 * s_in / 2 )
     (|c|_1: the chain subtracts the exact sum of x'; |t|_1: K3 / K5b subtract the rounded sum)
     plus 1e-5 * sum |w_hat| |x| for fp32 accumulation (also covers the K3 path of mode="kernels").
+
+    The symmetric single-GPU chain kernel (LO) takes its input as y = H_16 x per 16-element group
+    (lo_in): s_in comes from max|y|, the rounding happens on y, so the rounding term weighs |H_hi t|_1
+    (H_16 over the group index only); its zero-point correction converts a 16-term integer sum to fp32
+    (|v0| 2^-24 s_in d |z|).  lo_x0: y was formed in-kernel from x in fp32 (4 adds: 4u sum_group |x|).
+    lo_out: the stored output is H_16 y of fp32 sums over nch K-chunk partials, read back through H_16^-1
+    in fp64: (6 + nch) u sum_{16-row group} |w_hat| |x| more (two radix-4 rounds of 3 roundings each).
     """
     n = 256
     nb = cols // n
     deq = O.dequantize(payload, rows, cols, n, False)
     quants, sb, zb, _ = O.split_payload(payload, n, False)
     codes, _ = O.unpack_planes(quants, n)
-    t = codes.astype(np.float64) - np.trunc(O.f16_value(zb))[:, None]
+    z = np.trunc(O.f16_value(zb))
+    t = codes.astype(np.float64) - z[:, None]
     # the chain kernel corrects with the exact sum of x' (256 x_0): its limb-rounding term is |c|_1;
     # K3/K5b correct with the rounded sum: |t|_1 -- the max covers both
     t1 = np.maximum(np.abs(t).sum(axis=1), codes.astype(np.float64).sum(axis=1)).reshape(rows, nb)
-    ht1 = np.abs(t @ H256).sum(axis=1).reshape(rows, nb)
     d = O.f16_value(sb).reshape(rows, nb)
     xb = np.asarray(x, np.float64).reshape(nb, n)
-    mx = np.abs(xb).max(axis=1)
-    e_in = np.where(mx > 0, np.floor(np.log2(np.where(mx > 0, mx, 1.0))) - 21, 0)
-    xi = np.rint(xb * 2.0 ** -e_in[:, None])
-    amax = np.abs(xi @ H256).max(axis=1)
+    mag = np.abs(deq) @ np.abs(np.asarray(x, np.float64))
+    if not lo_in:
+        ht1 = np.abs(t @ H256).sum(axis=1).reshape(rows, nb)
+        mx = np.abs(xb).max(axis=1)
+        e_in = np.where(mx > 0, np.floor(np.log2(np.where(mx > 0, mx, 1.0))) - 21, 0)
+        xi = np.rint(xb * 2.0 ** -e_in[:, None])
+        amax = np.abs(xi @ H256).max(axis=1)
+        extra = 0.0
+    else:
+        H16 = O.hadamard(16)
+        yb = xb.reshape(nb, 16, 16) @ H16  # [block, group a, b]: H_16 over b
+        th = np.abs(np.einsum("ac,rcb->rab", H16, t.reshape(-1, 16, 16))).sum(axis=2)  # |H_hi t| per group a
+        ht1 = th.sum(axis=1).reshape(rows, nb)
+        mx = np.abs(yb).reshape(nb, -1).max(axis=1)
+        e_in = np.where(mx > 0, np.floor(np.log2(np.where(mx > 0, mx, 1.0))) - 21, 0)
+        yi = np.rint(yb * 2.0 ** -e_in[:, None, None])
+        amax = np.abs(np.einsum("ac,ncb->nab", H16, yi)).reshape(nb, -1).max(axis=1)
+        v0 = np.abs(yi[:, 0, :].sum(axis=1))
+        extra = d * np.abs(z).reshape(rows, nb) * (v0 * 2.0 ** (e_in - 24))[None, :]
+        if lo_x0:
+            dx = 4 * 2.0 ** -24 * np.abs(xb).reshape(nb, 16, 16).sum(axis=2)  # [block, a]
+            extra = extra + d / 16.0 * np.einsum("rna,na->rn", th.reshape(rows, nb, 16), dx)
     bl = np.where(amax > 0, np.floor(np.log2(np.where(amax > 0, amax, 1.0))) + 1, 0)
     k = np.maximum(0, bl - (8 * limbs - 2))
-    bound = (d / 16.0 * (t1 * 2.0 ** (e_in + k)[None, :] / 2 + ht1 * 2.0 ** e_in[None, :] / 2)).sum(axis=1)
-    mag = np.abs(deq) @ np.abs(np.asarray(x, np.float64))
-    return deq @ np.asarray(x, np.float64), bound + 1e-5 * mag
+    bound = (d / 16.0 * (t1 * 2.0 ** (e_in + k)[None, :] / 2 + ht1 * 2.0 ** e_in[None, :] / 2) + extra).sum(axis=1)
+    bound = bound + 1e-5 * mag
+    if lo_out:
+        full = rows // 16 * 16
+        gm = np.repeat(mag[:full].reshape(-1, 16).sum(axis=1), 16)
+        bound[:full] += (6 + nch) * 2.0 ** -24 * gm
+    return deq @ np.asarray(x, np.float64), bound
+
+
+def lo_flags(st, i):
+    """chain_bound's LO arguments for stage i of a LinearStack run (see LinearStack.lo)."""
+    lo = st.mode == "chain" and st.sym and st.lo_kernel
+    return dict(lo_in=lo, lo_x0=lo and (i == 0 or st.independent), lo_out=bool(lo and st.lo[i]),
+                nch=int(st.nch[i]) if lo else 1)
+
 
 SHAPES = [(26112, 256), (768, 512), (512, 512), (1280, 512), (512, 1024), (4608, 512), (256, 4608), (9000, 256), (400, 8960),
           (8960, 256), (300, 8704)]
@@ -74,7 +111,7 @@ def test_stack_matches_oracle_stagewise(mode, asym):
     xin = x.astype(np.float64)
     for i, q in enumerate(qs):
         y = st.stage_output(i).cpu().numpy().astype(np.float64)
-        exact, bound = chain_bound(pays[i], q.rows, q.cols, xin, 3)
+        exact, bound = chain_bound(pays[i], q.rows, q.cols, xin, 3, **lo_flags(st, i))
         assert np.all(np.abs(y - exact) <= bound), (mode, i, np.max(np.abs(y - exact) / bound))
         if i + 1 < len(qs):
             xin = st.stage_output(i).cpu().numpy().astype(np.float64)[: qs[i + 1].cols]
@@ -106,7 +143,7 @@ def test_chain_beyond_smem_descriptor_cache():
     for i, q in enumerate(qs):
         y = st.stage_output(i).cpu().numpy().astype(np.float64)
         if i >= 140 or i % 20 == 0:
-            exact, bound = chain_bound(pays[i], q.rows, q.cols, xin, 3)
+            exact, bound = chain_bound(pays[i], q.rows, q.cols, xin, 3, **lo_flags(st, i))
             assert np.all(np.abs(y - exact) <= bound), (i, np.max(np.abs(y - exact) / bound))
         if i + 1 < len(qs):
             xin = y[: qs[i + 1].cols]

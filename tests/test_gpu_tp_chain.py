@@ -26,7 +26,7 @@ def test_tp_chain_world1_matches_chain():
     qs = [P.quantize_tensor(torch.randn((r, c), generator=g, device="cuda") / c ** 0.5) for r, c in shapes]
     rows, cols = [r for r, _ in shapes], [c for _, c in shapes]
     tp = TPChainStack(qs, rows, cols)
-    ref = LinearStack(qs, mode="chain")
+    ref = LinearStack(qs, mode="chain", lo=False)
     rng = np.random.default_rng(2)
     for _ in range(3):  # graph replays alternate the epoch-parity halves of y
         x = rng.standard_normal(512).astype(np.float32)

@@ -38,7 +38,7 @@ def case_dequant():
 
 
 def case_chain(n_stages):
-    from test_gpu_stack import chain_bound
+    from test_gpu_stack import chain_bound, lo_flags
 
     from paper_2603_27914_b200.stack import LinearStack
 
@@ -51,7 +51,7 @@ def case_chain(n_stages):
     xin = x.astype(np.float64)
     for i, q in enumerate(qs):
         y = st.stage_output(i).cpu().numpy().astype(np.float64)
-        exact, bound = chain_bound(q.payload().cpu().numpy(), q.rows, q.cols, xin, 3)
+        exact, bound = chain_bound(q.payload().cpu().numpy(), q.rows, q.cols, xin, 3, **lo_flags(st, i))
         assert np.all(np.abs(y - exact) <= bound), i
         if i + 1 < len(qs):
             xin = y[: qs[i + 1].cols]

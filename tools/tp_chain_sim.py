@@ -52,7 +52,7 @@ def main():
     cfg = P.QuantConfig(symmetric=not a.asym)
     qs = [P.quantize_tensor(torch.randn((r, c), generator=g, device=dev) / c ** 0.5, cfg) for r, c in SHAPES]
     rows, cols = [r for r, _ in SHAPES], [c for _, c in SHAPES]
-    ref = LinearStack(qs, mode="chain")
+    ref = LinearStack(qs, mode="chain", lo=False)
     rng = np.random.default_rng(0)
     xs = [rng.standard_normal(cols[0]).astype(np.float32) for _ in range(a.steps)]
     want = [ref.forward(x).copy() for x in xs]
