@@ -441,14 +441,36 @@ __device__ void attn_part(const AttnParams& P, const unsigned long long* qkv, un
     const int lo = sp * chunk, hi = min(pos + 1, lo + chunk), n = max(0, hi - lo);
     float* kch = P.kc + (int64_t)kvh * P.ctx * HD;
     float* vch = P.vc + (int64_t)kvh * P.ctx * HD;
+    // the split's cached K and V rows (earlier tokens; the producer pulled them into L2) into registers
+    // while q / k / v of this token are pending: score rows p = lo + warp + 16 i, P V rows lo + c + 4 i
+    constexpr int KR = kAttnMaxChunk / kChainConsumerWarps, VR = kAttnMaxChunk / G;
+    float kr[KR][4], vr[VR];
+    {
+#pragma unroll
+        for (int i = 0; i < KR; ++i) {
+            const int p = lo + warp + kChainConsumerWarps * i;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) kr[i][j] = p < hi && p != pos ? kch[(int64_t)p * HD + lane + 32 * j] : 0.f;
+        }
+        const int c = t >> 7, dcol = t & (HD - 1);
+#pragma unroll
+        for (int i = 0; i < VR; ++i) {
+            const int p = lo + c + G * i;
+            vr[i] = p < hi && p != pos ? vch[(int64_t)p * HD + dcol] : 0.f;
+        }
+    }
     if (warp < G + 2) {
         const int base = warp < G ? (kvh * G + warp) * HD : (warp == G ? nh * HD + kvh * HD : (nh + nkv) * HD + kvh * HD);
+        float c0 = 0.f, s0 = 0.f, c1 = 0.f, s1 = 0.f;
+        if (warp <= G) {  // RoPE factors, loaded before the poll
+            c0 = __ldg(P.cosb + (int64_t)pos * (HD / 2) + lane);
+            s0 = __ldg(P.sinb + (int64_t)pos * (HD / 2) + lane);
+            c1 = __ldg(P.cosb + (int64_t)pos * (HD / 2) + lane + 32);
+            s1 = __ldg(P.sinb + (int64_t)pos * (HD / 2) + lane + 32);
+        }
         float v[4];  // dims lane, lane + 32, lane + 64, lane + 96
         tagged_load4(qkv + base, epoch, lane, v);
         if (warp <= G) {  // RoPE: pairs (i, i + 64)
-            const float c0 = __ldg(P.cosb + (int64_t)pos * (HD / 2) + lane), s0 = __ldg(P.sinb + (int64_t)pos * (HD / 2) + lane);
-            const float c1 = __ldg(P.cosb + (int64_t)pos * (HD / 2) + lane + 32),
-                        s1 = __ldg(P.sinb + (int64_t)pos * (HD / 2) + lane + 32);
             const float a0 = v[0], b0 = v[2], a1 = v[1], b1 = v[3];
             v[0] = a0 * c0 - b0 * s0;
             v[2] = a0 * s0 + b0 * c0;
@@ -471,10 +493,13 @@ __device__ void attn_part(const AttnParams& P, const unsigned long long* qkv, un
     for (int g = 0; g < G; ++g)
 #pragma unroll
         for (int j = 0; j < 4; ++j) qr[g][j] = qs[g * HD + lane + 32 * j];
-#pragma unroll 2
-    for (int p = lo + warp; p < hi; p += kChainConsumerWarps) {
-        const float* kp = p == pos ? kcur : kch + (int64_t)p * HD;
-        const float k0 = kp[lane], k1 = kp[lane + 32], k2 = kp[lane + 64], k3 = kp[lane + 96];
+#pragma unroll
+    for (int i = 0; i < KR; ++i) {
+        const int p = lo + warp + kChainConsumerWarps * i;
+        if (p >= hi) break;
+        const bool cur = p == pos;
+        const float k0 = cur ? kcur[lane] : kr[i][0], k1 = cur ? kcur[lane + 32] : kr[i][1],
+                    k2 = cur ? kcur[lane + 64] : kr[i][2], k3 = cur ? kcur[lane + 96] : kr[i][3];
         float d[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) d[g] = qr[g][0] * k0 + qr[g][1] * k1 + qr[g][2] * k2 + qr[g][3] * k3;
@@ -509,10 +534,11 @@ __device__ void attn_part(const AttnParams& P, const unsigned long long* qkv, un
         float acc[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) acc[g] = 0.f;
-#pragma unroll 4
-        for (int i = c; i < n; i += G) {
-            const int p = lo + i;
-            const float v = p == pos ? vcur[dcol] : vch[(int64_t)p * HD + dcol];
+#pragma unroll
+        for (int k = 0; k < VR; ++k) {
+            const int i = c + G * k;
+            if (i >= n) break;
+            const float v = lo + i == pos ? vcur[dcol] : vr[k];
 #pragma unroll
             for (int g = 0; g < G; ++g) acc[g] += ps[g * kAttnMaxChunk + i] * v;
         }
@@ -892,6 +918,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         if (GATED && (st.asym & (256 | 512))) {  // decoder attention stages (no weights, no ring units)
             const AttnParams& P = *reinterpret_cast<const AttnParams*>(st.tiled);
             const ChainStage pv = s - 1 < NST ? sm.desc[s - 1] : stages[s - 1];
+            if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 0] = globaltimer();
             if (st.asym & 256) {
                 consumer_sync();  // every consumer warp is done with its rotation scratch
                 for (int item = cta; item < P.nkv * P.S; item += G)
@@ -899,6 +926,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
             } else if (tid < kAttnHD) {
                 for (int h = cta; h < P.nh; h += G) attn_comb(P, pv.y, st.y, h, epoch, tid);
             }
+            if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 3] = globaltimer();
             continue;
         }
         if (!active) continue;
@@ -1279,8 +1307,14 @@ static int chain_run(const void* d_desc, int n_stages, const float* x0, int limb
     }
     static std::atomic<unsigned long long> smem_attr{0}, smem_attr_tr{0};
     const int smem = (int)sizeof(ChainSmem<GATED>);
+#ifdef CHAIN_GATED_TRACE  // experiment builds: a traced twin of the gated single-GPU kernel (tools/trace_decoder.py)
+    const bool tr = d_trace != nullptr;
+    auto kern = tr ? (GATED ? chain_kernel<true, true, true, false> : chain_kernel<false, true, true, true>)
+                   : chain_kernel<GATED, false, ASYM, TP>;
+#else
     const bool tr = !GATED && d_trace;  // the trace instantiation is the asymmetric-capable plain kernel
     auto kern = tr ? chain_kernel<false, true, true, true> : chain_kernel<GATED, false, ASYM, TP>;
+#endif
     if (int rc = ensure_smem_attr(kern, smem, tr ? smem_attr_tr : smem_attr, "chain: smem attribute")) return rc;
     if (grid <= 0) grid = device_sms();
     cudaLaunchConfig_t cfg = {};

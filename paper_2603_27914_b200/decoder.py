@@ -158,6 +158,9 @@ class DecoderStack:
         if -(-max_ctx // self.splits) > 64:  # positions per split (the chain's score scratch)
             raise ValueError("DecoderStack: ceil(max_ctx / attention splits) must be <= 64")
         self.res = [None] + [torch.zeros(self.h, dtype=torch.int64, device=self.dev) for _ in range(layers)]
+        # residual + o of layer L (tagged), published by its gate_up stage: the next qkv stage's norm input is
+        # then res_mid + down (two producers, one poll loop) instead of res + o + down
+        self.res_mid = [torch.zeros(self.h, dtype=torch.int64, device=self.dev) for _ in range(layers)]
         self.att_y = [torch.zeros(self.h, dtype=torch.int64, device=self.dev) for _ in range(layers)]
         self.part_y = [torch.zeros(self.nkv * self.splits * 4 * 130, dtype=torch.int64, device=self.dev)
                        for _ in range(layers)]
@@ -175,7 +178,8 @@ class DecoderStack:
             stages.append(dict(attn=512, params=self.attn_params[li], y=self.att_y[li]))
             o_idx = len(stages)
             stages.append(dict(q=o_w))
-            stages.append(dict(q=gu_w, flags=NORM_IN | RESID_IN, xin=self.gain[li][1], xres=self.res[li]))
+            stages.append(dict(q=gu_w, flags=NORM_IN | RESID_IN | XOUT, xin=self.gain[li][1], xres=self.res[li],
+                               xout=self.res_mid[li]))
             if li + 1 < layers:
                 nxt = dict(q=self.q[li + 1][0], xin=self.gain[li + 1][0])
             elif self.lm_head is not None:
@@ -186,7 +190,7 @@ class DecoderStack:
                 stages.append(dict(q=down_w, flags=GATED | ADD_OUT | ADD_OUT0, ref=o_idx, xres=self.res[li]))
             else:
                 stages.append(dict(q=down_w, flags=GATED))
-                nxt.update(flags=NORM_IN | RESID2_IN | XOUT, ref=o_idx, xres=self.res[li], xout=self.res[li + 1])
+                nxt.update(flags=NORM_IN | RESID_IN | XOUT, xres=self.res_mid[li], xout=self.res[li + 1])
                 stages.append(nxt)
         self.n_stages = len(stages)
         self.token_chain = _Chain(stages, self.logits if self.lm_head is not None else self.out, self.dev)
