@@ -562,56 +562,59 @@ __device__ void attn_part(const AttnParams& P, const unsigned long long* qkv, un
     consumer_sync();  // the scratch is free for the next item / stage
 }
 
-// head h: combine the S (<= 32) partials of its kv head into 128 tagged outputs (threads 0..127).  The
-// loads of a poll are independent (lane j fetches split j's max and sum; every thread its weighted-V
-// words, 8 splits per round trip), so a combine costs ~S / 8 L2 round trips, not S.
+// head h: combine the S (<= 32) partials of its kv head into 128 tagged outputs, with all 512 consumer
+// threads: thread (group q = t >> 7, dim d) loads the weighted-V words of splits q per .. q per + per - 1
+// (per = ceil(S / 4) <= 8) and lane j of every warp split j's (max, sum), all in ONE poll loop -- one L2
+// round trip once the partials are there -- then the four groups' sums meet in shared memory in a fixed
+// order (deterministic).  scratch: >= 4 x 128 floats.
 __device__ void attn_comb(const AttnParams& P, const unsigned long long* part, unsigned long long* att, int h,
-                          unsigned epoch, int t) {
-    constexpr int HD = kAttnHD, G = kAttnG, kGrp = 8;
-    const int kvh = h / G, g = h - kvh * G, S = P.S, lane = t & 31;
+                          unsigned epoch, int t, float* scratch) {
+    constexpr int HD = kAttnHD, G = kAttnG, Q = 4, kPer = 8;
+    const int kvh = h / G, g = h - kvh * G, S = P.S, lane = t & 31, q = t >> 7, dcol = t & (HD - 1);
+    const int per = (S + Q - 1) / Q;
     const unsigned long long* base = part + ((int64_t)kvh * S * G + g) * kAttnWords;  // split j: + j G kAttnWords
-    float mj = -INFINITY, sj = 0.f;
-    for (;;) {  // split statistics: lane j holds split j's (max, sum)
+    float mj = -INFINITY, sj = 0.f, a[kPer];
+    for (;;) {
         bool ok = true;
-        if (lane < S) {
+        if (lane < S) {  // split statistics: lane j holds split j's (max, sum)
             const unsigned long long w0 = ld_u64_relaxed(base + (int64_t)lane * G * kAttnWords);
             const unsigned long long w1 = ld_u64_relaxed(base + (int64_t)lane * G * kAttnWords + 1);
             ok = (unsigned)(w0 >> 32) == epoch && (unsigned)(w1 >> 32) == epoch;
             mj = __uint_as_float((unsigned)w0);
             sj = __uint_as_float((unsigned)w1);
         }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            a[u] = 0.f;
+            const int j = q * per + u;
+            if (u < per && j < S) {
+                const unsigned long long w = ld_u64_relaxed(base + (int64_t)j * G * kAttnWords + 2 + dcol);
+                ok &= (unsigned)(w >> 32) == epoch;
+                a[u] = __uint_as_float((unsigned)w);
+            }
+        }
         if (__all_sync(FULL, ok)) break;
     }
     float m = mj;
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(FULL, m, o));
     const float fj = mj == -INFINITY ? 0.f : __expf(mj - m);  // lane j's split weight
-    float num = 0.f, den = 0.f;
-    for (int j0 = 0; j0 < S; j0 += kGrp) {  // fixed split order: deterministic
-        float a[kGrp];
-        for (;;) {
-            bool ok = true;
+    float num = 0.f;
 #pragma unroll
-            for (int u = 0; u < kGrp; ++u) {
-                a[u] = 0.f;
-                if (j0 + u < S) {
-                    const unsigned long long w = ld_u64_relaxed(base + (int64_t)(j0 + u) * G * kAttnWords + 2 + t);
-                    ok &= (unsigned)(w >> 32) == epoch;
-                    a[u] = __uint_as_float((unsigned)w);
-                }
-            }
-            if (__all_sync(FULL, ok)) break;
-        }
-#pragma unroll
-        for (int u = 0; u < kGrp; ++u) {
-            const float f = __shfl_sync(FULL, fj, (j0 + u) & 31), sden = __shfl_sync(FULL, sj * fj, (j0 + u) & 31);
-            if (j0 + u < S) {
-                num += f * a[u];
-                den += sden;
-            }
-        }
+    for (int u = 0; u < kPer; ++u) {
+        const int j = q * per + u;
+        const float f = __shfl_sync(FULL, fj, j & 31);
+        if (u < per && j < S) num += f * a[u];
     }
-    const float o = den > 0.f ? num / den : 0.f;  // den == 0: every split empty (position out of range)
-    st_u64_relaxed(att + (int64_t)h * HD + t, ((unsigned long long)epoch << 32) | __float_as_uint(o));
+    scratch[q * HD + dcol] = num;
+    consumer_sync();
+    if (q == 0) {
+        float den = 0.f;
+        for (int j = 0; j < S; ++j) den += __shfl_sync(FULL, sj * fj, j);
+        const float o = scratch[dcol] + scratch[HD + dcol] + scratch[2 * HD + dcol] + scratch[3 * HD + dcol];
+        const float r = den > 0.f ? o / den : 0.f;  // den == 0: every split empty (position out of range)
+        st_u64_relaxed(att + (int64_t)h * HD + dcol, ((unsigned long long)epoch << 32) | __float_as_uint(r));
+    }
+    consumer_sync();  // the scratch is free again
 }
 
 
@@ -923,8 +926,9 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                 consumer_sync();  // every consumer warp is done with its rotation scratch
                 for (int item = cta; item < P.nkv * P.S; item += G)
                     attn_part(P, pv.y, st.y, item, epoch, warp, lane, reinterpret_cast<float*>(&sm.rot[0][0]));
-            } else if (tid < kAttnHD) {
-                for (int h = cta; h < P.nh; h += G) attn_comb(P, pv.y, st.y, h, epoch, tid);
+            } else {
+                for (int h = cta; h < P.nh; h += G)
+                    attn_comb(P, pv.y, st.y, h, epoch, tid, reinterpret_cast<float*>(&sm.rot[0][0]));
             }
             if (trace && tid == 0) trace[((int64_t)cta * S + s) * 4 + 3] = globaltimer();
             continue;

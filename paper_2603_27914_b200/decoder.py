@@ -157,6 +157,8 @@ class DecoderStack:
         self.splits = int(os.environ.get("ITQ3_ATTN_SPLITS", "0")) or max(1, per_sm - per_sm % 8 if per_sm >= 8 else per_sm)
         if -(-max_ctx // self.splits) > 64:  # positions per split (the chain's score scratch)
             raise ValueError("DecoderStack: ceil(max_ctx / attention splits) must be <= 64")
+        if self.splits > 32:  # the combine reads split statistics one per lane
+            raise ValueError("DecoderStack: at most 32 attention splits per kv head")
         self.res = [None] + [torch.zeros(self.h, dtype=torch.int64, device=self.dev) for _ in range(layers)]
         # residual + o of layer L (tagged), published by its gate_up stage: the next qkv stage's norm input is
         # then res_mid + down (two producers, one poll loop) instead of res + o + down
