@@ -632,7 +632,10 @@ struct ChainSmem {
     alignas(128) uint8_t ring[NSL][kSlotBytes];
     alignas(16) uint8_t rot[kChainConsumerWarps][kActSmemBlock];  // per-warp rotation scratch (attention scratch)
     float part[NSL][kChainConsumerWarps][2][16];        // per-warp row partials of a unit (limb pairs t = 0, 1)
-    float normsq[kChainConsumerWarps];                  // per-warp sums of squares (RMSNorm input stages)
+    // per-warp sums of squares of the last 16 RMSNorm input stages: every stage a CTA takes part in has >= 1
+    // unit, and the consumers run at most NSL < 15 units ahead of the reducers, so a buffer is never rewritten
+    // before the reducers are done with it
+    float normsq[16][kChainConsumerWarps];
     uint64_t full[NSL];
     uint64_t empty[NSL];
     uint64_t parts[NSL];  // 16 warps' partials of the unit in this slot are written
@@ -641,6 +644,7 @@ struct ChainSmem {
 
 static_assert(sizeof(ChainSmem<false>) <= 227 * 1024, "chain kernel shared memory exceeds the 227 KB per-CTA limit");
 static_assert(sizeof(ChainSmem<true>) <= 227 * 1024, "chain kernel shared memory exceeds the 227 KB per-CTA limit");
+static_assert(ChainSmem<true>::NSL < 15, "sm.normsq reuse needs fewer ring slots than RMSNorm buffers - 1");
 
 __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
     unsigned v;
@@ -740,12 +744,17 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         // Sums each unit's 16 per-warp row partials in warp order (deterministic), stores the
         // tagged outputs and releases the ring slot.  Runs behind the compute warps so they
         // never wait on each other.
-        int seq = 0;
+        int seq = 0, nrm = 0;
         for (int s = 0; s < S; ++s) {
             ChainStage st;
             StageSplit sp;
             if (!stage_get(sm, stages, cta, G, s, st, sp)) continue;
             const int n_units = (st.RT - 1 - sp.rt0) / sp.Gc + 1;
+            // RMSNorm input stage: outputs times rsqrt(mean(x^2) + 1e-5), the sums of squares the consumer
+            // warps left in sm.normsq[nb]
+            const bool norm = GATED && (st.asym & 4);
+            const int nb = nrm & 15;
+            nrm += norm;
             // y offset of this CTA's K-chunk (+ the epoch-parity half for tensor-parallel stages)
             const int64_t yoff = (int64_t)sp.ch * st.yrows + st.row0 +
                                  (TP && st.npeer ? (int64_t)(epoch & 1u) * sp.nch * st.yrows : 0);
@@ -783,6 +792,12 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                         sum = radix4_h(a, (lane >> 2) & 3);
                     } else {
                         sum += __shfl_xor_sync(FULL, sum, 16);
+                    }
+                    if (norm) {
+                        float tot = 0.f;
+#pragma unroll
+                        for (int w = 0; w < kChainConsumerWarps; ++w) tot += sm.normsq[nb][w];
+                        sum *= rsqrtf(tot / (float)st.cols + 1e-5f);
                     }
                 }
                 if (lane < 16) {
@@ -913,6 +928,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     uint8_t* rot = sm.rot[warp];
     if (!TRACE) trace = nullptr;
     const bool prof = trace != nullptr && cta == 0;
+    int nrm = 0;  // RMSNorm input stages done (sm.normsq buffer nrm & 15; the reducers count alike)
     long long c_wait = 0, c_tile = 0, c_rot = 0, c_in = 0, c_start = clock64();
     for (int s = 0; s < S; ++s) {
         ChainStage st;
@@ -940,12 +956,11 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         const int b0 = sp.ch * kUnitBlocks;
         const int nb = min(kUnitBlocks, st.NB - b0);
         const bool has_block = warp < nb;
-        float nscale = 1.f;
         float xv[8];  // RMSNorm input stages: this warp's block of the (residual) input before the norm
         if (GATED && (st.asym & 4)) {
             // RMSNorm input stage (decoder; host-checked cols <= 4096, so this CTA's chunk is the whole
-            // input vector): every consumer warp adds its block's squares, one named barrier, and the
-            // scale multiplies the input as it is loaded below.  Flag 16 (residual input, s >= 1): the
+            // input vector): every consumer warp leaves its block's sum of squares for the reducers, which
+            // scale the stage's outputs (below).  Flag 16 (residual input, s >= 1): the
             // input is x0 + the previous stage's output -- the residual stream after an o projection
             // folded into the same launch (h + W_o att, then RMSNorm, as the reference step orders it).
             float ss = 0.f;
@@ -983,12 +998,11 @@ __global__ void __launch_bounds__(kChainThreads, 1)
                 for (int e = 0; e < 8; ++e) ss += xv[e] * xv[e];
             }
             for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
-            if (lane == 0) sm.normsq[warp] = ss;
-            consumer_sync();
-            float tot = 0.f;
-#pragma unroll
-            for (int w = 0; w < kChainConsumerWarps; ++w) tot += sm.normsq[w];
-            nscale = rsqrtf(tot / (float)st.cols + 1e-5f);
+            // no CTA barrier: the GEMV is linear, so the norm's scalar rsqrt(mean(x^2) + eps) multiplies the
+            // stage's outputs in the reducer (which reads these sums after the unit's partials barrier); each
+            // warp goes on with its own block as soon as it has arrived
+            if (lane == 0) sm.normsq[nrm & 15][warp] = ss;
+            ++nrm;
         }
         uint2 bf[8];
         float fcx = 0.f, corr = 0.f;
@@ -996,9 +1010,9 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         if (has_block) {
             float f[8];
             if (GATED && (st.asym & 4)) {
-                // RMSNorm input: x * rsqrt(mean(x^2) + 1e-5) * gain (gain in st.xin)
+                // RMSNorm input: x * gain (gain in st.xin); the reducer applies rsqrt(mean(x^2) + 1e-5)
 #pragma unroll
-                for (int e = 0; e < 8; ++e) f[e] = xv[e] * nscale * __ldg(st.xin + 256 * (b0 + warp) + el + 32 * e);
+                for (int e = 0; e < 8; ++e) f[e] = xv[e] * __ldg(st.xin + 256 * (b0 + warp) + el + 32 * e);
             } else if (s == 0 || st.xin) {
                 const float* xs = st.xin ? st.xin : x0;
 #pragma unroll
