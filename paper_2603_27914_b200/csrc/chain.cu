@@ -1358,10 +1358,13 @@ static int chain_run(const void* d_desc, int n_stages, const float* x0, int limb
 // weight stage is symmetric (no zero-points); bit 2 = single GPU (no tensor-parallel stage).  Bits 1 and 2 pick
 // instantiations without the zero-point tile loop / the peer-store paths (faster: the kernel is at its
 // register cap, so every compiled path shapes the tile loop); a stage needing what was left out traps.
-// Instantiated: plain general, plain symmetric (single-GPU / tensor-parallel), gated general, gated single-GPU.
+// Instantiated: plain general, plain symmetric (single-GPU / tensor-parallel), gated general, gated single-GPU
+// (general / symmetric).
 extern "C" int itq3_chain_run_ex(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch,
                                  float* out, int grid, void* d_trace, void* stream, int flags) {
     const bool gated = flags & 1, sym = flags & 2, single = flags & 4;
+    if (gated && sym && single)
+        return chain_run<true, false, false>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
     if (gated)
         return single ? chain_run<true, true, false>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream)
                       : chain_run<true, true, true>(d_desc, n_stages, x0, limbs, d_epoch, out, grid, d_trace, stream);
