@@ -254,9 +254,12 @@ int itq3_chain_run(const void* d_desc, int n_stages, const float* x0, int limbs,
 /* the same, for chains with gated stages (descriptor flag bit 1) */
 int itq3_chain_run_gated(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch, float* out,
                          int grid, void* d_trace, void* stream);
-/* flags: bit 0 = gated chain (itq3_chain_run_gated), bit 1 = every weight stage symmetric (plain chains: no
- * zero-point tile loop), bit 2 = single GPU (no tensor-parallel stage: no peer-store paths); the specialised
- * instantiations are faster, and a stage needing what was left out traps the launch. */
+/* flags: bit 0 = gated chain (itq3_chain_run_gated), bit 1 = every weight stage symmetric (no zero-point tile
+ * loop), bit 2 = single GPU (no tensor-parallel stage: no peer-store paths); the specialised instantiations
+ * are faster, and a stage needing what was left out traps the launch.  Plain chains with bits 1 and 2 (flags 6)
+ * pass H_16 y between stages: every stage but the last stores H_16 (fp32) of each full 16-row tile of its
+ * tagged outputs (a partial last tile plain) and reads its input in that form (stage 0 transforms x0 itself);
+ * `out` and the last stage's outputs are plain.  Flags 2 = the same kernel family with plain stage outputs. */
 int itq3_chain_run_ex(const void* d_desc, int n_stages, const float* x0, int limbs, unsigned* d_epoch, float* out,
                       int grid, void* d_trace, void* stream, int flags);
 
