@@ -245,9 +245,10 @@ __device__ __forceinline__ void chain_rotate_to_smem(const float (&f)[8], int L,
                 v[e] = lo + hi;
                 v[e + hh] = lo - hi;
             }
-    unsigned amax = 0;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) amax = max(amax, (unsigned)abs(v[e]));
+    // max |v| as max(max v, -min v) over three-input integer min / max (7 instructions, not 8 IABS + 8 max)
+    const int vmx = __vimax3_s32(__vimax3_s32(v[0], v[1], v[2]), __vimax3_s32(v[3], v[4], v[5]), max(v[6], v[7]));
+    const int vmn = __vimin3_s32(__vimin3_s32(v[0], v[1], v[2]), __vimin3_s32(v[3], v[4], v[5]), min(v[6], v[7]));
+    unsigned amax = (unsigned)max(vmx, -vmn);
     amax = __reduce_max_sync(FULL, amax);
     // shift k so that |q| <= 2^(8L-2) (limbs never overflow): bitlen(amax) - k <= 8L - 2
     const int bl = 32 - __clz(amax);
