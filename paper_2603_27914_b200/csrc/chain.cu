@@ -494,23 +494,33 @@ __device__ void attn_part(const AttnParams& P, const unsigned long long* qkv, un
     for (int g = 0; g < G; ++g)
 #pragma unroll
         for (int j = 0; j < 4; ++j) qr[g][j] = qs[g * HD + lane + 32 * j];
+    // the warp's KR x G scores (positions lo + warp + 16 i beyond hi give 0 and are not stored), reduced
+    // over the lanes by a transposed butterfly: each exchange halves the values a lane keeps, so the 16
+    // sums take 16 shuffles in 5 dependent rounds (not 5 rounds per value); the additions pair exactly
+    // as the plain butterfly's, so the sums are bit-identical
+    static_assert(KR * G == 16, "the transposed reduction handles 16 values per lane");
+    float d[KR * G];
 #pragma unroll
     for (int i = 0; i < KR; ++i) {
-        const int p = lo + warp + kChainConsumerWarps * i;
-        if (p >= hi) break;
-        const bool cur = p == pos;
+        const bool cur = lo + warp + kChainConsumerWarps * i == pos;
         const float k0 = cur ? kcur[lane] : kr[i][0], k1 = cur ? kcur[lane + 32] : kr[i][1],
                     k2 = cur ? kcur[lane + 64] : kr[i][2], k3 = cur ? kcur[lane + 96] : kr[i][3];
-        float d[G];
 #pragma unroll
-        for (int g = 0; g < G; ++g) d[g] = qr[g][0] * k0 + qr[g][1] * k1 + qr[g][2] * k2 + qr[g][3] * k3;
+        for (int g = 0; g < G; ++g) d[i * G + g] = qr[g][0] * k0 + qr[g][1] * k1 + qr[g][2] * k2 + qr[g][3] * k3;
+    }
 #pragma unroll
-        for (int o = 16; o; o >>= 1)
+    for (int o = 16, w = 8; o >= 2; o >>= 1, w >>= 1) {  // lane keeps values [w * bit, w * bit + w)
+        const bool up = lane & o;
 #pragma unroll
-            for (int g = 0; g < G; ++g) d[g] += __shfl_xor_sync(FULL, d[g], o);
-        if (lane == 0)
-#pragma unroll
-            for (int g = 0; g < G; ++g) ps[g * kAttnMaxChunk + p - lo] = d[g];
+        for (int j = 0; j < w; ++j) {
+            const float send = up ? d[j] : d[j + w], keep = up ? d[j + w] : d[j];
+            d[j] = keep + __shfl_xor_sync(FULL, send, o);
+        }
+    }
+    d[0] += __shfl_xor_sync(FULL, d[0], 1);  // value lane >> 1 = (position i, head g) = (v >> 2, v & 3)
+    {
+        const int v = lane >> 1, p = lo + warp + kChainConsumerWarps * (v / G);
+        if (!(lane & 1) && p < hi) ps[(v % G) * kAttnMaxChunk + p - lo] = d[0];
     }
     consumer_sync();
     if (warp < G) {
