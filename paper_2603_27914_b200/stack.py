@@ -62,7 +62,13 @@ def _hadamard16(dev) -> torch.Tensor:
 
 class LinearStack:
     """mode="chain": one persistent cooperative kernel per step (csrc/chain.cu, default);
-    mode="kernels": 2 launches per stage (K3 rotate_act + K4 gemv), for comparison."""
+    mode="kernels": 2 launches per stage (K3 rotate_act + K4 gemv), for comparison.
+
+    independent=True: every stage reads x (no dependency between stages) -- the streaming reference pass.
+    lo (symmetric chains): True runs the instantiation that passes H_16 y between stages (faster; its
+    intermediate stage outputs are stored in that form and `stage_output` undoes it), False the one with plain
+    stage outputs (bit-identical to the tensor-parallel chain).  The final output is the same either way up to
+    the fp32 rounding of the H_16 transforms (tests/test_gpu_stack.py bounds both)."""
 
     balance = True  # host-balanced work split (balanced_work); False: the kernel's default round robin
 
