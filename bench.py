@@ -65,6 +65,7 @@ METRIC = "decode tokens/sec (batch-1 fused IFWHT-dequant GEMV chain, %s linear s
 WORKLOAD = "%s linear stack decode: %d layers x (%s), batch 1" % (
     MODEL, N_LAYERS, ", ".join(f"{n} {r}x{c}" for n, r, c in LAYER_SHAPES))
 FALLBACK_HBM_GBS = 6650.0
+FALLBACK_BF16_TFLOPS = 1590.0  # B200_PROFILING.md's fallback dense bf16 figure (used only without MEASURED_PEAKS.json)
 
 
 def dist_env():
@@ -471,6 +472,9 @@ def measure_c3(dev, reps: int = 20) -> dict:
     except (OSError, ValueError):
         pass
     bf16 = float(peaks.get("bf16_tflops", 0) or 0) or None
+    bf16_src = "measured (MEASURED_PEAKS.json bf16_tflops)"
+    if bf16 is None:
+        bf16, bf16_src = FALLBACK_BF16_TFLOPS, "fallback (B200_PROFILING.md)"
     hbm, _ = measured_peak()
     out = {"shape": f"{rows}x{K}", "weight_copies": len(copies)}
     for M in (16, 64, 2048):
@@ -509,8 +513,8 @@ def measure_c3(dev, reps: int = 20) -> dict:
              "us": ms * 1e3, "kernel_us": ms_k * 1e3, "tflops": flops / ms / 1e9, "kernel_tflops": flops / ms_k / 1e9,
              "weight_bytes": wbytes, "kernel_weight_gbps": wbytes / ms_k / 1e6,
              "kernel_frac_hbm": wbytes / ms_k / 1e6 / hbm}
-        if bf16:
-            r["kernel_frac_bf16_measured"] = r["kernel_tflops"] / bf16
+        r["kernel_frac_bf16"] = r["kernel_tflops"] / bf16
+        r["bf16_peak_tflops"], r["bf16_peak_source"] = bf16, bf16_src
         r["kernel_frac_int8_nominal"] = r["kernel_tflops"] / INT8_NOMINAL_TOPS
         out[f"m{M}"] = r
     del copies
