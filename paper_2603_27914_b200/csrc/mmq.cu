@@ -216,6 +216,7 @@ struct PairSmem {
 struct PairWork {
     int tiles_r, tiles_n, ks, NS;  // NS = stages along K
     int F, R, kt;                  // tail split (kt = 1: none)
+    int bsub;                      // BN = 128 tiles over a 256-token activation layout (itq3_mmq_block_n(m) = 256)
     __device__ int items() const { return F + R * kt; }
     // split = -1 for an item written straight to Y
     __device__ void decode(int it, int& tr, int& tn, int& s0, int& s1, int& split) const {
@@ -289,7 +290,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
                 int tr, tn, s0, s1, split;
                 wk.decode(it, tr, tn, s0, s1, split);
                 const uint8_t* wsrc = wrec + ((int64_t)(2 * tr + rank) * wk.NS) * wbytes;
-                const uint8_t* bsrc = act + ((int64_t)(2 * tn + rank) * wk.NS) * (BN * 128);
+                // B: this CTA's 64- or 128-token half, one stage = two 64-k SW128 tiles.  bsub (128-token tiles
+                // over the 256-token layout): the half is rows 64 rank .. of the layout's 128-token half tn, i.e.
+                // the same 8 KB of each 16 KB tile (the swizzle repeats every 8 rows): two copies per stage
+                const bool bsub = BN == 128 && wk.bsub;
+                const uint8_t* bsrc = bsub ? act + (int64_t)tn * wk.NS * (256 * 128) + rank * 8192
+                                           : act + ((int64_t)(2 * tn + rank) * wk.NS) * (BN * 128);
                 for (int st = s0; st < s1; ++st, ++g) {
                     const int s = g % kPairNS;
                     {
@@ -300,7 +306,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMmqThreads, 1)
                     const long long ti0 = clock64();
                     mbar_expect_tx_(&sm.full[s], wbytes + ((dflags & 1) ? 0 : BN * 128));
                     bulk_g2s_(sm.w[s], wsrc + (int64_t)st * wbytes, wbytes, &sm.full[s]);
-                    if (!(dflags & 1)) bulk_g2s_(sm.b[s], bsrc + (int64_t)st * (BN * 128), BN * 128, &sm.full[s]);
+                    if (dflags & 1) {
+                    } else if (bsub) {
+                        bulk_g2s_(sm.b[s], bsrc + (int64_t)st * 32768, 8192, &sm.full[s]);
+                        bulk_g2s_(sm.b[s] + 8192, bsrc + (int64_t)st * 32768 + 16384, 8192, &sm.full[s]);
+                    } else {
+                        bulk_g2s_(sm.b[s], bsrc + (int64_t)st * (BN * 128), BN * 128, &sm.full[s]);
+                    }
                     t_issue += clock64() - ti0;
                 }
             }
@@ -954,10 +966,21 @@ static int mmq_max_clusters() {
     return n;
 }
 
-static int mmq_splits(int64_t rows, int64_t cols, int64_t m) {
+// Pair tile width: the activation layout's (itq3_mmq_block_n), except that a 256-token layout runs 128-token
+// tiles (PairWork::bsub) when 256-token tiles would leave more than half of the CTA pairs idle and K <= 4096
+// -- twice the tiles instead of split-K's fp32 partial slabs and reduce pass (4096 x 4096, M = 512: 33.7 ->
+// 21.3 us; 1024 x 4096, M = 2048: 32.0 -> 21.3 us).  At larger K the doubled A expansion costs more than the
+// split-K traffic it saves (4096 x 14336, M = 256: 37.7 -> 42.8 us), so those keep 256-token tiles.
+static int mmq_pick_bn(int64_t rows, int64_t cols, int64_t m) {
+    if (itq3_mmq_block_n(m) == 128) return 128;
+    if (cols > 4096) return 256;
+    const int64_t tiles = (int64_t)(mmq_rows_pad(rows) / 256) * ((m + 255) / 256);
+    return tiles * 2 <= mmq_max_clusters() ? 128 : 256;
+}
+
+static int mmq_splits(int64_t rows, int64_t cols, int64_t m, int BN) {
     // split K only when the output tiles leave more than half of the CTA pairs idle, so the fp32
     // partial traffic never costs more than the idle SMs it recovers; >= 4 stages (512 k) per split
-    const int BN = itq3_mmq_block_n(m);
     const int64_t tiles = (int64_t)(mmq_rows_pad(rows) / 256) * ((m + BN - 1) / BN);
     const int64_t pairs = mmq_max_clusters();
     if (tiles * 2 > pairs) return 1;
@@ -996,7 +1019,8 @@ static int launch_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int asym, 
     PairWork wk;
     wk.tiles_r = mmq_rows_pad(rows) / 256;
     wk.tiles_n = (int)((m + BN - 1) / BN);
-    wk.ks = ws ? mmq_splits(rows, cols, m) : 1;
+    wk.ks = ws ? mmq_splits(rows, cols, m, BN) : 1;
+    wk.bsub = BN == 128 && itq3_mmq_block_n(m) == 256;
     wk.NS = (int)(cols / kStK);
     const int64_t tiles = (int64_t)wk.tiles_r * wk.tiles_n;
     const int P = mmq_max_clusters();
@@ -1040,9 +1064,9 @@ extern "C" int itq3_mmq_set_trace(void* buf) {
 }
 
 extern "C" int64_t itq3_mmq_ws_nbytes(int64_t rows, int64_t cols, int64_t m) {
-    const int ks = mmq_splits(rows, cols, m);
+    const int BN = mmq_pick_bn(rows, cols, m);
+    const int ks = mmq_splits(rows, cols, m, BN);
     if (ks > 1) return (int64_t)ks * rows * m * (int64_t)sizeof(float);
-    const int BN = itq3_mmq_block_n(m);
     int F, R, kt;
     mmq_tail_plan((int64_t)(mmq_rows_pad(rows) / 256) * ((m + BN - 1) / BN), (int)(cols / kStK), mmq_max_clusters(), true,
                   F, R, kt);
@@ -1057,7 +1081,7 @@ extern "C" int itq3_mmq(const uint8_t* mmq, int64_t rows, int64_t cols, int flag
     }
     cudaStream_t s = (cudaStream_t)stream;
     float* ws = (float*)workspace;
-    const bool n128 = itq3_mmq_block_n(m) == 128;
+    const bool n128 = mmq_pick_bn(rows, cols, m) == 128;
     if (y_dtype == ITQ3_F32)
         return n128 ? launch_mmq<128>(mmq, rows, cols, flags, act, m, (float*)y, stride_r, stride_m, ws, s)
                     : launch_mmq<256>(mmq, rows, cols, flags, act, m, (float*)y, stride_r, stride_m, ws, s);
@@ -1081,7 +1105,7 @@ extern "C" int itq3_mmq_peers(const uint8_t* mmq, int64_t rows, int64_t cols, in
     }
     cudaStream_t s = (cudaStream_t)stream;
     const auto* yp = (const unsigned long long*)d_ypeers;
-    const bool n128 = itq3_mmq_block_n(m) == 128;
+    const bool n128 = mmq_pick_bn(rows, cols, m) == 128;
     // every output row is written once -- by its tile's epilogue, or by the split reduce -- to all peers
     float* ws = (float*)workspace;
     if (y_dtype == ITQ3_F32)
